@@ -1,0 +1,100 @@
+/*
+ * gse_oracle.h -- ORACLE: plain, slow, CPU-only reference of the GSE-SEM method
+ * (arXiv 2411.04686).  TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load this code.  It shares
+ * no code, header, table or constant generator with the CUDA library under
+ * paper_2411_04686_b200/ (which has its own header include/gse.h).
+ *
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n.
+ */
+#ifndef GSE_ORACLE_H
+#define GSE_ORACLE_H
+#include <stdint.h>
+
+#define ORC_OK 0
+#define ORC_NOT_CONVERGED 2
+#define ORC_NUMERICAL_ABORT 3
+#define ORC_ERR_INVALID_ARG 10
+#define ORC_ERR_DIM 11
+#define ORC_ERR_NONFINITE 12
+#define ORC_ERR_NO_VALUES 13
+#define ORC_ERR_UNREPRESENTABLE 14
+#define ORC_ERR_INVALID_EXP_INDEX 15
+
+/* ---- codec (Alg. 1) ---- */
+int orc_exponent_histogram(int64_t nnz, const double* val, uint64_t* hist2048,
+                           int64_t* n_zero, int64_t* first_nonfinite);
+int orc_build_table(const uint64_t* hist2048, int k_max, uint16_t* table, int* table_len);
+int orc_encode_value(double x, const uint16_t* table, int table_len, uint64_t* word, int* ei);
+void orc_segment(uint64_t word, uint16_t* head, uint16_t* tail1, uint32_t* tail2);
+uint64_t orc_assemble(uint16_t head, uint16_t tail1, uint32_t tail2, int level);
+int orc_decode(uint64_t word, int ei, const uint16_t* table, int table_len, double* out);
+int orc_encode_head16_with_ei(double x, const uint16_t* table, int table_len, int ei_bits,
+                              uint16_t* out);
+
+/* ---- CSR conversion ---- */
+int orc_encode_csr(int64_t rows, int64_t cols, int64_t nnz, const int64_t* row_ptr,
+                   const int32_t* col, const double* val, int k_max,
+                   uint16_t* table /* k_max */, int* table_len, int* ei_bits, int* ei_in_column,
+                   uint32_t* col_ei, uint8_t* side_ei, uint16_t* head, uint16_t* tail1,
+                   uint32_t* tail2, int64_t* bad_index);
+
+/* matrix as seen by the oracle solvers: either plain FP64 CSR (val != NULL) or GSE */
+typedef struct {
+  int64_t rows, cols;
+  const int64_t* row_ptr;
+  const int32_t* col;   /* FP64 mode */
+  const double* val;    /* FP64 mode; NULL => GSE mode */
+  const uint32_t* col_ei;
+  const uint8_t* side_ei;
+  int ei_bits, ei_in_column;
+  const uint16_t* head;
+  const uint16_t* tail1;
+  const uint32_t* tail2;
+  const uint16_t* table;
+  int table_len;
+} orc_matrix;
+
+/* ---- SpMV (Alg. 2) ---- */
+int orc_spmv_fp64(int64_t rows, const int64_t* row_ptr, const int32_t* col, const double* val,
+                  const double* x, double* y);
+int orc_spmv_gse(const orc_matrix* A, int level, const double* x, double* y);
+int orc_apply(const orc_matrix* A, int level, const double* x, double* y);
+
+/* ---- residual monitor (Eqs. 3-6) ---- */
+double orc_rsd(const double* w, int64_t t);
+int64_t orc_ndec(const double* w, int64_t t);
+double orc_reldec(const double* w, int64_t t);
+int orc_should_escalate(const double* w, int64_t t, double rsd_limit, int64_t ndec_limit,
+                        double reldec_limit);
+
+typedef struct {
+  int enabled, start_level, max_level;
+  int64_t l, t, m;
+  double rsd_limit;
+  int64_t ndec_limit;
+  double reldec_limit;
+  int verify_at_full;
+  double level_floor[2];
+} orc_schedule;
+
+typedef struct {
+  int64_t iterations, iters_per_level[3];
+  int converged, n_switches;
+  int64_t switch_iter[2];
+  int switch_to_level[2];
+  double rel_residual_recurrence, rel_residual_true;
+  int64_t spmv_count[3];
+} orc_report;
+
+void orc_default_schedule(int solver, orc_schedule* s);
+
+/* ---- solvers ---- */
+int orc_cg(const orc_matrix* A, const double* b, double* x, double tol, int64_t max_iters,
+           const orc_schedule* sched, orc_report* rep);
+int orc_gmres(const orc_matrix* A, const double* b, double* x, double tol, int restart,
+              int64_t max_iters, const orc_schedule* sched, orc_report* rep);
+
+/* cost of the oracle's plain threads knob (GSE_THREADS); returns threads used */
+int orc_set_threads(int n);
+#endif

@@ -1,0 +1,299 @@
+"""Pins of the oracle SpMV, residual monitor and CG / GMRES(30) drivers against what the
+paper and the mathematics fix:
+  * SPEC worked examples (golden file), brute-force dense matvec, exactness of integer /
+    dyadic data, level-3 == FP64 bitwise for d <= 11, head-exact Poisson;
+  * Eq. 3-6 / Conditions 1-3 on hand windows; section 4.4.1 defaults;
+  * CG/GMRES solutions against dense direct solves (numpy.linalg.solve), iteration counts
+    against an independent implementation (scipy.sparse.linalg.cg), Krylov exactness
+    (diagonal matrices), <= n-step convergence on SPD systems.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import gse_inputs as gi
+import oracle as O
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def enc(A, k=8):
+    return O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val, k)
+
+
+def f64(A):
+    return O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+
+
+def bitseq(a, b):
+    return np.array_equal(np.asarray(a).view(np.uint64), np.asarray(b).view(np.uint64))
+
+
+# ------------------------------------------------------------------ SpMV
+@pytest.mark.parametrize("ex", GOLD["spmv"], ids=lambda e: e["cite"])
+def test_spmv_examples(ex):
+    A = gi.from_dense(np.array(ex["dense"]))
+    x = np.array(ex["x"])
+    if "level" not in ex:
+        assert list(O.spmv_fp64(f64(A), x)) == ex["y"]
+    for L in ([ex["level"]] if "level" in ex else [1, 2, 3]):
+        assert list(O.spmv_gse(enc(A), x, L)) == ex["y"]
+
+
+@pytest.mark.parametrize("kind", ["classes", "wide", "mixed"])
+def test_spmv_brute_force_dense(kind):
+    """y = D_L x where D_L is the dense matrix of per-element decoded values."""
+    A = gi.random_csr(40, 37, 6, seed=11, value_kind=kind, empty_rows=0.1)
+    G = enc(A)
+    x = gi.uniform_vec(A.cols, seed=7)
+    for L in (1, 2, 3):
+        dv = O.decode_all(G, L)
+        D = np.zeros((A.rows, A.cols))
+        r = np.repeat(np.arange(A.rows), np.diff(A.row_ptr))
+        D[r, A.col] = dv
+        y = O.spmv_gse(G, x, L)
+        ref = D @ x
+        scale = np.abs(D) @ np.abs(x)
+        assert np.all(np.abs(y - ref) <= 1e-14 * scale + 0.0)
+        assert np.all(y[np.diff(A.row_ptr) == 0] == 0.0)
+
+
+def test_spmv_fp64_brute_force_and_integer_exact():
+    A = gi.random_csr(60, 50, 8, seed=12)
+    x = gi.uniform_vec(A.cols)
+    y = O.spmv_fp64(f64(A), x)
+    scale = np.abs(A.dense()) @ np.abs(x)
+    assert np.all(np.abs(y - A.dense() @ x) <= 1e-14 * scale)
+    B = gi.Csr(A.rows, A.cols, A.row_ptr, A.col, np.round(A.val * 8))
+    xi = np.arange(B.cols, dtype=float) - 20
+    assert np.array_equal(O.spmv_fp64(f64(B), xi), B.dense() @ xi)  # integers: exact
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_spmv_level3_bitwise_equals_fp64_when_d_le_11(seed):
+    """S:296 / S:468: every d <= 11 -> level 3 decode is lossless and the accumulation order
+    is identical, so spmv_gse(3) == spmv_fp64 bitwise."""
+    A = gi.random_csr(100, 100, 7, seed=seed, exps=[1013, 1018, 1022, 1023])
+    G = enc(A)
+    assert max(G.table) - 1013 <= 11
+    x = gi.uniform_vec(A.cols, seed=seed)
+    assert bitseq(O.spmv_gse(G, x, 3), O.spmv_fp64(f64(A), x))
+
+
+@pytest.mark.parametrize("mk", [lambda: gi.poisson2d(32), lambda: gi.poisson3d(12)])
+def test_constant_poisson_exact_in_head(mk):
+    """4/-1 and 6/-1 have <= 2 significant bits at d = 1: all levels bitwise equal FP64."""
+    A = mk()
+    G = enc(A)
+    x = gi.uniform_vec(A.cols)
+    ref = O.spmv_fp64(f64(A), x)
+    for L in (1, 2, 3):
+        assert bitseq(O.spmv_gse(G, x, L), ref)
+
+
+def test_spmv_1x1_head_error_equals_codec_error():
+    """on a 1x1 matrix the head-only SpMV error equals the codec truncation error."""
+    rng = np.random.default_rng(8)
+    for v in rng.uniform(-3, 3, 200):
+        A = gi.from_dense(np.array([[v]]))
+        G = enc(A)
+        w, ei = O.encode_value(v, G.table)
+        h, _, _ = O.segment(w)
+        dec1 = O.decode(O.assemble(h, 0, 0, 1), ei, G.table)
+        assert O.spmv_gse(G, np.array([1.0]), 1)[0] == dec1
+
+
+def test_spmv_level_monotone_error_ones():
+    """with x = 1, max abs error vs FP64 is non-increasing in the level."""
+    A = gi.poisson2d(32, "varcoef")
+    G = enc(A)
+    x = np.ones(A.cols)
+    ref = O.spmv_fp64(f64(A), x)
+    errs = [np.abs(O.spmv_gse(G, x, L) - ref).max() for L in (1, 2, 3)]
+    assert errs[0] >= errs[1] >= errs[2] and errs[0] > 0
+
+
+# ------------------------------------------------------------------ monitor
+def test_monitor_examples():
+    for ex in GOLD["monitor"]["rsd"]:
+        assert O.rsd(ex["window"]) == pytest.approx(ex["value"], abs=1e-15)
+    for ex in GOLD["monitor"]["n_dec"]:
+        assert O.n_dec(ex["window"]) == ex["value"]
+    for ex in GOLD["monitor"]["rel_dec"]:
+        assert O.rel_dec(ex["window"], ex["t"]) == pytest.approx(ex["value"], abs=1e-15)
+
+
+def test_monitor_properties():
+    w = np.array([4.0, 1.0, 3.0, 2.0, 5.0, 0.5])
+    t = w.size - 1
+    # Eq. 3 evaluated from its definition: population std / mean of resid[j-t..j-1]
+    head = w[:t]
+    assert O.rsd(w, t) == pytest.approx(math.sqrt(((head - head.mean()) ** 2).mean()) / head.mean())
+    assert O.rsd(7.5 * w, t) == pytest.approx(O.rsd(w, t))  # scale invariance
+    assert O.n_dec(np.linspace(1, 0.1, 11)) == 10  # strictly decreasing window -> t
+    assert O.n_dec(np.full(11, 0.3)) == 0  # ties score 0 (Eq. 5)
+    assert O.rsd(np.zeros(5)) == 0.0  # avg < 1e-300 guard
+
+
+def test_conditions():
+    t = 10
+    const = np.full(t + 1, 0.2)
+    assert O.should_escalate(const, 0.5, 5, 0.45)  # C3: nDec = 0
+    halving = 0.5 ** np.arange(t + 1)
+    assert not O.should_escalate(halving, 0.5, 5, 0.45)
+    osc = np.array([1.0, 0.05, 1.0, 0.05, 1.0, 0.05, 1.0, 0.05, 1.0, 0.05, 1.0])
+    assert O.rsd(osc, t) > 0.9 and O.n_dec(osc) == 5
+    assert O.should_escalate(osc, 0.5, 6, 0.45)  # C1: RSD > lim and nDec < nDec_lim
+    assert not O.should_escalate(osc, 0.95, 6, -10.0)
+    slow = np.linspace(1.0, 0.9, t + 1)  # nDec = t, relDec = 0.09
+    assert O.should_escalate(slow, 10.0, 5, 0.45)  # C2
+    assert not O.should_escalate(slow, 10.0, 5, 0.05)
+    assert not O.should_escalate(np.zeros(t + 1), 0.5, 5, 0.45)  # zero leading residual
+
+
+def test_defaults_equal_section_4_4_1():
+    d = GOLD["defaults"]
+    for solver in ("cg", "gmres"):
+        s = O.default_schedule(solver)
+        for k in ("l", "t", "m", "ndec_limit"):
+            assert getattr(s, k) == d[solver][k]
+        for k in ("rsd_limit", "reldec_limit"):
+            assert getattr(s, k) == d[solver][k]
+        assert s.enabled == 1 and s.start_level == 1 and s.max_level == 3
+
+
+# ------------------------------------------------------------------ CG
+@pytest.mark.parametrize("ex", GOLD["cg"], ids=lambda e: e["cite"])
+def test_cg_examples(ex):
+    A = gi.from_dense(np.array(ex["dense"]))
+    x, rep = O.cg(f64(A), np.array(ex["b"]), tol=1e-12, max_iters=100)
+    assert rep.converged
+    if "x_num" in ex:
+        want = np.array(ex["x_num"]) / ex["x_den"]
+        assert np.abs(x - want).max() <= 1e-10 and rep.iterations <= ex["max_iters_allowed"]
+    else:
+        assert rep.iterations == ex["iterations"] and np.allclose(x, ex["b"])
+
+
+@pytest.mark.parametrize("n", [5, 17, 40, 64])
+def test_cg_spd_converges_within_3n_and_matches_direct(n):
+    A = gi.spd_small(n, seed=n)
+    b = gi.uniform_vec(n, seed=n)
+    x, rep = O.cg(f64(A), b, tol=1e-12, max_iters=3 * n)
+    assert rep.converged and rep.iterations <= 3 * n
+    xd = np.linalg.solve(A.dense(), b)
+    assert np.abs(x - xd).max() <= 1e-9 * np.abs(xd).max()
+
+
+@pytest.mark.parametrize("N", [8, 16])
+def test_cg_iterations_match_independent_scipy(N):
+    """Iteration count of the oracle's plain CG equals scipy.sparse.linalg.cg (independent
+    implementation, same criterion ||r_k|| <= tol ||b||) within +-1 on 3D Poisson."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+    A = gi.poisson3d(N)
+    b = gi.ones_rhs(A)
+    x, rep = O.cg(f64(A), b, tol=1e-10, max_iters=5000)
+    S = sp.csr_matrix((A.val, A.col, A.row_ptr), shape=(A.rows, A.cols))
+    its = []
+    xs, info = spla.cg(S, b, rtol=1e-10, atol=0.0, maxiter=5000, callback=lambda xk: its.append(1))
+    assert info == 0 and abs(len(its) - rep.iterations) <= 1
+    assert np.abs(x - 1.0).max() < 1e-7  # b = A 1 -> x = 1
+
+
+def test_cg_breakdown_on_indefinite():
+    A = gi.from_dense(np.array([[1.0, 0.0], [0.0, -1.0]]))
+    _, rep = O.cg(f64(A), np.array([1.0, 1.0]), tol=1e-10)
+    assert rep.status == O.NUMERICAL_ABORT
+
+
+def test_cg_zero_rhs():
+    A = gi.poisson2d(4)
+    x, rep = O.cg(f64(A), np.zeros(16), x0=np.ones(16))
+    assert rep.converged and rep.iterations == 0 and np.all(x == 0)
+
+
+# ------------------------------------------------------------------ GMRES
+@pytest.mark.parametrize("ex", GOLD["gmres"], ids=lambda e: e["cite"])
+def test_gmres_examples(ex):
+    A = gi.from_dense(np.array(ex["dense"]))
+    x, rep = O.gmres(f64(A), np.array(ex["b"]), tol=1e-12)
+    assert rep.converged and rep.iterations == ex["iterations"] and np.allclose(x, ex["x"])
+
+
+@pytest.mark.parametrize("k", [1, 3, 7])
+def test_gmres_diagonal_krylov_exactness(k):
+    """diagonal A with k distinct eigenvalues -> converges within k inner steps."""
+    n = 50
+    rng = np.random.default_rng(k)
+    eig = rng.uniform(1, 10, k)[rng.integers(0, k, n)]
+    A = gi.from_dense(np.diag(eig))
+    x, rep = O.gmres(f64(A), rng.uniform(-1, 1, n), tol=1e-12)
+    assert rep.converged and rep.iterations <= k
+
+
+@pytest.mark.parametrize("N", [6, 10])
+def test_gmres_matches_direct_solve(N):
+    A = gi.convdiff3d(N)
+    b = gi.uniform_vec(A.rows, seed=N)
+    x, rep = O.gmres(f64(A), b, tol=1e-11, restart=30)
+    assert rep.converged and rep.rel_residual_true <= 1e-11 * 1.01
+    xd = np.linalg.solve(A.dense(), b)
+    assert np.abs(x - xd).max() <= 1e-8 * np.abs(xd).max()
+
+
+def test_gmres_full_equals_fp64_when_d_le_11():
+    """identical inner-iteration count and bitwise-identical iterate."""
+    A = gi.random_csr(80, 80, 5, seed=3, exps=[1020, 1022, 1023])
+    A = gi.Csr(A.rows, A.cols, A.row_ptr, A.col, A.val)  # add a strong diagonal
+    d = A.dense() + 12 * np.eye(80)
+    A = gi.from_dense(d)
+    b = gi.uniform_vec(80)
+    x1, r1 = O.gmres(f64(A), b, tol=1e-12)
+    x2, r2 = O.gmres(enc(A), b, tol=1e-12, sched=O.fixed_schedule(3))
+    assert r1.iterations == r2.iterations and bitseq(x1, x2)
+
+
+# ------------------------------------------------------------------ stepped driver
+def test_stepped_cg_no_switch_when_head_exact():
+    """Constant Poisson is exact in the head: the stepped solve runs at level 1 only and
+    the level-3 verification (R16) accepts it; iterations equal FP64 CG."""
+    A = gi.poisson3d(10)
+    b = gi.ones_rhs(A)
+    _, r64 = O.cg(f64(A), b, tol=1e-10)
+    x, rep = O.cg(enc(A), b, tol=1e-10, sched=O.schedule("cg"))
+    assert rep.converged and rep.n_switches == 0 and rep.iters_per_level == (r64.iterations, 0, 0)
+    assert rep.rel_residual_true <= 1e-10
+
+
+@pytest.mark.parametrize("solver", ["cg", "gmres"])
+def test_stepped_stall_escalates_and_converges(solver):
+    """head-only truncation stalls above tol -> >= 1 switch, monotone tag, true
+    residual <= tol (scaled schedule l=30, t=10, m=10)."""
+    A = gi.poisson2d(32, "varcoef") if solver == "cg" else gi.convdiff3d(10)
+    b = gi.ones_rhs(A)
+    G = enc(A)
+    s = O.schedule(solver, l=30, t=10, m=10)
+    run = O.cg if solver == "cg" else O.gmres
+    x, rep = run(G, b, tol=1e-10, sched=s)
+    assert rep.converged and rep.n_switches >= 1 and rep.rel_residual_true <= 1e-10
+    assert list(rep.switch_to_level) == sorted(rep.switch_to_level)
+    assert list(rep.switch_iter) == sorted(rep.switch_iter)
+    # without verification the head-only run "converges" on A_1 but not on A (R16)
+    s0 = O.schedule(solver, verify_at_full=0)
+    _, rep0 = run(G, b, tol=1e-10, sched=s0)
+    assert rep0.converged and rep0.n_switches == 0 and rep0.rel_residual_true > 1e-8
+
+
+def test_stepped_forced_escalation_reaches_full():
+    """l=0, m=1, nDec_limit=t+1 -> level 3 within 2 checks."""
+    A = gi.poisson2d(16, "varcoef")
+    b = gi.ones_rhs(A)
+    t = 5
+    s = O.schedule("cg", l=0, t=t, m=1, ndec_limit=t + 1, rsd_limit=-1.0)
+    _, rep = O.cg(enc(A), b, tol=1e-10, sched=s)
+    assert rep.n_switches == 2 and rep.switch_to_level == (2, 3)
+    assert rep.switch_iter == (t + 1, t + 2)
