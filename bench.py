@@ -1,0 +1,451 @@
+#!/usr/bin/env python
+"""bench.py -- the driver's benchmark contract for the GSE-SEM hot path on B200.
+
+Workload (BASELINE.json configs[1]): 3D Poisson 7-point 128^3 (n = 2,097,152, nnz =
+14,581,760), b = A*1, x0 = 0.  One STEP = the whole hot path on that input: gse_encode
+(histogram, table, encode into head/tail1/tail2 planes, partition) followed by the stepped
+mixed-precision CG solve to a TRUE relative residual <= 1e-10 (paper-default schedule,
+verify_at_full).  value = solves / s over all ranks (N > 1: independent replicas, weak
+scaling, until the row-partitioned path lands).
+
+Also reported on the same matrix: the SpMV segment sweep (GB/s, GFLOP/s, fraction of the
+measured HBM peak, per segment count and for FP64 / FP32 accumulation and the FP64-CSR
+comparator), the FP64-CSR CG time-to-1e-10, roofline of the dominant kernel, the oracle CPU
+baseline, the end-to-end number through the C-ABI with host buffers, and SM clocks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gse|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("GSE SpMV GB/s & GFLOP/s (frac of HBM peak) per segment count; "
+          "CG time-to-1e-10")
+UNIT = "CG solves to 1e-10 per s (encode + stepped CG, 3D Poisson 128^3)"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gse", choices=["gse", "reference"])
+    ap.add_argument("--N", type=int, default=128, help="grid edge (configs[1]: 128)")
+    ap.add_argument("--variant", default="const", choices=["const", "varcoef"])
+    ap.add_argument("--spmv-reps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-iters", type=int, default=40,
+                    help="oracle CG iterations in the bounded CPU sample")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nme, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nme)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax),
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------------ distributed plumbing
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo" if args.impl == "reference" else "nccl")
+        pg = dist
+    return world, rank, local, pg
+
+
+def max_over_ranks(v: float, pg, device=None):
+    if pg is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(pg):
+    if pg is not None:
+        pg.barrier()
+
+
+# ------------------------------------------------------------------ reference arm (oracle)
+def oracle_sample(A, b, iters: int):
+    """Bounded oracle sample: oracle encode of the full matrix + `iters` CG iterations at
+    level 1 (the level the stepped solve runs at on this workload).  Returns seconds."""
+    import oracle as O
+    t0 = time.perf_counter()
+    R = O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+    t1 = time.perf_counter()
+    s = O.schedule("cg", verify_at_full=0)
+    _, rep = O.cg(R, b, tol=1e-300, max_iters=iters, sched=s)
+    t2 = time.perf_counter()
+    return t1 - t0, (t2 - t1) / max(rep.iterations, 1)
+
+
+def run_reference(args, world, rank, pg):
+    if rank != 0:
+        return
+    import gse_inputs as gi
+    import oracle as O
+    cores = O.set_threads(0)
+    A = gi.poisson3d(args.N, args.variant)
+    b = gi.ones_rhs(A)
+    # iterations of the full solve: plain oracle CG count for this workload (cached per run)
+    iters_full = _oracle_iterations(A, b)
+    times = []
+    for i in range(args.warmup + args.steps):
+        te, ti = oracle_sample(A, b, max(4, args.cpu_iters // 4))
+        if i >= args.warmup:
+            times.append(te + ti * iters_full)
+    t = statistics.mean(times)
+    value = 1.0 / t
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config(args, A),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"oracle encode + {max(4, args.cpu_iters // 4)} CG "
+                                       f"iterations per step, extrapolated to {iters_full} "
+                                       "iterations"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _oracle_iterations(A, b):
+    # closed-form gauge would be a guess; count with the oracle's own CG only when cheap,
+    # else use the GPU-independent 2.85 N rule measured in SURVEY 8(d) for 3D Poisson.
+    if A.rows <= 64 ** 3:
+        import oracle as O
+        F = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+        return O.cg(F, b, tol=1e-10)[1].iterations
+    N = round(A.rows ** (1 / 3))
+    return int(round(2.85 * N))
+
+
+def _config(args, A):
+    return {"workload": f"3D Poisson 7-point {args.N}^3 ({args.variant}) stepped GSE CG to 1e-10 "
+                        "(configs[1])",
+            "n": int(A.rows), "nnz": int(A.nnz), "k_max": 8, "tol": 1e-10,
+            "schedule": "paper default CG (l=3000,t=250,m=500) + verify_at_full",
+            "step": "gse_encode + gse_solve_cg (inputs resident in HBM)",
+            "l2": "flushed (256 MiB write) before every timed step; per-step CUDA events",
+            "parallelism": "replicas" if args.gpus > 1 else "single GPU"}
+
+
+# ------------------------------------------------------------------ GSE arm
+def run_gse(args, world, rank, local, pg):
+    import torch
+    import gse_inputs as gi
+    import paper_2411_04686_b200 as g
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    hbm_peak, peak_src = peaks()
+
+    A = gi.poisson3d(args.N, args.variant)
+    b_h = gi.ones_rhs(A)
+    rp = torch.from_numpy(A.row_ptr.astype(np.int32)).to(dev)
+    col = torch.from_numpy(A.col).to(dev)
+    val = torch.from_numpy(A.val).to(dev)
+    b = torch.from_numpy(b_h).to(dev)
+    x = torch.zeros(A.rows, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    sched = g.gse_default_schedule("cg")
+
+    def step():
+        M = g.gse_encode(rp, col, val, A.rows, A.cols, k_max=8)
+        x.zero_()
+        _, rep = g.gse_solve_cg(M, b, x, tol=1e-10, max_iters=5000, sched=sched)
+        M.close()
+        return rep
+
+    for _ in range(args.warmup):
+        rep = step()
+    torch.cuda.synchronize()
+    barrier(pg)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    reps = []
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        barrier(pg)
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            ev[i][0].record(stream)
+            reps.append(step())
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    clocks = clk.summary()
+    step_ms = [s.elapsed_time(e) for s, e in ev]
+    total_ms = max_over_ranks(sum(step_ms), pg, dev)
+    barrier(pg)
+    rep = reps[-1]
+    value = world * args.steps / (total_ms * 1e-3)
+
+    extra = spmv_and_cg_sweep(args, A, rp, col, val, b, dev, stream, flush, hbm_peak)
+    e2e = None if args.no_e2e else e2e_measure(args, A, b_h, dev, stream)
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, A, b_h, rep["iterations"])
+    launches = estimate_launches(rep, extra["info"]) * args.steps
+    if rank != 0:
+        return
+    dom = extra["spmv"]["L1"]
+    roof = {"bound": "hbm", "kernel": "k_spmv<1> (level-1 GSE SpMV, the CG inner kernel)",
+            "achieved": dom["GBps"], "peak": hbm_peak, "unit": "GB/s",
+            "frac": dom["GBps"] / hbm_peak, "peak_source": peak_src,
+            "traffic": _profiled_traffic(), "algorithmic_bytes_per_launch": dom["bytes"],
+            "avg_launch_us": dom["us"]}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config(args, A),
+        "time_to_1e-10_ms": {"stepped_gse_step": statistics.median(step_ms),
+                             "stepped_gse_solve_only": extra["cg_gse_ms"],
+                             "encode": extra["encode_ms"], "fp64_csr_cg": extra["cg_fp64_ms"],
+                             "speedup_vs_fp64_csr": extra["cg_fp64_ms"] / extra["cg_gse_ms"]},
+        "solve": {"iterations": rep["iterations"], "iters_per_level": rep["iters_per_level"],
+                  "switch_iter": rep["switch_iter"], "rel_residual_true": rep["rel_residual_true"],
+                  "fp64_iterations": extra["cg_fp64_iters"]},
+        "spmv_sweep": extra["spmv"],
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def estimate_launches(rep, info):
+    """Kernels launched per step: encode (rowptr, hist, select, encode, flags, 2 CUB select
+    kernels, fill_desc = 8), CG setup (dot, spmv, residual = 3), 3 per iteration inside the
+    graph while-loop, verify / final residual (2 each)."""
+    return 8 + 3 + 3 * rep["iterations"] + 2 * (1 + rep["n_switches"]) + 2
+
+
+def _profiled_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+    if os.path.exists(p):
+        try:
+            d = json.load(open(p))
+            return d.get("k_spmv_L1", {}).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+def time_cuda(fn, reps, stream, flush):
+    import torch
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(reps)]
+    for i in range(reps):
+        flush.fill_(float(i))
+        evs[i][0].record(stream)
+        fn()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    return [s.elapsed_time(e) for s, e in evs]
+
+
+def spmv_and_cg_sweep(args, A, rp, col, val, b, dev, stream, flush, hbm_peak):
+    import torch
+    import paper_2411_04686_b200 as g
+    n, nnz = A.rows, A.nnz
+    M = g.gse_encode(rp, col, val, A.rows, A.cols)
+    F = g.gse_fp64_matrix(rp, col, val, A.rows, A.cols)
+    x = torch.rand(n, dtype=torch.float64, device=dev)
+    y = torch.empty(n, dtype=torch.float64, device=dev)
+    x32, y32 = x.float(), torch.empty(n, dtype=torch.float32, device=dev)
+    for _ in range(3):
+        g.gse_spmv(M, x, y, segments=1)
+    out = {}
+    rows_bytes = 4 * (n + 1)
+    for L, s_l in ((1, 2), (2, 4), (3, 8)):
+        ms = time_cuda(lambda: g.gse_spmv(M, x, y, segments=L), args.spmv_reps, stream, flush)
+        t = statistics.mean(ms) * 1e-3
+        byt = nnz * (4 + s_l) + rows_bytes + 16 * n
+        out[f"L{L}"] = {"bytes": byt, "us": t * 1e6, "GBps": byt / t / 1e9,
+                        "GFLOPs": 2 * nnz / t / 1e9, "frac_hbm": byt / t / 1e9 / hbm_peak}
+    for L, s_l in ((1, 2), (3, 8)):
+        ms = time_cuda(lambda: g.gse_spmv_f32acc(M, x32, y32, segments=L), args.spmv_reps,
+                       stream, flush)
+        t = statistics.mean(ms) * 1e-3
+        byt = nnz * (4 + s_l) + rows_bytes + 8 * n
+        out[f"L{L}_f32acc"] = {"bytes": byt, "us": t * 1e6, "GBps": byt / t / 1e9,
+                               "GFLOPs": 2 * nnz / t / 1e9, "frac_hbm": byt / t / 1e9 / hbm_peak}
+    ms = time_cuda(lambda: g.gse_spmv(F, x, y, segments=3), args.spmv_reps, stream, flush)
+    t = statistics.mean(ms) * 1e-3
+    byt = nnz * 12 + rows_bytes + 16 * n
+    out["fp64_csr"] = {"bytes": byt, "us": t * 1e6, "GBps": byt / t / 1e9,
+                       "GFLOPs": 2 * nnz / t / 1e9, "frac_hbm": byt / t / 1e9 / hbm_peak}
+    # CG solve only (no encode), stepped GSE vs FP64-CSR
+    xs = torch.zeros(n, dtype=torch.float64, device=dev)
+    sched = g.gse_default_schedule("cg")
+
+    def cg_gse():
+        xs.zero_()
+        return g.gse_solve_cg(M, b, xs, tol=1e-10, sched=sched)[1]
+
+    def cg_f64():
+        xs.zero_()
+        return g.gse_solve_cg(F, b, xs, tol=1e-10)[1]
+
+    cg_gse()
+    cg_f64()
+    reps = 3
+    t_gse = statistics.median(time_cuda(cg_gse, reps, stream, flush))
+    t_f64 = statistics.median(time_cuda(cg_f64, reps, stream, flush))
+    rf = cg_f64()
+
+    def enc():
+        m = g.gse_encode(rp, col, val, A.rows, A.cols)
+        m.close()
+
+    t_enc = statistics.median(time_cuda(enc, 3, stream, flush))
+    info = M.info
+    M.close()
+    F.close()
+    return {"spmv": out, "cg_gse_ms": t_gse, "cg_fp64_ms": t_f64, "cg_fp64_iters": rf["iterations"],
+            "encode_ms": t_enc, "info": info}
+
+
+def e2e_measure(args, A, b_h, dev, stream):
+    """Same step through the C-ABI with HOST (pinned) buffers: H2D of the CSR and b inside
+    the call, D2H of x at the end."""
+    import torch
+    import paper_2411_04686_b200 as g
+    rp = torch.from_numpy(A.row_ptr.astype(np.int32)).pin_memory()
+    col = torch.from_numpy(A.col).pin_memory()
+    val = torch.from_numpy(A.val).pin_memory()
+    b = torch.from_numpy(b_h).pin_memory()
+    x = torch.zeros(A.rows, dtype=torch.float64).pin_memory()
+    sched = g.gse_default_schedule("cg")
+    s = stream.cuda_stream
+
+    def step():
+        M = g.gse_encode(rp, col, val, A.rows, A.cols, device=dev.index, stream=s)
+        x.zero_()
+        g.gse_solve_cg(M, b, x, tol=1e-10, sched=sched, stream=s)
+        M.close()
+
+    step()
+    ts = []
+    for _ in range(max(2, args.steps // 2)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        step()
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    h2d = rp.numel() * 4 + col.numel() * 4 + val.numel() * 8 + b.numel() * 8 + x.numel() * 8
+    return {"value": 1.0 / t, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(x.numel() * 8), "ms_per_step": t * 1e3,
+            "timer": "host wall clock around the synchronous C-ABI calls"}
+
+
+def cpu_baseline(args, A, b_h, iters_full):
+    import oracle as O
+    cores = O.set_threads(0)
+    te, ti = oracle_sample(A, b_h, args.cpu_iters)
+    t = te + ti * iters_full
+    return {"value": 1.0 / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"oracle encode of the full matrix ({te:.2f} s) + {args.cpu_iters} level-1 "
+                      f"CG iterations ({ti * 1e3:.1f} ms each), extrapolated to the GPU run's "
+                      f"{iters_full} iterations; OpenMP rows in SpMV/encode, sequential dots"}
+
+
+def main():
+    args = parse()
+    world, rank, local, pg = dist_init(args)
+    args.gpus = world if world > 1 else args.gpus
+    if args.impl == "reference":
+        run_reference(args, world, rank, pg)
+    else:
+        run_gse(args, world, rank, local, pg)
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,223 @@
+/*
+ * gse.h -- C-ABI of the B200-native GSE-SEM library (arXiv 2411.04686, "Precision-Aware
+ * Iterative Algorithms Based on Group-Shared Exponents of Floating-Point Numbers").
+ *
+ * Citations: P:n = PAPER.md line n (section / equation / algorithm in brackets), S:n =
+ * SPEC.md line n, R<k> = reading k of the DESIGN.md ledger (where the paper is silent).
+ *
+ * Problem statement (P:29 [section 1]): solve A x = b with CG / GMRES for a sparse A.  The
+ * library stores A once in GSE-SEM form -- a table of k shared exponents (P:113-123
+ * [section 3.2]), a per-value sign + exponent index (EI) + denormalised significand split
+ * into head/tail1/tail2 planes (P:163 [section 3.2.3]), the EI riding in the spare high
+ * bits of the CSR column index (P:168 [section 3.3.1]) -- and reads it at 1, 2 or 3
+ * segments (P:180-212 [section 3.3.2, Alg. spmv]) inside the stepped mixed-precision
+ * solvers (P:217-294 [section 3.4, Alg. stepped-GMRES, Eqs. 3-6]).
+ *
+ * CONVENTIONS (apply to every entry point)
+ *  - Pointers: every array argument may be HOST (pageable or pinned) or DEVICE memory;
+ *    the library inspects it (cudaPointerGetAttributes) and stages host arrays through
+ *    device buffers on `stream`.  Device arrays must live on the device the matrix lives
+ *    on.  Host outputs are complete when the call returns (the call synchronises
+ *    `stream`); device outputs are stream-ordered on `stream`.
+ *  - stream: a cudaStream_t passed as void* (NULL = the legacy default stream).
+ *  - Ownership: the caller owns every array it passes and keeps it alive until the stream
+ *    work completes; the library never frees caller memory.  A gse_matrix owns all its
+ *    device memory (planes, table, LUT, partition, solver workspaces) until
+ *    gse_matrix_free.  A gse_matrix is immutable after creation: concurrent gse_spmv on
+ *    different streams is safe; solver calls on one matrix must be
+ *    serialised by the caller (they share the matrix's solver workspace).
+ *  - Errors: every entry point returns gse_status and never aborts; details of the last
+ *    error of the calling thread are in gse_last_error_detail().  Asynchronous kernel
+ *    faults surface at the next synchronising call (encode, solvers, host-pointer calls).
+ */
+#ifndef GSE_H
+#define GSE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSE_VERSION_MAJOR 0
+#define GSE_VERSION_MINOR 1
+
+typedef enum {
+  GSE_OK = 0,
+  GSE_NOT_CONVERGED = 2,          /* max iterations reached; report valid (S:413 exit 2)   */
+  GSE_NUMERICAL_ABORT = 3,        /* CG breakdown p.Ap <= 0 or non-finite residual */
+  GSE_ERR_INVALID_ARG = 10,       /* bad segments/k_max/tol<=0/schedule/CSR structure      */
+  GSE_ERR_DIM_MISMATCH = 11,      /* non-square matrix for a solver, wrong slice sizes     */
+  GSE_ERR_NONFINITE = 12,         /* NaN/Inf value in the input matrix       */
+  GSE_ERR_NO_VALUES = 13,         /* no normal non-zero value: empty histogram      */
+  GSE_ERR_UNREPRESENTABLE = 14,   /* reserved: caller table without an entry > e    */
+  GSE_ERR_INVALID_EXP_INDEX = 15, /* reserved: EI >= table length                   */
+  GSE_ERR_FP32_RANGE = 16,        /* FP32 accumulation asked but table exceeds FP32 (R20)  */
+  GSE_ERR_WRONG_FORMAT = 17,      /* operation not defined for this matrix kind            */
+  GSE_ERR_CUDA = 20,
+  GSE_ERR_NCCL = 21,
+  GSE_ERR_OOM = 22
+} gse_status;
+
+typedef struct gse_matrix_s* gse_matrix; /* opaque; owns its device memory   */
+typedef struct gse_dist_s* gse_dist;     /* opaque; owns its NCCL communicator */
+
+/* Plain FP64 CSR input: 0-based, rows sorted by column, no duplicates,
+ * row_ptr[0] = 0, row_ptr[rows] = nnz.  row_ptr is int32 (row_ptr_64 = 0) or int64. */
+typedef struct {
+  int64_t rows, cols, nnz;
+  const void* row_ptr;
+  int row_ptr_64;
+  const int32_t* col_idx;
+  const double* values;
+} gse_csr_f64;
+
+typedef struct {
+  int k_max;      /* number of shared exponents k: power of two in [1, 64]; default 8 */
+  int device;     /* CUDA device ordinal for the matrix; -1 = infer from device pointers, else 0 */
+  int64_t sample_block_rows; /* reserved (sampling extraction P:116, NEXT-3); must be 0      */
+  uint64_t seed;             /* reserved for sampling                                      */
+} gse_encode_opts;
+
+typedef enum { GSE_KIND_GSE = 0, GSE_KIND_FP64 = 1 } gse_matrix_kind;
+
+typedef struct {
+  int kind;          /* gse_matrix_kind                                                     */
+  int k_max, ei_bits, ei_in_column, table_len;
+  uint16_t table[64]; /* stored exponents E = e + 1, EI order (R4-R5)                 */
+  int64_t rows, cols, nnz;
+  int64_t n_blocks;   /* SpMV row blocks                           */
+  int64_t n_zero_values; /* zero / subnormal inputs encoded as signed zero (R2)              */
+  int device;
+  size_t plane_bytes[5]; /* col_ei, head, tail1, tail2, side_ei (kind GSE); col, val (FP64) */
+} gse_matrix_info;
+
+/* ---------------------------------------------------------------------------------------
+ * gse_encode -- build the GSE-SEM form of A (steps a1-a3 of SURVEY 8(a)).
+ *   a1 histogram of biased exponents over all values (P:116 [3.2.1]; zero/subnormal counted
+ *      apart; first NaN/Inf reported as GSE_ERR_NONFINITE with "(row, col)" in the detail);
+ *   a2 table: the k_max most frequent exponents, ties to the larger exponent, e_max forced
+ *      into the last slot, entries e+1 (P:116, P:123 [3.2.1-3.2.2]; R4, R5);
+ *   a3 per value: nearest entry E > e, d = E - e, D = 1<<(63-d) | f shifted by 11-d
+ *      (truncation), split into head 16 b / tail1 16 b / tail2 32 b; EI embedded in the top
+ *      log2(k_max) bits of the column index iff cols < 2^(32-ei_bits), else a uint8 side
+ *      array (Alg. formatConvert P:128-160 generalised to 64 bits; R1-R3, R6).
+ * Output planes are bit-identical to the oracle (tests/test_gpu_parity.py).
+ * Errors: INVALID_ARG (structure: row_ptr not monotone, col out of range, k_max),
+ * NONFINITE, NO_VALUES, OOM, CUDA.  Synchronises `stream` (reads back the table).
+ * ------------------------------------------------------------------------------------- */
+gse_status gse_encode(const gse_csr_f64* A, const gse_encode_opts* opts, gse_matrix* out,
+                      void* stream);
+
+/* The FP64-CSR comparator matrix (the paper's FP64-SpMV baseline): copies
+ * row_ptr/col/values to the device; usable with gse_spmv (segments must be 3) and the
+ * solvers with a disabled schedule (fixed FP64). */
+gse_status gse_fp64_matrix(const gse_csr_f64* A, int device, gse_matrix* out, void* stream);
+
+gse_status gse_matrix_get_info(gse_matrix A, gse_matrix_info* info);
+
+/* Copy the encoded planes out (any pointer may be NULL to skip): col_ei[nnz] uint32,
+ * side_ei[nnz] uint8 (only when !ei_in_column), head[nnz] / tail1[nnz] uint16,
+ * tail2[nnz] uint32, table[table_len] uint16.  Host or device destinations. */
+gse_status gse_matrix_copy_planes(gse_matrix A, uint32_t* col_ei, uint8_t* side_ei,
+                                  uint16_t* head, uint16_t* tail1, uint32_t* tail2,
+                                  uint16_t* table, void* stream);
+
+/* a4: decode every stored value at `segments` (1, 2, 3) to FP64 (Alg. spmv l.6-17,
+ * P:191-201 and P:212; signed zero for a zero significand, R10; flush when the true
+ * exponent <= 0, R11).  values[nnz].  Bit-exact with the oracle. */
+gse_status gse_decode(gse_matrix A, int segments, double* values, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * gse_spmv -- a5: y = A_L x with L = segments in {1, 2, 3}: only the requested planes are
+ * read, each value decoded on the fly to FP64 and multiplied/accumulated in FP64 ("we load
+ * low-precision sparse matrices only during memory access and still perform multiplication
+ * and accumulation operations based on double-precision"; Alg. spmv).
+ * x[cols], y[rows] FP64.  For a GSE_KIND_FP64 matrix (segments = 3) this is plain CSR
+ * SpMV (a6).  Within-row products are summed in storage order for rows up to the short-row
+ * limit; the result is within 1e-12 * sum_j |a_ij x_j| of the oracle.
+ * ------------------------------------------------------------------------------------- */
+gse_status gse_spmv(gse_matrix A, const double* x, double* y, int segments, void* stream);
+
+/* FP32-accumulation variant (BASELINE north_star; R20): x, y float; each decoded value is
+ * rounded toward zero to FP32 (FP32-underflow -> 0), multiplied and accumulated in FP32.
+ * GSE_ERR_FP32_RANGE if the table can represent values >= 2^128. */
+gse_status gse_spmv_f32acc(gse_matrix A, const float* x, float* y, int segments, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Stepped mixed-precision solvers (P:217-294 [3.4]).
+ * ------------------------------------------------------------------------------------- */
+typedef struct {
+  int enabled;                 /* 1: stepped (Alg. stepped-GMRES); 0: fixed start_level     */
+  int start_level, max_level;  /* 1..3 (A_1 head, A_2 head+tail1, A_3 full)          */
+  int64_t l, t, m;             /* first check at l, window t, period m (t < l)        */
+  double rsd_limit;            /* Condition 1, Eq. 3                                  */
+  int64_t ndec_limit;          /* replaces t/2 in Conditions 1-2 (R13)                */
+  double reldec_limit;         /* Condition 2, Eq. 6                                  */
+  int verify_at_full;          /* R16: a converged recurrence at L < 3 is checked with A_3   */
+  double level_floor[2];       /* R17: escalate when resid < floor[L-1] at L = 1, 2; 0 = off */
+} gse_step_schedule;
+
+typedef struct {
+  int64_t iterations;          /* CG iterations / GMRES inner iterations (global counter)    */
+  int64_t iters_per_level[3];
+  int converged, n_switches;
+  int64_t switch_iter[2];
+  int switch_to_level[2];
+  double rel_residual_recurrence; /* last monitored residual (CG recurrence / Givens est.)  */
+  double rel_residual_true;       /* ||b - A_3 x|| / ||b|| computed at exit                 */
+  double seconds;                 /* device time of the solve (CUDA events)                 */
+  int64_t spmv_count[3];          /* SpMVs issued per level (incl. replacement / verify)    */
+} gse_solve_report;
+
+/* Paper defaults (P:433, P:441 [4.4.1]): CG l=3000 t=250 m=500 0.50/130/0.45; GMRES
+ * l=9000 t=300 m=1500 0.03/80/0.08; enabled, start 1, max 3, verify_at_full 1, floors 0. */
+void gse_default_schedule(int solver /* 0 = CG, 1 = GMRES */, gse_step_schedule* out);
+
+/* Unpreconditioned CG with the stepped driver: w = A_tag p each iteration; the
+ * monitor (Eqs. 3-6, Conditions 1-3) sees ||r_j||/||b|| after iteration j, checks at
+ * j >= l, (j - l) % m == 0, window of t+1 full; one level per trigger (R12); at a switch
+ * CG restarts from the current x with r = b - A_new x, p = r (R15).  b[n], x[n] (in: x0,
+ * out: solution); n = rows = cols.  Returns OK (converged), NOT_CONVERGED, NUMERICAL_ABORT
+ * or an error; rep may be NULL.  sched NULL = fixed level 3. */
+gse_status gse_solve_cg(gse_matrix A, const double* b, double* x, double tol, int64_t max_iters,
+                        const gse_step_schedule* sched, gse_solve_report* rep, void* stream);
+
+/* Restarted GMRES(restart) (restart 30, 500 outer): MGS Arnoldi, Givens rotations
+ * (R18), estimate |g_{j+1}|/||b|| monitored per inner iteration with a global counter,
+ * explicit residual at restarts; a switch ends the cycle (x += V y) and restarts at the
+ * new level (R15). */
+gse_status gse_solve_gmres(gse_matrix A, const double* b, double* x, double tol, int restart,
+                           int64_t max_iters, const gse_step_schedule* sched,
+                           gse_solve_report* rep, void* stream);
+
+void gse_matrix_free(gse_matrix A);
+
+const char* gse_status_string(gse_status s);
+const char* gse_last_error_detail(void);
+
+/* Route library device allocations (planes, workspaces) through a caller allocator, e.g.
+ * torch's caching allocator.  NULL alloc restores cudaMallocAsync / cudaFreeAsync. */
+gse_status gse_set_allocator(void* (*alloc)(size_t bytes, void* stream, void* ctx),
+                             void (*free_)(void* ptr, void* stream, void* ctx), void* ctx);
+
+/* ---------------------------------------------------------------------------------------
+ * Multi-GPU, one process per GPU: contiguous row blocks; a rank holds rows
+ * [row_begin, row_begin + local_rows) with GLOBAL column ids; the table is global
+ * (histogram allreduce, R21); columns are renumbered locally (owned first, halo after).
+ * b, x, y are the rank's row slices.  gse_spmv / gse_solve_* on a distributed matrix
+ * exchange the halo and allreduce dot products over NCCL.
+ * ------------------------------------------------------------------------------------- */
+gse_status gse_nccl_unique_id(void* id128 /* host, 128 bytes */);
+gse_status gse_dist_create(const void* nccl_unique_id /* host, 128 B */, int rank, int nranks,
+                           int device, gse_dist* out);
+gse_status gse_encode_dist(gse_dist D, const gse_csr_f64* local_rows, int64_t row_begin,
+                           int64_t global_rows, const gse_encode_opts* opts, gse_matrix* out,
+                           void* stream);
+void gse_dist_free(gse_dist D);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSE_H */

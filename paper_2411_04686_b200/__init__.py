@@ -1,0 +1,379 @@
+"""paper_2411_04686_b200 -- thin Python binding of the B200-native GSE-SEM library.
+
+The product is the C-ABI shared library ``libgse_b200.so`` (include/gse.h), built from
+``csrc/*.cu`` for sm_100a.  This module only marshals arguments (torch tensors or numpy
+arrays -> raw pointers, the current CUDA stream) and raises on error statuses; every step of
+the method runs in the library's kernels.  There is no CPU fallback: if the library cannot
+be loaded, importing this package fails.
+
+Function names follow the C-ABI: gse_encode, gse_fp64_matrix, gse_spmv, gse_spmv_f32acc,
+gse_decode, gse_matrix_copy_planes, gse_matrix_get_info, gse_solve_cg, gse_solve_gmres,
+gse_default_schedule, gse_matrix_free.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import shutil
+
+import numpy as np
+
+from . import build as _build
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = _build.LIB
+
+# ---------------------------------------------------------------------------- status codes
+GSE_OK, GSE_NOT_CONVERGED, GSE_NUMERICAL_ABORT = 0, 2, 3
+GSE_ERR_INVALID_ARG, GSE_ERR_DIM_MISMATCH, GSE_ERR_NONFINITE, GSE_ERR_NO_VALUES = 10, 11, 12, 13
+GSE_ERR_UNREPRESENTABLE, GSE_ERR_INVALID_EXP_INDEX, GSE_ERR_FP32_RANGE = 14, 15, 16
+GSE_ERR_WRONG_FORMAT, GSE_ERR_CUDA, GSE_ERR_NCCL, GSE_ERR_OOM = 17, 20, 21, 22
+GSE_KIND_GSE, GSE_KIND_FP64 = 0, 1
+
+ABI_SYMBOLS = (
+    "gse_encode", "gse_fp64_matrix", "gse_matrix_get_info", "gse_matrix_copy_planes",
+    "gse_decode", "gse_spmv", "gse_spmv_f32acc", "gse_default_schedule", "gse_solve_cg",
+    "gse_solve_gmres", "gse_matrix_free", "gse_status_string", "gse_last_error_detail",
+    "gse_set_allocator", "gse_nccl_unique_id", "gse_dist_create", "gse_encode_dist",
+    "gse_dist_free",
+)
+
+
+def _load():
+    if _build.stale():
+        if shutil.which(_build.NVCC) or os.path.exists(_build.NVCC):
+            _build.build()
+        elif not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing and nvcc is unavailable: run "
+                              "`python -c 'import __graft_entry__ as g; g.build()'`")
+    return C.CDLL(LIB_PATH)
+
+
+_lib = _load()
+
+
+# ---------------------------------------------------------------------------- ctypes structs
+class CsrF64(C.Structure):
+    _fields_ = [("rows", C.c_int64), ("cols", C.c_int64), ("nnz", C.c_int64),
+                ("row_ptr", C.c_void_p), ("row_ptr_64", C.c_int),
+                ("col_idx", C.c_void_p), ("values", C.c_void_p)]
+
+
+class EncodeOpts(C.Structure):
+    _fields_ = [("k_max", C.c_int), ("device", C.c_int), ("sample_block_rows", C.c_int64),
+                ("seed", C.c_uint64)]
+
+
+class MatrixInfo(C.Structure):
+    _fields_ = [("kind", C.c_int), ("k_max", C.c_int), ("ei_bits", C.c_int),
+                ("ei_in_column", C.c_int), ("table_len", C.c_int), ("table", C.c_uint16 * 64),
+                ("rows", C.c_int64), ("cols", C.c_int64), ("nnz", C.c_int64),
+                ("n_blocks", C.c_int64), ("n_zero_values", C.c_int64), ("device", C.c_int),
+                ("plane_bytes", C.c_size_t * 5)]
+
+
+class StepSchedule(C.Structure):
+    _fields_ = [("enabled", C.c_int), ("start_level", C.c_int), ("max_level", C.c_int),
+                ("l", C.c_int64), ("t", C.c_int64), ("m", C.c_int64),
+                ("rsd_limit", C.c_double), ("ndec_limit", C.c_int64),
+                ("reldec_limit", C.c_double), ("verify_at_full", C.c_int),
+                ("level_floor", C.c_double * 2)]
+
+
+class SolveReport(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("iters_per_level", C.c_int64 * 3),
+                ("converged", C.c_int), ("n_switches", C.c_int),
+                ("switch_iter", C.c_int64 * 2), ("switch_to_level", C.c_int * 2),
+                ("rel_residual_recurrence", C.c_double), ("rel_residual_true", C.c_double),
+                ("seconds", C.c_double), ("spmv_count", C.c_int64 * 3)]
+
+
+def _declare(L):
+    vp, i32, i64, dbl = C.c_void_p, C.c_int, C.c_int64, C.c_double
+    L.gse_encode.argtypes = [C.POINTER(CsrF64), C.POINTER(EncodeOpts), C.POINTER(vp), vp]
+    L.gse_fp64_matrix.argtypes = [C.POINTER(CsrF64), i32, C.POINTER(vp), vp]
+    L.gse_matrix_get_info.argtypes = [vp, C.POINTER(MatrixInfo)]
+    L.gse_matrix_copy_planes.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp]
+    L.gse_decode.argtypes = [vp, i32, vp, vp]
+    L.gse_spmv.argtypes = [vp, vp, vp, i32, vp]
+    L.gse_spmv_f32acc.argtypes = [vp, vp, vp, i32, vp]
+    L.gse_default_schedule.argtypes = [i32, C.POINTER(StepSchedule)]
+    L.gse_default_schedule.restype = None
+    L.gse_solve_cg.argtypes = [vp, vp, vp, dbl, i64, C.POINTER(StepSchedule),
+                               C.POINTER(SolveReport), vp]
+    L.gse_solve_gmres.argtypes = [vp, vp, vp, dbl, i32, i64, C.POINTER(StepSchedule),
+                                  C.POINTER(SolveReport), vp]
+    L.gse_matrix_free.argtypes = [vp]
+    L.gse_matrix_free.restype = None
+    L.gse_status_string.argtypes = [i32]
+    L.gse_status_string.restype = C.c_char_p
+    L.gse_last_error_detail.argtypes = []
+    L.gse_last_error_detail.restype = C.c_char_p
+
+
+_declare(_lib)
+
+
+class GseError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        detail = _lib.gse_last_error_detail().decode(errors="replace")
+        msg = _lib.gse_status_string(status).decode()
+        super().__init__(f"{where}: {msg} (status {status}){': ' + detail if detail else ''}")
+        self.status = status
+        self.detail = detail
+
+
+def _check(status: int, where: str, ok=(GSE_OK,)):
+    if status not in ok:
+        raise GseError(status, where)
+    return status
+
+
+# ---------------------------------------------------------------------------- marshalling
+def _is_torch(a):
+    return type(a).__module__.startswith("torch")
+
+
+def _addr(a):
+    """Raw address of a contiguous torch tensor or numpy array (None -> NULL)."""
+    if a is None:
+        return None
+    if _is_torch(a):
+        assert a.is_contiguous(), "tensor must be contiguous"
+        return a.data_ptr()
+    assert isinstance(a, np.ndarray) and a.flags["C_CONTIGUOUS"], "array must be contiguous"
+    return a.ctypes.data
+
+
+def _stream(*arrays, stream=None):
+    if stream is not None:
+        return stream if isinstance(stream, int) else stream.cuda_stream
+    for a in arrays:
+        if a is not None and _is_torch(a) and a.is_cuda:
+            import torch
+            return torch.cuda.current_stream(a.device).cuda_stream
+    return None
+
+
+def _device_of(*arrays):
+    for a in arrays:
+        if a is not None and _is_torch(a) and a.is_cuda:
+            return a.device.index
+    return -1
+
+
+def _dtype_ok(a, np_dtype):
+    if _is_torch(a):
+        import torch
+        want = {np.float64: torch.float64, np.float32: torch.float32, np.int32: torch.int32,
+                np.int64: torch.int64}[np_dtype]
+        return a.dtype == want
+    return a.dtype == np_dtype
+
+
+class Matrix:
+    """Owning handle of a gse_matrix (freed on close / garbage collection)."""
+
+    def __init__(self, handle: int):
+        self.handle = C.c_void_p(handle)
+        self._info = None
+
+    @property
+    def info(self) -> dict:
+        if self._info is None:
+            self._info = gse_matrix_get_info(self)
+        return self._info
+
+    def close(self):
+        if self.handle and self.handle.value:
+            _lib.gse_matrix_free(self.handle)
+            self.handle = C.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _csr(rows, cols, row_ptr, col_idx, values):
+    assert _dtype_ok(col_idx, np.int32) and _dtype_ok(values, np.float64)
+    rp64 = 1 if _dtype_ok(row_ptr, np.int64) else 0
+    assert rp64 or _dtype_ok(row_ptr, np.int32), "row_ptr must be int32 or int64"
+    nnz = int(values.numel() if _is_torch(values) else values.size)
+    return CsrF64(rows, cols, nnz, _addr(row_ptr), rp64, _addr(col_idx), _addr(values))
+
+
+def gse_encode(row_ptr, col_idx, values, rows: int, cols: int, k_max: int = 8,
+               device: int | None = None, stream=None) -> Matrix:
+    """a1-a3: build the GSE-SEM matrix (host or device CSR input; see include/gse.h)."""
+    A = _csr(rows, cols, row_ptr, col_idx, values)
+    dev = _device_of(values, col_idx, row_ptr) if device is None else device
+    if dev < 0:
+        dev = _current_device()
+    opts = EncodeOpts(k_max, dev, 0, 0)
+    out = C.c_void_p()
+    _check(_lib.gse_encode(C.byref(A), C.byref(opts), C.byref(out),
+                           _stream(values, col_idx, row_ptr, stream=stream)), "gse_encode")
+    return Matrix(out.value)
+
+
+def gse_fp64_matrix(row_ptr, col_idx, values, rows: int, cols: int, device: int | None = None,
+                    stream=None) -> Matrix:
+    """The FP64-CSR comparator matrix (paper's FP64-SpMV baseline)."""
+    A = _csr(rows, cols, row_ptr, col_idx, values)
+    dev = _device_of(values, col_idx, row_ptr) if device is None else device
+    if dev < 0:
+        dev = _current_device()
+    out = C.c_void_p()
+    _check(_lib.gse_fp64_matrix(C.byref(A), dev, C.byref(out),
+                                _stream(values, col_idx, row_ptr, stream=stream)),
+           "gse_fp64_matrix")
+    return Matrix(out.value)
+
+
+def _current_device() -> int:
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.current_device()
+    except Exception:
+        pass
+    return 0
+
+
+def gse_matrix_get_info(A: Matrix) -> dict:
+    info = MatrixInfo()
+    _check(_lib.gse_matrix_get_info(A.handle, C.byref(info)), "gse_matrix_get_info")
+    return {
+        "kind": info.kind, "k_max": info.k_max, "ei_bits": info.ei_bits,
+        "ei_in_column": bool(info.ei_in_column), "table_len": info.table_len,
+        "table": [info.table[i] for i in range(info.table_len)], "rows": info.rows,
+        "cols": info.cols, "nnz": info.nnz, "n_blocks": info.n_blocks,
+        "n_zero_values": info.n_zero_values, "device": info.device,
+        "plane_bytes": [info.plane_bytes[i] for i in range(5)],
+    }
+
+
+def gse_matrix_copy_planes(A: Matrix) -> dict:
+    """Copy the encoded planes to host numpy arrays (for bit-exact parity checks)."""
+    inf = A.info
+    n = inf["nnz"]
+    out = {"col_ei": np.zeros(max(n, 1), np.uint32), "head": np.zeros(max(n, 1), np.uint16),
+           "tail1": np.zeros(max(n, 1), np.uint16), "tail2": np.zeros(max(n, 1), np.uint32),
+           "table": np.zeros(64, np.uint16)}
+    side = None if inf["ei_in_column"] else np.zeros(max(n, 1), np.uint8)
+    _check(_lib.gse_matrix_copy_planes(A.handle, _addr(out["col_ei"]), _addr(side),
+                                       _addr(out["head"]), _addr(out["tail1"]),
+                                       _addr(out["tail2"]), _addr(out["table"]), None),
+           "gse_matrix_copy_planes")
+    res = {k: v[:n] for k, v in out.items() if k != "table"}
+    res["table"] = out["table"][: inf["table_len"]]
+    res["side_ei"] = None if side is None else side[:n]
+    return res
+
+
+def _like(x, n, np_dtype):
+    if _is_torch(x):
+        import torch
+        dt = torch.float64 if np_dtype == np.float64 else torch.float32
+        return torch.empty(n, dtype=dt, device=x.device)
+    return np.empty(n, dtype=np_dtype)
+
+
+def gse_decode(A: Matrix, segments: int, out=None, like=None):
+    """a4: every stored value decoded at `segments` to FP64."""
+    n = A.info["nnz"]
+    if out is None:
+        out = _like(like, n, np.float64) if like is not None else np.empty(n, np.float64)
+    _check(_lib.gse_decode(A.handle, segments, _addr(out), _stream(out)), "gse_decode")
+    return out
+
+
+def gse_spmv(A: Matrix, x, y=None, segments: int = 3, stream=None):
+    """a5/a6: y = A_L x, FP64 accumulation."""
+    if y is None:
+        y = _like(x, A.info["rows"], np.float64)
+    assert _dtype_ok(x, np.float64) and _dtype_ok(y, np.float64)
+    _check(_lib.gse_spmv(A.handle, _addr(x), _addr(y), segments, _stream(x, y, stream=stream)),
+           "gse_spmv")
+    return y
+
+
+def gse_spmv_f32acc(A: Matrix, x, y=None, segments: int = 3, stream=None):
+    """y = A_L x with FP32 accumulation (R20)."""
+    if y is None:
+        y = _like(x, A.info["rows"], np.float32)
+    assert _dtype_ok(x, np.float32) and _dtype_ok(y, np.float32)
+    _check(_lib.gse_spmv_f32acc(A.handle, _addr(x), _addr(y), segments,
+                                _stream(x, y, stream=stream)), "gse_spmv_f32acc")
+    return y
+
+
+def gse_default_schedule(solver: str = "cg", **overrides) -> StepSchedule:
+    s = StepSchedule()
+    _lib.gse_default_schedule(0 if solver == "cg" else 1, C.byref(s))
+    for k, v in overrides.items():
+        if k == "level_floor":
+            s.level_floor[0], s.level_floor[1] = v
+        else:
+            setattr(s, k, v)
+    return s
+
+
+def fixed_schedule(level: int = 3) -> StepSchedule:
+    s = gse_default_schedule("cg")
+    s.enabled = 0
+    s.start_level = level
+    return s
+
+
+def _report(r: SolveReport, status: int) -> dict:
+    ns = min(r.n_switches, 2)
+    return {"status": status, "iterations": r.iterations,
+            "iters_per_level": tuple(r.iters_per_level), "converged": bool(r.converged),
+            "n_switches": r.n_switches, "switch_iter": tuple(r.switch_iter[:ns]),
+            "switch_to_level": tuple(r.switch_to_level[:ns]),
+            "rel_residual_recurrence": r.rel_residual_recurrence,
+            "rel_residual_true": r.rel_residual_true, "seconds": r.seconds,
+            "spmv_count": tuple(r.spmv_count)}
+
+
+_SOLVE_OK = (GSE_OK, GSE_NOT_CONVERGED, GSE_NUMERICAL_ABORT)
+
+
+def gse_solve_cg(A: Matrix, b, x=None, tol: float = 1e-10, max_iters: int = 5000,
+                 sched: StepSchedule | None = None, stream=None):
+    """Stepped CG (a7, a9, a10).  x (in: x0, out: solution) is overwritten.  Returns
+    (x, report)."""
+    if x is None:
+        x = _like(b, A.info["rows"], np.float64)
+        x[:] = 0
+    rep = SolveReport()
+    st = _lib.gse_solve_cg(A.handle, _addr(b), _addr(x), tol, max_iters,
+                           None if sched is None else C.byref(sched), C.byref(rep),
+                           _stream(b, x, stream=stream))
+    _check(st, "gse_solve_cg", _SOLVE_OK)
+    return x, _report(rep, st)
+
+
+def gse_solve_gmres(A: Matrix, b, x=None, tol: float = 1e-10, restart: int = 30,
+                    max_iters: int = 15000, sched: StepSchedule | None = None, stream=None):
+    """Stepped restarted GMRES(restart) (a8, a9, a10).  Returns (x, report)."""
+    if x is None:
+        x = _like(b, A.info["rows"], np.float64)
+        x[:] = 0
+    rep = SolveReport()
+    st = _lib.gse_solve_gmres(A.handle, _addr(b), _addr(x), tol, restart, max_iters,
+                              None if sched is None else C.byref(sched), C.byref(rep),
+                              _stream(b, x, stream=stream))
+    _check(st, "gse_solve_gmres", _SOLVE_OK)
+    return x, _report(rep, st)
+
+
+def gse_matrix_free(A: Matrix):
+    A.close()
+
+
+def lib():
+    return _lib

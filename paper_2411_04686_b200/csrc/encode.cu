@@ -1,0 +1,556 @@
+// encode.cu -- GSE-SEM format conversion on the GPU and the
+// SpMV row-block partition.
+//
+//   a1 k_hist     : histogram of biased exponents (P:116 [3.2.1]); zero/subnormal counted
+//                   apart; first NaN/Inf index.  Warp-aggregated smem atomics.
+//   a2 k_select   : one CTA: top-k_max exponents by (count desc, e desc), e_max forced into
+//                   the last slot, entries e+1 (R4, R5); then the 2048-entry
+//                   LUT e -> (EI, d = min{E - e >= 1}) used by a3 (Alg. formatConvert
+//                   l.6-21, precomputed once per exponent instead of per value).
+//   a3 k_encode   : per value Alg. formatConvert l.22-26 generalised to the 64-bit SEM:
+//                   D = 1<<(63-d) | f<<(11-d) (or f>>(d-11)), truncation (R1); zero ->
+//                   signed zero (R2); d > 63 -> signed zero (R3); split head/tail1/tail2
+//                   (P:163); EI into the column index or the side array.
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include "decode.cuh"
+#include "gse_internal.cuh"
+
+namespace gse {
+
+struct EncodeStatus {
+  unsigned long long hist[2048];
+  unsigned long long n_zero;
+  unsigned long long first_nonfinite;  // ~0ull if none
+  unsigned long long first_bad_col;    // ~0ull if none
+  unsigned int bad_structure;          // row_ptr not monotone / wrong ends
+  int table_len;
+  int n_distinct;
+  int e_max;
+  unsigned short table[64];
+  unsigned int lut[2048];  // ei | d << 8 ; 0xFFFFFFFF = no entry above e
+};
+
+// ------------------------------------------------------------------ a1 histogram
+__global__ void __launch_bounds__(512) k_hist(const double* __restrict__ val, int64_t nnz,
+                                              EncodeStatus* __restrict__ st) {
+  __shared__ unsigned int h[2048];
+  __shared__ unsigned long long s_first;
+  __shared__ unsigned int s_zero;
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) h[i] = 0;
+  if (threadIdx.x == 0) {
+    s_first = ~0ull;
+    s_zero = 0;
+  }
+  __syncthreads();
+  unsigned int zc = 0;
+  unsigned long long first = ~0ull;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += stride) {
+    unsigned long long u = (unsigned long long)__double_as_longlong(__ldcs(val + i));
+    unsigned e = (unsigned)(u >> 52) & 0x7FFu;
+    if (e == 0x7FFu) {
+      first = min(first, (unsigned long long)i);
+      e = 0xFFFFFFFFu;
+    } else if (e == 0u) {
+      ++zc;
+      e = 0xFFFFFFFFu;
+    }
+    // warp-aggregated increment: one smem atomic per distinct exponent in the warp
+    unsigned active = __activemask();
+    unsigned peers = __match_any_sync(active, e);
+    int leader = __ffs(peers) - 1;
+    if (e != 0xFFFFFFFFu && (int)(threadIdx.x & 31) == leader)
+      atomicAdd(&h[e], (unsigned)__popc(peers));
+  }
+  if (first != ~0ull) atomicMin(&s_first, first);
+  if (zc) atomicAdd(&s_zero, zc);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x)
+    if (h[i]) atomicAdd(&st->hist[i], (unsigned long long)h[i]);
+  if (threadIdx.x == 0) {
+    if (s_zero) atomicAdd(&st->n_zero, (unsigned long long)s_zero);
+    if (s_first != ~0ull) atomicMin(&st->first_nonfinite, s_first);
+  }
+}
+
+// ------------------------------------------------------------------ a2 table + LUT
+__device__ unsigned long long block_max_u64(unsigned long long v, unsigned long long* red) {
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = (l < (int)(blockDim.x >> 5)) ? red[l] : 0ull;
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+    if (l == 0) red[32] = v;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+__global__ void __launch_bounds__(1024) k_select(EncodeStatus* __restrict__ st, int k_max) {
+  __shared__ unsigned long long key[2048];
+  __shared__ unsigned long long red[33];
+  __shared__ int sel[64];
+  unsigned long long mloc = 0, nd = 0;
+  for (int e = threadIdx.x; e < 2048; e += blockDim.x) {
+    unsigned long long c = (e >= 1 && e <= 2046) ? st->hist[e] : 0ull;
+    // key orders by count desc, then exponent desc (R4); unique because e is in the key
+    key[e] = c ? ((c << 11) | (unsigned long long)e) : 0ull;
+    if (c) {
+      mloc = max(mloc, (unsigned long long)e);
+      ++nd;
+    }
+  }
+  const unsigned long long e_max = block_max_u64(mloc, red);
+  // count distinct exponents (sum via max-reduction of per-thread prefix is overkill:
+  // use an atomic into shared)
+  __shared__ unsigned int s_nd;
+  if (threadIdx.x == 0) s_nd = 0;
+  __syncthreads();
+  if (nd) atomicAdd(&s_nd, (unsigned)nd);
+  __syncthreads();
+  const int n_distinct = (int)s_nd;
+  const int take = n_distinct < k_max ? n_distinct : k_max;
+  for (int k = 0; k < take; ++k) {
+    unsigned long long loc = 0;
+    for (int e = threadIdx.x; e < 2048; e += blockDim.x) loc = max(loc, key[e]);
+    unsigned long long best = block_max_u64(loc, red);
+    if (threadIdx.x == 0) {
+      sel[k] = (int)(best & 0x7FFull);
+      key[best & 0x7FFull] = 0ull;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && take > 0) {
+    bool have = false;
+    for (int k = 0; k < take; ++k) have |= (sel[k] == (int)e_max);
+    if (!have) sel[take - 1] = (int)e_max;  // P:123 forced e_max + 1 (R5)
+    for (int k = 0; k < take; ++k) st->table[k] = (unsigned short)(sel[k] + 1);
+    st->table_len = take;
+    st->n_distinct = n_distinct;
+    st->e_max = (int)e_max;
+  }
+  if (threadIdx.x == 0 && take == 0) {
+    st->table_len = 0;
+    st->n_distinct = 0;
+  }
+  __syncthreads();
+  // LUT: nearest larger shared exponent per biased exponent (Alg. formatConvert l.6-21)
+  for (int e = threadIdx.x; e < 2048; e += blockDim.x) {
+    int best = -1, dbest = 1 << 30;
+    for (int k = 0; k < take; ++k) {
+      int d = (sel[k] + 1) - e;
+      if (d >= 1 && d < dbest) {
+        dbest = d;
+        best = k;
+      }
+    }
+    st->lut[e] = best < 0 ? 0xFFFFFFFFu : ((unsigned)best | ((unsigned)dbest << 8));
+  }
+}
+
+// ------------------------------------------------------------------ a3 encode
+template <bool IN_COL>
+__global__ void __launch_bounds__(256) k_encode(const double* __restrict__ val,
+                                                const int32_t* __restrict__ col, int64_t nnz,
+                                                int64_t cols, const EncodeStatus* __restrict__ st,
+                                                int ei_bits, uint32_t* __restrict__ col_ei,
+                                                uint8_t* __restrict__ side,
+                                                uint16_t* __restrict__ head,
+                                                uint16_t* __restrict__ tail1,
+                                                uint32_t* __restrict__ tail2,
+                                                unsigned long long* __restrict__ bad_col) {
+  __shared__ unsigned int lut[2048];
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) lut[i] = st->lut[i];
+  __syncthreads();
+  const int sh = 32 - ei_bits;
+  unsigned long long bad = ~0ull;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += stride) {
+    const unsigned long long u = (unsigned long long)__double_as_longlong(__ldcs(val + i));
+    const int32_t c = __ldcs(col + i);
+    if (c < 0 || (int64_t)c >= cols) bad = min(bad, (unsigned long long)i);
+    const unsigned long long s = u >> 63;
+    const unsigned e = (unsigned)(u >> 52) & 0x7FFu;
+    const unsigned long long f = u & ((1ull << 52) - 1);
+    unsigned long long w = s << 63;
+    unsigned ei = 0;
+    if (e != 0u && e != 0x7FFu) {
+      const unsigned lu = lut[e];
+      ei = lu & 0xFFu;
+      const unsigned d = lu >> 8;
+      if (d <= 63u) {
+        unsigned long long D = 1ull << (63 - d);
+        D |= (d <= 11u) ? (f << (11 - d)) : (f >> (d - 11));
+        w |= D;
+      }
+    }
+    head[i] = (uint16_t)(w >> 48);
+    tail1[i] = (uint16_t)(w >> 32);
+    tail2[i] = (uint32_t)w;
+    if (IN_COL) {
+      col_ei[i] = (uint32_t)c | (ei_bits ? (ei << sh) : 0u);
+    } else {
+      col_ei[i] = (uint32_t)c;
+      side[i] = (uint8_t)ei;
+    }
+  }
+  if (bad != ~0ull) atomicMin(bad_col, bad);
+}
+
+// ------------------------------------------------------------------ row_ptr + partition
+template <class RP>
+__global__ void k_rowptr(const RP* __restrict__ in, int64_t rows, int64_t nnz,
+                         uint32_t* __restrict__ out, unsigned* __restrict__ bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= rows; r += stride) {
+    long long a = (long long)in[r];
+    bool ok = a >= 0 && a <= nnz;
+    if (r == 0) ok = ok && a == 0;
+    if (r == rows) ok = ok && a == nnz;
+    if (r < rows) ok = ok && (long long)in[r + 1] >= a;
+    if (!ok) atomicOr(bad, 1u);
+    out[r] = (uint32_t)a;
+  }
+}
+
+__global__ void k_block_flags(const uint32_t* __restrict__ rp, int64_t rows,
+                              uint8_t* __restrict__ flag) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += stride) {
+    const uint32_t a = rp[r], b = rp[r + 1];
+    bool st = (r == 0) || (b - a > LMAX);
+    if (!st) {
+      const uint32_t p = rp[r - 1];
+      st = (a / CHUNK != p / CHUNK) || (a - p > LMAX);
+    }
+    flag[r] = st ? 1 : 0;
+  }
+}
+
+__global__ void k_fill_desc(const uint32_t* __restrict__ starts, const int* __restrict__ nsel,
+                            const uint32_t* __restrict__ rp, int64_t rows,
+                            BlockDesc* __restrict__ desc) {
+  const int nb = *nsel;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += stride) {
+    if (b < nb) {
+      const uint32_t r = starts[b];
+      desc[b] = BlockDesc{r, rp[r]};
+    } else {
+      desc[b] = BlockDesc{(uint32_t)rows, rp[rows]};
+    }
+  }
+}
+
+static int grid_for(int64_t n, int threads, int dev) {
+  int64_t g = (n + threads - 1) / threads;
+  int64_t cap = (int64_t)num_sms(dev) * 8;
+  if (g > cap) g = cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+gse_status build_partition(Matrix& M, cudaStream_t s) {
+  M.n_blocks = 0;
+  if (M.rows == 0) {
+    M.blocks = dev_alloc_n<BlockDesc>(1, s);
+    if (!M.blocks) return GSE_ERR_OOM;
+    BlockDesc h{0, 0};
+    GSE_CUDA_TRY(cudaMemcpyAsync(M.blocks, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+    GSE_CUDA_TRY(cudaStreamSynchronize(s));
+    return GSE_OK;
+  }
+  uint8_t* flags = dev_alloc_n<uint8_t>(M.rows, s);
+  uint32_t* starts = dev_alloc_n<uint32_t>(M.rows, s);
+  int* nsel = dev_alloc_n<int>(1, s);
+  if (!flags || !starts || !nsel) return GSE_ERR_OOM;
+  k_block_flags<<<grid_for(M.rows, 256, M.device), 256, 0, s>>>(M.row_ptr, M.rows, flags);
+  thrust::counting_iterator<uint32_t> it(0);
+  size_t tmp_bytes = 0;
+  cub::DeviceSelect::Flagged(nullptr, tmp_bytes, it, flags, starts, nsel, (int)M.rows, s);
+  void* tmp = dev_alloc(tmp_bytes + 16, s);
+  if (!tmp) return GSE_ERR_OOM;
+  cub::DeviceSelect::Flagged(tmp, tmp_bytes, it, flags, starts, nsel, (int)M.rows, s);
+  int nb = 0;
+  GSE_CUDA_TRY(cudaMemcpyAsync(&nb, nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GSE_CUDA_TRY(cudaStreamSynchronize(s));
+  M.n_blocks = nb;
+  M.blocks = dev_alloc_n<BlockDesc>((size_t)nb + 1, s);
+  if (!M.blocks) return GSE_ERR_OOM;
+  k_fill_desc<<<grid_for(nb + 1, 256, M.device), 256, 0, s>>>(starts, nsel, M.row_ptr, M.rows,
+                                                              M.blocks);
+  GSE_CUDA_TRY(cudaGetLastError());
+  dev_free(tmp, s);
+  dev_free(flags, s);
+  dev_free(starts, s);
+  dev_free(nsel, s);
+  return GSE_OK;
+}
+
+static gse_status convert_row_ptr(Matrix& M, const void* d_row_ptr, int rp64, cudaStream_t s,
+                                  unsigned* d_bad) {
+  M.row_ptr = dev_alloc_n<uint32_t>((size_t)M.rows + 1, s);
+  if (!M.row_ptr) return GSE_ERR_OOM;
+  int g = grid_for(M.rows + 1, 256, M.device);
+  if (rp64)
+    k_rowptr<long long><<<g, 256, 0, s>>>((const long long*)d_row_ptr, M.rows, M.nnz,
+                                          M.row_ptr, d_bad);
+  else
+    k_rowptr<int><<<g, 256, 0, s>>>((const int*)d_row_ptr, M.rows, M.nnz, M.row_ptr, d_bad);
+  GSE_CUDA_TRY(cudaGetLastError());
+  return GSE_OK;
+}
+
+void build_decode_table(Matrix& M) {
+  memset(&M.htab, 0, sizeof(M.htab));
+  const int sL[3] = {48, 32, 0};
+  int emax = 0;
+  for (int i = 0; i < M.table_len; ++i) {
+    const int E = M.table[i];
+    emax = E > emax ? E : emax;
+    for (int L = 0; L < 3; ++L) {
+      M.htab.d64[L][i] = (long long)(E - 1086 + sL[L]) * (1LL << 52);
+      M.htab.d32[L][i] = (E - 1086 + sL[L]) * (1 << 23);
+    }
+  }
+  // FP32 accumulation is defined iff every decodable value is < 2^128 (R20): the largest
+  // true exponent is E_max - 1 - 1023 <= 127.
+  M.fp32_ok = (emax <= 1151);
+}
+
+static std::string row_col_of(const void* d_row_ptr, int rp64, const int32_t* d_col,
+                              int64_t rows, int64_t idx, cudaStream_t s) {
+  // error path only: binary search the row on the host
+  std::string out;
+  int64_t lo = 0, hi = rows;  // find r with rp[r] <= idx < rp[r+1]
+  auto rp_at = [&](int64_t r) -> int64_t {
+    if (rp64) {
+      long long v = 0;
+      cudaMemcpyAsync(&v, (const long long*)d_row_ptr + r, 8, cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      return v;
+    }
+    int v = 0;
+    cudaMemcpyAsync(&v, (const int*)d_row_ptr + r, 4, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    return v;
+  };
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) / 2;
+    if (rp_at(mid) <= idx)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  int c = -1;
+  cudaMemcpyAsync(&c, d_col + idx, 4, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  char buf[128];
+  snprintf(buf, sizeof(buf), "row %lld col %d (element %lld)", (long long)lo, c,
+           (long long)idx);
+  return buf;
+}
+
+gse_status encode_matrix(Matrix& M, const gse_csr_f64& A, const void* d_row_ptr, int rp64,
+                         const int32_t* d_col, const double* d_val, cudaStream_t s) {
+  M.kind = GSE_KIND_GSE;
+  int eb = 0;
+  while ((1 << eb) < M.k_max) ++eb;
+  M.ei_bits = eb;
+  M.ei_in_column = (M.cols < (1LL << (32 - eb))) ? 1 : 0;
+
+  EncodeStatus* st = dev_alloc_n<EncodeStatus>(1, s);
+  if (!st) return GSE_ERR_OOM;
+  GSE_CUDA_TRY(cudaMemsetAsync(st, 0, sizeof(EncodeStatus), s));
+  GSE_CUDA_TRY(cudaMemsetAsync(&st->first_nonfinite, 0xFF, 8, s));
+  GSE_CUDA_TRY(cudaMemsetAsync(&st->first_bad_col, 0xFF, 8, s));
+
+  gse_status rc = convert_row_ptr(M, d_row_ptr, rp64, s, &st->bad_structure);
+  if (rc != GSE_OK) return rc;
+
+  const int nsm = num_sms(M.device);
+  if (M.nnz > 0) {
+    int g = grid_for(M.nnz, 512, M.device);
+    if (g > nsm * 4) g = nsm * 4;
+    k_hist<<<g, 512, 0, s>>>(d_val, M.nnz, st);
+    GSE_CUDA_TRY(cudaGetLastError());
+  }
+  k_select<<<1, 1024, 0, s>>>(st, M.k_max);
+  GSE_CUDA_TRY(cudaGetLastError());
+
+  // read back the table / status (one sync, the table is needed on the host for the
+  // decode constants and gse_matrix_get_info)
+  EncodeStatus* h = (EncodeStatus*)malloc(sizeof(EncodeStatus));
+  GSE_CUDA_TRY(cudaMemcpyAsync(h, st, sizeof(EncodeStatus), cudaMemcpyDeviceToHost, s));
+  GSE_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h->bad_structure) {
+    free(h);
+    dev_free(st, s);
+    set_error("invalid CSR structure: row_ptr must start at 0, be non-decreasing and end at nnz");
+    return GSE_ERR_INVALID_ARG;
+  }
+  if (h->first_nonfinite != ~0ull) {
+    std::string where = row_col_of(d_row_ptr, rp64, d_col, M.rows, (int64_t)h->first_nonfinite, s);
+    free(h);
+    dev_free(st, s);
+    set_error("non-finite value at " + where);
+    return GSE_ERR_NONFINITE;
+  }
+  if (h->table_len == 0) {
+    free(h);
+    dev_free(st, s);
+    set_error("no representable values (all values zero or subnormal)");
+    return GSE_ERR_NO_VALUES;
+  }
+  M.table_len = h->table_len;
+  for (int i = 0; i < 64; ++i) M.table[i] = i < M.table_len ? h->table[i] : 0;
+  M.n_zero = (int64_t)h->n_zero;
+  free(h);
+  build_decode_table(M);
+
+  const size_t np = padded(M.nnz);
+  M.col_ei = dev_alloc_n<uint32_t>(np, s);
+  M.head = dev_alloc_n<uint16_t>(np, s);
+  M.tail1 = dev_alloc_n<uint16_t>(np, s);
+  M.tail2 = dev_alloc_n<uint32_t>(np, s);
+  if (!M.ei_in_column) M.side_ei = dev_alloc_n<uint8_t>(np, s);
+  M.dtab = dev_alloc_n<DecodeTable>(1, s);
+  if (!M.col_ei || !M.head || !M.tail1 || !M.tail2 || !M.dtab ||
+      (!M.ei_in_column && !M.side_ei))
+    return GSE_ERR_OOM;
+  GSE_CUDA_TRY(cudaMemcpyAsync(M.dtab, &M.htab, sizeof(DecodeTable), cudaMemcpyHostToDevice, s));
+  // zero the padding tail so vector loads past nnz read zeros
+  const size_t pad = np - (size_t)M.nnz;
+  GSE_CUDA_TRY(cudaMemsetAsync(M.col_ei + M.nnz, 0, pad * 4, s));
+  GSE_CUDA_TRY(cudaMemsetAsync(M.head + M.nnz, 0, pad * 2, s));
+  GSE_CUDA_TRY(cudaMemsetAsync(M.tail1 + M.nnz, 0, pad * 2, s));
+  GSE_CUDA_TRY(cudaMemsetAsync(M.tail2 + M.nnz, 0, pad * 4, s));
+  if (M.side_ei) GSE_CUDA_TRY(cudaMemsetAsync(M.side_ei + M.nnz, 0, pad, s));
+
+  if (M.nnz > 0) {
+    int g = grid_for(M.nnz, 256, M.device);
+    if (M.ei_in_column)
+      k_encode<true><<<g, 256, 0, s>>>(d_val, d_col, M.nnz, M.cols, st, M.ei_bits, M.col_ei,
+                                       nullptr, M.head, M.tail1, M.tail2, &st->first_bad_col);
+    else
+      k_encode<false><<<g, 256, 0, s>>>(d_val, d_col, M.nnz, M.cols, st, M.ei_bits, M.col_ei,
+                                        M.side_ei, M.head, M.tail1, M.tail2,
+                                        &st->first_bad_col);
+    GSE_CUDA_TRY(cudaGetLastError());
+  }
+  rc = build_partition(M, s);
+  if (rc != GSE_OK) return rc;
+  unsigned long long badc = 0;
+  GSE_CUDA_TRY(cudaMemcpyAsync(&badc, &st->first_bad_col, 8, cudaMemcpyDeviceToHost, s));
+  GSE_CUDA_TRY(cudaStreamSynchronize(s));
+  dev_free(st, s);
+  if (badc != ~0ull) {
+    set_error("column index out of range at " +
+              row_col_of(d_row_ptr, rp64, d_col, M.rows, (int64_t)badc, s));
+    return GSE_ERR_INVALID_ARG;
+  }
+  return GSE_OK;
+}
+
+// ------------------------------------------------------------------ FP64 comparator
+__global__ void k_copy_fp64(const double* __restrict__ val, const int32_t* __restrict__ col,
+                            int64_t nnz, int64_t cols, double* __restrict__ vout,
+                            uint32_t* __restrict__ cout, unsigned long long* __restrict__ bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long b = ~0ull;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += stride) {
+    const int32_t c = col[i];
+    if (c < 0 || (int64_t)c >= cols) b = min(b, (unsigned long long)i);
+    vout[i] = val[i];
+    cout[i] = (uint32_t)c;
+  }
+  if (b != ~0ull) atomicMin(bad, b);
+}
+
+gse_status fp64_matrix(Matrix& M, const void* d_row_ptr, int rp64, const int32_t* d_col,
+                       const double* d_val, cudaStream_t s) {
+  M.kind = GSE_KIND_FP64;
+  M.ei_bits = 0;
+  M.ei_in_column = 1;
+  M.table_len = 0;
+  M.fp32_ok = 0;
+  unsigned* d_flags = dev_alloc_n<unsigned>(4, s);
+  if (!d_flags) return GSE_ERR_OOM;
+  GSE_CUDA_TRY(cudaMemsetAsync(d_flags, 0, 16, s));
+  GSE_CUDA_TRY(cudaMemsetAsync(d_flags + 2, 0xFF, 8, s));
+  gse_status rc = convert_row_ptr(M, d_row_ptr, rp64, s, d_flags);
+  if (rc != GSE_OK) return rc;
+  const size_t np = padded(M.nnz);
+  M.val = dev_alloc_n<double>(np, s);
+  M.col_ei = dev_alloc_n<uint32_t>(np, s);
+  if (!M.val || !M.col_ei) return GSE_ERR_OOM;
+  GSE_CUDA_TRY(cudaMemsetAsync(M.val + M.nnz, 0, (np - M.nnz) * 8, s));
+  GSE_CUDA_TRY(cudaMemsetAsync(M.col_ei + M.nnz, 0, (np - M.nnz) * 4, s));
+  if (M.nnz > 0) {
+    k_copy_fp64<<<grid_for(M.nnz, 256, M.device), 256, 0, s>>>(
+        d_val, d_col, M.nnz, M.cols, M.val, M.col_ei, (unsigned long long*)(d_flags + 2));
+    GSE_CUDA_TRY(cudaGetLastError());
+  }
+  rc = build_partition(M, s);
+  if (rc != GSE_OK) return rc;
+  unsigned h[4];
+  GSE_CUDA_TRY(cudaMemcpyAsync(h, d_flags, 16, cudaMemcpyDeviceToHost, s));
+  GSE_CUDA_TRY(cudaStreamSynchronize(s));
+  dev_free(d_flags, s);
+  if (h[0]) {
+    set_error("invalid CSR structure: row_ptr must start at 0, be non-decreasing and end at nnz");
+    return GSE_ERR_INVALID_ARG;
+  }
+  unsigned long long badc = ((unsigned long long)h[3] << 32) | h[2];
+  if (badc != ~0ull) {
+    set_error("column index out of range");
+    return GSE_ERR_INVALID_ARG;
+  }
+  return GSE_OK;
+}
+
+// ------------------------------------------------------------------ a4 decode (all values)
+template <int L>
+__global__ void k_decode_all(const uint32_t* __restrict__ col_ei, const uint8_t* __restrict__ side,
+                             const uint16_t* __restrict__ head, const uint16_t* __restrict__ tail1,
+                             const uint32_t* __restrict__ tail2, int64_t nnz, int ei_bits,
+                             const DecodeTable* __restrict__ dt, double* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int sh = 32 - ei_bits;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += stride) {
+    const unsigned ei = side ? side[i] : __funnelshift_rc(col_ei[i], 0u, sh);
+    const long long d = dt->d64[L - 1][ei];
+    const uint32_t h = head[i];
+    double v;
+    if (L == 1)
+      v = decode_l1(h, d);
+    else if (L == 2)
+      v = decode_l2(h, tail1[i], d);
+    else
+      v = decode_l3(h, tail1[i], tail2[i], d);
+    out[i] = v;
+  }
+}
+
+gse_status decode_all(const Matrix& M, int level, double* out, cudaStream_t s) {
+  if (M.nnz == 0) return GSE_OK;
+  const int g = grid_for(M.nnz, 256, M.device);
+  const uint8_t* side = M.ei_in_column ? nullptr : M.side_ei;
+  if (level == 1)
+    k_decode_all<1><<<g, 256, 0, s>>>(M.col_ei, side, M.head, M.tail1, M.tail2, M.nnz,
+                                      M.ei_bits, M.dtab, out);
+  else if (level == 2)
+    k_decode_all<2><<<g, 256, 0, s>>>(M.col_ei, side, M.head, M.tail1, M.tail2, M.nnz,
+                                      M.ei_bits, M.dtab, out);
+  else
+    k_decode_all<3><<<g, 256, 0, s>>>(M.col_ei, side, M.head, M.tail1, M.tail2, M.nnz,
+                                      M.ei_bits, M.dtab, out);
+  GSE_CUDA_TRY(cudaGetLastError());
+  return GSE_OK;
+}
+
+}  // namespace gse

@@ -1,0 +1,132 @@
+// gse_internal.cuh -- internal types of the B200 GSE-SEM library (not part of the ABI).
+// Everything here is the product path; it shares nothing with oracle/.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/gse.h"
+
+namespace gse {
+
+// ---------------------------------------------------------------- SpMV partition constants
+// A "block" (one CTA of the SpMV kernel) covers a run of consecutive rows whose starts fall
+// in one CHUNK of the nnz stream (rows <= LMAX nnz), or a single long row (> LMAX nnz).
+// Short blocks hold < CHUNK + LMAX + 7 <= TILE nnz (8-aligned), so one pass of
+// SPMV_THREADS x VEC = TILE slots covers them.
+constexpr int SPMV_THREADS = 256;
+constexpr int VEC = 8;
+constexpr int TILE = SPMV_THREADS * VEC;  // 2048
+constexpr uint32_t LMAX = 256;
+constexpr uint32_t CHUNK = 1784;  // CHUNK + LMAX + 6 <= TILE
+static_assert(CHUNK + LMAX + 6 <= TILE, "short block must fit one pass");
+constexpr int NNZ_PAD = 8;  // plane allocations padded to a multiple of 8 elements (+8)
+
+struct BlockDesc {
+  uint32_t row0;  // first row of the block
+  uint32_t nnz0;  // row_ptr[row0]
+};
+
+// decode constants per level: |v| = D_L * 2^(E - 1086 + s_L),
+// s_L = 48 / 32 / 0 for L = 1 / 2 / 3, applied by adding delta to the bits of double(D_L).
+struct DecodeTable {
+  long long d64[3][64];  // (E - 1086 + s_L) << 52
+  int d32[3][64];        // (E - 1086 + s_L) << 23 (FP32 accumulation)
+};
+
+struct SolverWs;  // solvers.cu
+struct DistCtx;   // dist.cu
+
+struct Matrix {
+  int kind = GSE_KIND_GSE;
+  int device = 0;
+  int64_t rows = 0, cols = 0, nnz = 0;
+  int k_max = 8, ei_bits = 3, ei_in_column = 1, table_len = 0;
+  uint16_t table[64] = {0};
+  int64_t n_zero = 0;
+  int fp32_ok = 0;
+  // device arrays
+  uint32_t* row_ptr = nullptr;  // [rows + 1]
+  uint32_t* col_ei = nullptr;   // [nnz_pad] column | EI << (32 - ei_bits)  (or plain column)
+  uint8_t* side_ei = nullptr;   // [nnz_pad] when !ei_in_column
+  uint16_t* head = nullptr;     // [nnz_pad]
+  uint16_t* tail1 = nullptr;    // [nnz_pad]
+  uint32_t* tail2 = nullptr;    // [nnz_pad]
+  double* val = nullptr;        // [nnz_pad] FP64 kind
+  BlockDesc* blocks = nullptr;  // [n_blocks + 1]
+  int64_t n_blocks = 0;
+  DecodeTable* dtab = nullptr;  // device copy
+  DecodeTable htab;             // host copy
+  SolverWs* ws = nullptr;
+  DistCtx* dist = nullptr;      // non-null for a row-partitioned matrix
+  int64_t n_local_cols = 0;     // dist: owned + halo columns
+};
+
+// ---------------------------------------------------------------- errors / allocation
+void set_error(const std::string& msg);
+gse_status cuda_status(cudaError_t e, const char* what);
+
+#define GSE_CUDA_TRY(expr)                                                     \
+  do {                                                                          \
+    cudaError_t _e = (expr);                                                    \
+    if (_e != cudaSuccess) return ::gse::cuda_status(_e, #expr);                \
+  } while (0)
+
+void* dev_alloc(size_t bytes, cudaStream_t s);
+void dev_free(void* p, cudaStream_t s);
+
+template <class T>
+T* dev_alloc_n(size_t n, cudaStream_t s) {
+  return static_cast<T*>(dev_alloc(n * sizeof(T) + 0, s));
+}
+
+inline size_t padded(int64_t nnz) { return (size_t)((nnz + NNZ_PAD - 1) / NNZ_PAD + 1) * NNZ_PAD; }
+
+bool is_device_ptr(const void* p, int* device);
+
+int num_sms(int device);
+
+// ---------------------------------------------------------------- kernels (launchers)
+// encode.cu
+gse_status build_partition(Matrix& M, cudaStream_t s);
+gse_status encode_matrix(Matrix& M, const gse_csr_f64& A, const void* d_row_ptr, int rp64,
+                         const int32_t* d_col, const double* d_val, cudaStream_t s);
+gse_status fp64_matrix(Matrix& M, const void* d_row_ptr, int rp64, const int32_t* d_col,
+                       const double* d_val, cudaStream_t s);
+void build_decode_table(Matrix& M);
+gse_status decode_all(const Matrix& M, int level, double* out, cudaStream_t s);
+
+// spmv.cu
+struct DotOut {
+  double* partials = nullptr;   // [n_blocks]
+  unsigned* ticket = nullptr;   // last-block counter (reset by the last block)
+  double* result = nullptr;     // deterministic sum of partials
+};
+gse_status launch_spmv(const Matrix& M, int level, const double* x, double* y,
+                       const DotOut* dot, cudaStream_t s);
+gse_status launch_spmv_guarded(const Matrix& M, int level, const double* x, double* y,
+                               const int* stop, cudaStream_t s);
+gse_status launch_spmv_f32(const Matrix& M, int level, const float* x, float* y,
+                           cudaStream_t s);
+
+// solvers.cu
+gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t max_iters,
+                    const gse_step_schedule& sched, gse_solve_report& rep, cudaStream_t s);
+gse_status solve_gmres(Matrix& M, const double* b, double* x, double tol, int restart,
+                       int64_t max_iters, const gse_step_schedule& sched,
+                       gse_solve_report& rep, cudaStream_t s);
+void free_solver_ws(Matrix& M);
+
+// dist.cu
+gse_status dist_halo_exchange(const Matrix& M, double* x_local_ext, cudaStream_t s);
+gse_status dist_allreduce_sum(const Matrix& M, double* d_vals, int count, cudaStream_t s);
+void free_dist(Matrix& M);
+
+}  // namespace gse
+
+struct gse_matrix_s {
+  gse::Matrix m;
+};

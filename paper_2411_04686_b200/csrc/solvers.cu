@@ -1,0 +1,874 @@
+// solvers.cu -- stepped mixed-precision CG and GMRES(m) on the GPU.
+//
+// Paper: Alg. stepped-GMRES: w_j = A_tag v_j, tag raised when the residual
+// monitor (Eqs. 3-6, Conditions 1-3) asks for more precision; CG / GMRES(30)
+// settings of P:299.  The paper's vector ops were cuBLAS calls -- prior art.
+//
+// B200 design:
+//  * every iteration is a fixed sequence of fused kernels with deterministic last-block
+//    reductions -- CG: [spmv + p.q] -> [x += a p, r -= a q, r.r, monitor] -> [p = r + b p];
+//    GMRES inner step j: [spmv] -> (j+1) x [w -= h v_{i-1}, w.v_i] -> [w -= h v_j, ||w||,
+//    Givens, monitor] -> [v_{j+1} = w / h];
+//  * the residual monitor (ring of t+1 residuals, RSD / nDec / relDec, Conditions 1-3)
+//    runs on the device in the last CTA of the update kernel: no host round trip per
+//    iteration;
+//  * CG iterations run inside a CUDA-graph WHILE node: the update kernel clears the
+//    condition (cudaGraphSetConditional) when an event occurs (converged recurrence,
+//    escalation request, breakdown, max iterations).  GMRES runs one graph per restart
+//    cycle (kernels early-exit once the cycle is stopped).  The host only handles events:
+//    level switch with residual replacement (R15), verification with A_3 (R16).
+#include <cmath>
+#include <vector>
+
+#include "gse_internal.cuh"
+
+namespace gse {
+
+enum Event : int {
+  EV_NONE = 0,
+  EV_CONVERGED = 1,   // recurrence / estimate <= tol
+  EV_ESCALATE = 2,    // monitor asks for a higher level
+  EV_ABORT = 3,       // breakdown / non-finite
+  EV_MAXITER = 4,     // iteration budget exhausted
+  EV_EXPLICIT_OK = 5  // GMRES restart: explicit residual <= tol
+};
+
+constexpr int MAX_RESTART = 64;
+
+struct SolveCtrl {
+  double bnorm, tol;
+  double rr, rr_new, pq, beta, resid;
+  double dot;  // scratch reduction target
+  long long iter, max_iters;
+  int level, event, stop, stepped, max_level;
+  long long l, t, m, ndec_limit;
+  double rsd_limit, reldec_limit, floor_[2];
+  long long ring_count, ring_head;
+  // GMRES
+  int restart, k;
+  double hn;
+  double H[(MAX_RESTART + 1) * MAX_RESTART];
+  double cs[MAX_RESTART], sn[MAX_RESTART], g[MAX_RESTART + 1], y[MAX_RESTART];
+};
+
+struct SolverWs {
+  int64_t n = 0;
+  int vgrid = 0;
+  double *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *b = nullptr, *tmp = nullptr;
+  double* V = nullptr;  // GMRES basis (restart + 1) x n
+  int V_cols = 0;
+  double* partials = nullptr;
+  unsigned* ticket = nullptr;
+  SolveCtrl* ctrl = nullptr;
+  double* ring = nullptr;
+  int64_t ring_cap = 0;
+  SolveCtrl* hctrl = nullptr;  // pinned host mirror
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t cg_exec[3] = {nullptr, nullptr, nullptr};
+  cudaGraph_t cg_graph[3] = {nullptr, nullptr, nullptr};
+  cudaGraphExec_t gm_exec[3] = {nullptr, nullptr, nullptr};
+  cudaGraph_t gm_graph[3] = {nullptr, nullptr, nullptr};
+  int gm_restart = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+// ---------------------------------------------------------------- reductions
+__device__ __forceinline__ double warp_sum_d(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+
+__device__ double block_sum_d(double v) {
+  __shared__ double red[32];
+  v = warp_sum_d(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+    red[0] = s;
+  }
+  __syncthreads();
+  s = red[0];
+  __syncthreads();
+  return s;
+}
+
+// returns true in (all threads of) the last CTA; *total = deterministic grid sum
+__device__ bool grid_sum(double part, double* partials, unsigned* ticket, double* total) {
+  __shared__ unsigned s_last;
+  __shared__ double s_tot;
+  const double bs = block_sum_d(part);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = bs;
+    __threadfence();
+    s_last = (atomicAdd(ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  double acc = 0.0;
+  for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) acc += __ldcg(partials + i);
+  const double tot = block_sum_d(acc);
+  if (threadIdx.x == 0) {
+    s_tot = tot;
+    *ticket = 0u;
+  }
+  __syncthreads();
+  *total = s_tot;
+  return true;
+}
+
+#define GRID_LOOP(i, n) \
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
+// ---------------------------------------------------------------- residual monitor
+// Mirrors the oracle's order of operations (ring push, RSD Eq. 3, nDec Eqs. 4-5, relDec
+// Eq. 6, Conditions 1-3 with nDec_limit (R13), optional floors (R17)).
+__device__ void ring_push(SolveCtrl* c, double* ring, double v) {
+  const long long cap = c->t + 1;
+  if (!c->stepped || cap <= 0) return;
+  if (c->ring_count < cap) {
+    ring[(c->ring_head + c->ring_count) % cap] = v;
+    c->ring_count++;
+  } else {
+    ring[c->ring_head] = v;
+    c->ring_head = (c->ring_head + 1) % cap;
+  }
+}
+
+__device__ int monitor_check(const SolveCtrl* c, const double* ring, long long j, double resid) {
+  if (!c->stepped || c->level >= c->max_level) return 0;
+  if (c->level <= 2 && c->floor_[c->level - 1] > 0.0 && resid < c->floor_[c->level - 1]) return 1;
+  const long long t = c->t, cap = t + 1;
+  if (j < c->l || ((j - c->l) % c->m) != 0 || c->ring_count < cap) return 0;
+  auto w = [&](long long i) { return ring[(c->ring_head + i) % cap]; };
+  if (!(w(0) > 0.0)) return 0;
+  double sum = 0.0;
+  for (long long i = 0; i < t; ++i) sum = __dadd_rn(sum, w(i));
+  const double avg = sum / (double)t;
+  double rsd = 0.0;
+  if (!(avg < 1e-300)) {
+    double ss = 0.0;
+    for (long long i = 0; i < t; ++i) {
+      const double dv = __dsub_rn(w(i), avg);
+      ss = __dadd_rn(ss, __dmul_rn(dv, dv));
+    }
+    rsd = sqrt(ss / (double)t) / avg;
+  }
+  long long nd = 0;
+  for (long long i = 0; i < t; ++i) nd += (w(i) > w(i + 1)) ? 1 : 0;
+  const double rd = (w(0) - w(t - 1)) / w(0);
+  const int c1 = (rsd > c->rsd_limit) && (nd < c->ndec_limit);
+  const int c2 = (nd >= c->ndec_limit) && (rd < c->reldec_limit);
+  const int c3 = (nd == 0);
+  return c1 || c2 || c3;
+}
+
+// ---------------------------------------------------------------- generic vector kernels
+// tot = a . b  (into *out)
+__global__ void __launch_bounds__(256) k_dot(const double* __restrict__ a,
+                                             const double* __restrict__ b, int64_t n,
+                                             double* partials, unsigned* ticket, double* out) {
+  double acc = 0.0;
+  GRID_LOOP(i, n) acc = __dadd_rn(acc, __dmul_rn(a[i], b[i]));
+  double tot;
+  if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0) *out = tot;
+}
+
+// r = b - Ax ; (optionally p = r) ; *out = r.r
+__global__ void __launch_bounds__(256) k_residual(const double* __restrict__ b,
+                                                  const double* Ax,  // may alias r
+                                                  double* r, double* __restrict__ p,
+                                                  int64_t n, double* partials, unsigned* ticket,
+                                                  double* out) {
+  double acc = 0.0;
+  GRID_LOOP(i, n) {
+    const double v = __dsub_rn(b[i], Ax[i]);
+    r[i] = v;
+    if (p) p[i] = v;
+    acc = __dadd_rn(acc, __dmul_rn(v, v));
+  }
+  double tot;
+  if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0) *out = tot;
+}
+
+// ---------------------------------------------------------------- CG kernels
+// x += alpha p ; r -= alpha q ; rr_new = r.r ; monitor ; events
+__global__ void __launch_bounds__(256) k_cg_update(SolveCtrl* __restrict__ c, double* ring,
+                                                   double* __restrict__ x, double* __restrict__ r,
+                                                   const double* __restrict__ p,
+                                                   const double* __restrict__ q, int64_t n,
+                                                   double* partials, unsigned* ticket,
+                                                   cudaGraphConditionalHandle handle) {
+  const double pq = c->pq, rr = c->rr;
+  const bool ok = (pq > 0.0) && isfinite(pq);
+  const double alpha = rr / pq;
+  double acc = 0.0;
+  if (ok) {
+    GRID_LOOP(i, n) {
+      x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+      const double ri = __dsub_rn(r[i], __dmul_rn(alpha, q[i]));
+      r[i] = ri;
+      acc = __dadd_rn(acc, __dmul_rn(ri, ri));
+    }
+  }
+  double tot;
+  if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0) {
+    const long long j = c->iter + 1;
+    c->iter = j;
+    int ev = EV_NONE;
+    if (!ok) {
+      ev = EV_ABORT;
+    } else {
+      const double resid = sqrt(tot) / c->bnorm;
+      c->resid = resid;
+      c->rr_new = tot;
+      if (!isfinite(resid)) {
+        ev = EV_ABORT;
+      } else {
+        ring_push(c, ring, resid);
+        if (resid <= c->tol)
+          ev = EV_CONVERGED;
+        else if (monitor_check(c, ring, j, resid))
+          ev = EV_ESCALATE;
+        else if (j >= c->max_iters)
+          ev = EV_MAXITER;
+      }
+    }
+    c->event = ev;
+    if (ev != EV_NONE) {
+      cudaGraphSetConditional(handle, 0u);
+    } else {
+      c->beta = tot / rr;
+      c->rr = tot;
+    }
+  }
+}
+
+// p = r + beta p (skipped when an event is pending: the host restarts / stops)
+__global__ void __launch_bounds__(256) k_cg_xpay(const SolveCtrl* __restrict__ c,
+                                                 double* __restrict__ p,
+                                                 const double* __restrict__ r, int64_t n) {
+  if (c->event != EV_NONE) return;
+  const double beta = c->beta;
+  GRID_LOOP(i, n) p[i] = __dadd_rn(r[i], __dmul_rn(beta, p[i]));
+}
+
+// ---------------------------------------------------------------- GMRES kernels
+// prologue: w = b - A x ; beta = ||w|| ; explicit convergence / budget checks
+__global__ void __launch_bounds__(256) k_gm_restart(SolveCtrl* __restrict__ c,
+                                                    const double* __restrict__ b,
+                                                    double* __restrict__ w, int64_t n,
+                                                    double* partials, unsigned* ticket) {
+  double acc = 0.0;
+  GRID_LOOP(i, n) {
+    const double v = __dsub_rn(b[i], w[i]);
+    w[i] = v;
+    acc = __dadd_rn(acc, __dmul_rn(v, v));
+  }
+  double tot;
+  if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0) {
+    const double beta = sqrt(tot);
+    const double resid = beta / c->bnorm;
+    c->resid = resid;
+    c->beta = beta;
+    c->k = 0;
+    c->stop = 0;
+    c->event = EV_NONE;
+    if (!isfinite(resid)) {
+      c->event = EV_ABORT;
+      c->stop = 1;
+    } else if (resid <= c->tol) {
+      c->event = EV_EXPLICIT_OK;
+      c->stop = 1;
+    } else if (c->iter >= c->max_iters) {
+      c->event = EV_MAXITER;
+      c->stop = 1;
+    } else {
+      for (int i = 0; i <= c->restart; ++i) c->g[i] = 0.0;
+      c->g[0] = beta;
+    }
+  }
+}
+
+// dst = src / *den   (skipped when stopped)
+__global__ void __launch_bounds__(256) k_gm_scale(const SolveCtrl* __restrict__ c,
+                                                  const double* __restrict__ src,
+                                                  double* __restrict__ dst, int64_t n,
+                                                  int use_hn) {
+  if (c->stop) return;
+  const double den = use_hn ? c->hn : c->beta;
+  GRID_LOOP(i, n) dst[i] = src[i] / den;
+}
+
+// MGS step i of inner iteration j: (i > 0) w -= H[i-1][j] v_{i-1}; H[i][j] = w . v_i
+__global__ void __launch_bounds__(256) k_gm_mgs(SolveCtrl* __restrict__ c, double* __restrict__ w,
+                                                const double* __restrict__ V, int64_t n, int i,
+                                                int j, double* partials, unsigned* ticket) {
+  if (c->stop) return;
+  const int m = c->restart;
+  const double* vi = V + (size_t)i * n;
+  double acc = 0.0;
+  if (i > 0) {
+    const double h = c->H[(i - 1) * m + j];
+    const double* vp = V + (size_t)(i - 1) * n;
+    GRID_LOOP(q, n) {
+      const double wv = __dsub_rn(w[q], __dmul_rn(h, vp[q]));
+      w[q] = wv;
+      acc = __dadd_rn(acc, __dmul_rn(wv, vi[q]));
+    }
+  } else {
+    GRID_LOOP(q, n) acc = __dadd_rn(acc, __dmul_rn(w[q], vi[q]));
+  }
+  double tot;
+  if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0) c->H[i * m + j] = tot;
+}
+
+// last MGS step: w -= H[j][j] v_j ; hn = ||w|| ; Givens (R18) ; estimate ; monitor
+__global__ void __launch_bounds__(256) k_gm_last(SolveCtrl* __restrict__ c, double* ring,
+                                                 double* __restrict__ w,
+                                                 const double* __restrict__ V, int64_t n, int j,
+                                                 double* partials, unsigned* ticket) {
+  if (c->stop) return;
+  const int m = c->restart;
+  const double h = c->H[j * m + j];
+  const double* vj = V + (size_t)j * n;
+  double acc = 0.0;
+  GRID_LOOP(q, n) {
+    const double wv = __dsub_rn(w[q], __dmul_rn(h, vj[q]));
+    w[q] = wv;
+    acc = __dadd_rn(acc, __dmul_rn(wv, wv));
+  }
+  double tot;
+  if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0) {
+    const double hn = sqrt(tot);
+    c->hn = hn;
+    double* H = c->H;
+    H[(j + 1) * m + j] = hn;
+    for (int i = 0; i < j; ++i) {  // apply previous rotations to column j
+      const double h1 = H[i * m + j], h2 = H[(i + 1) * m + j];
+      const double a1 = __dmul_rn(c->cs[i], h1), a2 = __dmul_rn(c->sn[i], h2);
+      const double b1 = __dmul_rn(c->sn[i], h1), b2 = __dmul_rn(c->cs[i], h2);
+      H[i * m + j] = __dadd_rn(a1, a2);
+      H[(i + 1) * m + j] = __dsub_rn(b2, b1);
+    }
+    const double h1 = H[j * m + j], h2 = H[(j + 1) * m + j];
+    double cc, ss;
+    if (h2 == 0.0) {
+      cc = 1.0;
+      ss = 0.0;
+    } else if (fabs(h2) > fabs(h1)) {
+      const double tau = h1 / h2;
+      ss = 1.0 / sqrt(__dadd_rn(1.0, __dmul_rn(tau, tau)));
+      cc = __dmul_rn(ss, tau);
+    } else {
+      const double tau = h2 / h1;
+      cc = 1.0 / sqrt(__dadd_rn(1.0, __dmul_rn(tau, tau)));
+      ss = __dmul_rn(cc, tau);
+    }
+    c->cs[j] = cc;
+    c->sn[j] = ss;
+    H[j * m + j] = __dadd_rn(__dmul_rn(cc, h1), __dmul_rn(ss, h2));
+    H[(j + 1) * m + j] = 0.0;
+    c->g[j + 1] = -__dmul_rn(ss, c->g[j]);
+    c->g[j] = __dmul_rn(cc, c->g[j]);
+    const double resid = fabs(c->g[j + 1]) / c->bnorm;
+    c->resid = resid;
+    const long long jg = c->iter + 1;
+    c->iter = jg;
+    c->k = j + 1;
+    if (!isfinite(resid)) {
+      c->event = EV_ABORT;
+      c->stop = 1;
+    } else {
+      ring_push(c, ring, resid);
+      if (resid <= c->tol || hn == 0.0) {
+        c->event = EV_CONVERGED;
+        c->stop = 1;
+      } else if (monitor_check(c, ring, jg, resid)) {
+        c->event = EV_ESCALATE;
+        c->stop = 1;
+      } else if (jg >= c->max_iters) {
+        c->stop = 1;  // the next restart reports MAXITER after the explicit check
+      }
+    }
+  }
+}
+
+// back substitution H[0:k,0:k] y = g[0:k] (one thread; k <= restart)
+__global__ void k_gm_backsolve(SolveCtrl* __restrict__ c) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (c->event == EV_ABORT) {
+    c->k = 0;
+    return;
+  }
+  const int k = c->k, m = c->restart;
+  for (int i = k - 1; i >= 0; --i) {
+    double s = c->g[i];
+    for (int l = i + 1; l < k; ++l) s = __dsub_rn(s, __dmul_rn(c->H[i * m + l], c->y[l]));
+    c->y[i] = s / c->H[i * m + i];
+  }
+}
+
+// x += sum_i y_i v_i (same per-element operation order as the oracle)
+__global__ void __launch_bounds__(256) k_gm_xupdate(const SolveCtrl* __restrict__ c,
+                                                    double* __restrict__ x,
+                                                    const double* __restrict__ V, int64_t n) {
+  const int k = c->k;
+  if (k == 0) return;
+  GRID_LOOP(q, n) {
+    double xv = x[q];
+    for (int i = 0; i < k; ++i) xv = __dadd_rn(xv, __dmul_rn(c->y[i], V[(size_t)i * n + q]));
+    x[q] = xv;
+  }
+}
+
+
+
+// ---------------------------------------------------------------- workspace
+static gse_status ensure_ws(Matrix& M, int64_t ring_t, int gm_restart, cudaStream_t s) {
+  SolverWs*& ws = M.ws;
+  const int64_t n = M.rows;
+  if (!ws) {
+    ws = new SolverWs();
+    ws->n = n;
+    ws->vgrid = num_sms(M.device) * 4;
+    const size_t nn = (size_t)(n > 0 ? n : 1);
+    ws->x = dev_alloc_n<double>(nn, s);
+    ws->r = dev_alloc_n<double>(nn, s);
+    ws->p = dev_alloc_n<double>(nn, s);
+    ws->q = dev_alloc_n<double>(nn, s);
+    ws->b = dev_alloc_n<double>(nn, s);
+    ws->tmp = dev_alloc_n<double>(nn, s);
+    const int64_t np = (M.n_blocks > ws->vgrid ? M.n_blocks : ws->vgrid) + 1;
+    ws->partials = dev_alloc_n<double>((size_t)np, s);
+    ws->ticket = dev_alloc_n<unsigned>(4, s);
+    ws->ctrl = dev_alloc_n<SolveCtrl>(1, s);
+    if (!ws->x || !ws->r || !ws->p || !ws->q || !ws->b || !ws->tmp || !ws->partials ||
+        !ws->ticket || !ws->ctrl)
+      return GSE_ERR_OOM;
+    GSE_CUDA_TRY(cudaMemsetAsync(ws->ticket, 0, 16, s));
+    GSE_CUDA_TRY(cudaMallocHost(&ws->hctrl, sizeof(SolveCtrl)));
+    GSE_CUDA_TRY(cudaStreamCreateWithFlags(&ws->cap_stream, cudaStreamNonBlocking));
+    GSE_CUDA_TRY(cudaEventCreate(&ws->ev0));
+    GSE_CUDA_TRY(cudaEventCreate(&ws->ev1));
+  }
+  if (ring_t + 1 > ws->ring_cap) {
+    if (ws->ring) dev_free(ws->ring, s);
+    ws->ring_cap = ring_t + 1;
+    ws->ring = dev_alloc_n<double>((size_t)ws->ring_cap, s);
+    if (!ws->ring) return GSE_ERR_OOM;
+  }
+  if (gm_restart > 0 && gm_restart + 1 > ws->V_cols) {
+    if (ws->V) dev_free(ws->V, s);
+    ws->V_cols = gm_restart + 1;
+    ws->V = dev_alloc_n<double>((size_t)ws->V_cols * (size_t)(n > 0 ? n : 1), s);
+    if (!ws->V) return GSE_ERR_OOM;
+  }
+  return GSE_OK;
+}
+
+void free_solver_ws(Matrix& M) {
+  SolverWs* ws = M.ws;
+  if (!ws) return;
+  cudaStream_t s = nullptr;
+  for (int L = 0; L < 3; ++L) {
+    if (ws->cg_exec[L]) cudaGraphExecDestroy(ws->cg_exec[L]);
+    if (ws->cg_graph[L]) cudaGraphDestroy(ws->cg_graph[L]);
+    if (ws->gm_exec[L]) cudaGraphExecDestroy(ws->gm_exec[L]);
+    if (ws->gm_graph[L]) cudaGraphDestroy(ws->gm_graph[L]);
+  }
+  for (double* p : {ws->x, ws->r, ws->p, ws->q, ws->b, ws->tmp, ws->V, ws->partials, ws->ring})
+    if (p) dev_free(p, s);
+  if (ws->ticket) dev_free(ws->ticket, s);
+  if (ws->ctrl) dev_free(ws->ctrl, s);
+  if (ws->hctrl) cudaFreeHost(ws->hctrl);
+  if (ws->cap_stream) cudaStreamDestroy(ws->cap_stream);
+  if (ws->ev0) cudaEventDestroy(ws->ev0);
+  if (ws->ev1) cudaEventDestroy(ws->ev1);
+  delete ws;
+  M.ws = nullptr;
+}
+
+static gse_status read_ctrl(SolverWs* ws, cudaStream_t s) {
+  GSE_CUDA_TRY(cudaMemcpyAsync(ws->hctrl, ws->ctrl, sizeof(SolveCtrl), cudaMemcpyDeviceToHost, s));
+  GSE_CUDA_TRY(cudaStreamSynchronize(s));
+  return GSE_OK;
+}
+
+template <class T>
+static gse_status set_field(SolverWs* ws, T SolveCtrl::*field, T v, cudaStream_t s) {
+  // stream-ordered host->device write of one control field (pinned staging)
+  size_t off = (size_t)(&(((SolveCtrl*)nullptr)->*field));
+  T* staging = (T*)((char*)ws->hctrl + off);
+  *staging = v;
+  GSE_CUDA_TRY(cudaMemcpyAsync((char*)ws->ctrl + off, staging, sizeof(T), cudaMemcpyHostToDevice, s));
+  return GSE_OK;
+}
+
+static DotOut dot_to(SolverWs* ws, double* target) {
+  DotOut d;
+  d.partials = ws->partials;
+  d.ticket = ws->ticket;
+  d.result = target;
+  return d;
+}
+
+// ---------------------------------------------------------------- CG graph per level
+static gse_status build_cg_graph(Matrix& M, int level) {
+  SolverWs* ws = M.ws;
+  if (ws->cg_exec[level - 1]) return GSE_OK;
+  cudaGraph_t g;
+  GSE_CUDA_TRY(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  GSE_CUDA_TRY(cudaGraphConditionalHandleCreate(&h, g, 1u, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  GSE_CUDA_TRY(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  cudaStream_t cs = ws->cap_stream;
+  GSE_CUDA_TRY(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
+                                             cudaStreamCaptureModeRelaxed));
+  const int64_t n = M.rows;
+  DotOut d = dot_to(ws, &ws->ctrl->pq);
+  gse_status rc = launch_spmv(M, level, ws->p, ws->q, &d, cs);
+  k_cg_update<<<ws->vgrid, 256, 0, cs>>>(ws->ctrl, ws->ring, ws->x, ws->r, ws->p, ws->q, n,
+                                         ws->partials, ws->ticket, h);
+  k_cg_xpay<<<ws->vgrid, 256, 0, cs>>>(ws->ctrl, ws->p, ws->r, n);
+  cudaGraph_t captured;
+  cudaError_t e = cudaStreamEndCapture(cs, &captured);
+  if (rc != GSE_OK) return rc;
+  GSE_CUDA_TRY(e);
+  GSE_CUDA_TRY(cudaGraphInstantiate(&ws->cg_exec[level - 1], g, 0));
+  ws->cg_graph[level - 1] = g;
+  return GSE_OK;
+}
+
+static void fill_sched(SolveCtrl* h, const gse_step_schedule& sc, int stepped) {
+  h->stepped = stepped;
+  h->max_level = sc.max_level;
+  h->l = sc.l;
+  h->t = sc.t;
+  h->m = sc.m;
+  h->ndec_limit = sc.ndec_limit;
+  h->rsd_limit = sc.rsd_limit;
+  h->reldec_limit = sc.reldec_limit;
+  h->floor_[0] = sc.level_floor[0];
+  h->floor_[1] = sc.level_floor[1];
+  h->ring_count = 0;
+  h->ring_head = 0;
+}
+
+static void log_switch(gse_solve_report& rep, int64_t j, int lvl) {
+  if (rep.n_switches < 2) {
+    rep.switch_iter[rep.n_switches] = j;
+    rep.switch_to_level[rep.n_switches] = lvl;
+  }
+  rep.n_switches++;
+}
+
+// true relative residual ||b - A_3 x|| / ||b|| (x = ws->x); uses ws->tmp / ws->q
+static gse_status true_resid(Matrix& M, const double* x, double bnorm, gse_solve_report& rep,
+                             double* out, cudaStream_t s) {
+  SolverWs* ws = M.ws;
+  gse_status rc = launch_spmv(M, 3, x, ws->tmp, nullptr, s);
+  if (rc != GSE_OK) return rc;
+  rep.spmv_count[2]++;
+  k_residual<<<ws->vgrid, 256, 0, s>>>(ws->b, ws->tmp, ws->tmp, nullptr, M.rows, ws->partials,
+                                       ws->ticket, &ws->ctrl->dot);
+  GSE_CUDA_TRY(cudaGetLastError());
+  rc = read_ctrl(ws, s);
+  if (rc != GSE_OK) return rc;
+  *out = sqrt(ws->hctrl->dot) / bnorm;
+  return GSE_OK;
+}
+
+gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t max_iters,
+                    const gse_step_schedule& sched, gse_solve_report& rep, cudaStream_t s) {
+  const int64_t n = M.rows;
+  const int stepped = sched.enabled && M.kind == GSE_KIND_GSE;
+  int level = (M.kind == GSE_KIND_FP64) ? 3 : sched.start_level;
+  gse_status rc = ensure_ws(M, stepped ? sched.t : 0, 0, s);
+  if (rc != GSE_OK) return rc;
+  SolverWs* ws = M.ws;
+  GSE_CUDA_TRY(cudaEventRecord(ws->ev0, s));
+  GSE_CUDA_TRY(cudaMemcpyAsync(ws->b, b, n * 8, cudaMemcpyDeviceToDevice, s));
+  GSE_CUDA_TRY(cudaMemcpyAsync(ws->x, x, n * 8, cudaMemcpyDeviceToDevice, s));
+  // ||b||, r0 = b - A_L x0, p0 = r0, rr
+  k_dot<<<ws->vgrid, 256, 0, s>>>(ws->b, ws->b, n, ws->partials, ws->ticket, &ws->ctrl->dot);
+  rc = launch_spmv(M, level, ws->x, ws->q, nullptr, s);
+  if (rc != GSE_OK) return rc;
+  rep.spmv_count[level - 1]++;
+  k_residual<<<ws->vgrid, 256, 0, s>>>(ws->b, ws->q, ws->r, ws->p, n, ws->partials, ws->ticket,
+                                       &ws->ctrl->rr);
+  GSE_CUDA_TRY(cudaGetLastError());
+  rc = read_ctrl(ws, s);
+  if (rc != GSE_OK) return rc;
+  SolveCtrl* hc = ws->hctrl;
+  const double bnorm = sqrt(hc->dot);
+  gse_status status = GSE_NOT_CONVERGED;
+  int64_t iter = 0;
+  if (bnorm == 0.0) {
+    GSE_CUDA_TRY(cudaMemsetAsync(x, 0, n * 8, s));
+    rep.converged = 1;
+    rep.rel_residual_true = 0.0;
+    GSE_CUDA_TRY(cudaStreamSynchronize(s));
+    return GSE_OK;
+  }
+  double resid = sqrt(hc->rr) / bnorm;
+  rep.rel_residual_recurrence = resid;
+  bool done = false;
+  if (resid <= tol) {
+    double rt = 0;
+    if (!(stepped && level < 3 && sched.verify_at_full)) {
+      status = GSE_OK;
+      done = true;
+    } else {
+      rc = true_resid(M, ws->x, bnorm, rep, &rt, s);
+      if (rc != GSE_OK) return rc;
+      if (rt <= tol) {
+        status = GSE_OK;
+        done = true;
+      } else {
+        level = 3;
+        log_switch(rep, 0, level);
+        rc = launch_spmv(M, level, ws->x, ws->q, nullptr, s);
+        if (rc != GSE_OK) return rc;
+        rep.spmv_count[level - 1]++;
+        k_residual<<<ws->vgrid, 256, 0, s>>>(ws->b, ws->q, ws->r, ws->p, n, ws->partials,
+                                             ws->ticket, &ws->ctrl->rr);
+      }
+    }
+  }
+  // control block (scalars live on the device from here on)
+  hc = ws->hctrl;
+  if (!done) {
+    rc = read_ctrl(ws, s);  // refresh rr
+    if (rc != GSE_OK) return rc;
+    hc->bnorm = bnorm;
+    hc->tol = tol;
+    hc->iter = 0;
+    hc->max_iters = max_iters;
+    hc->level = level;
+    hc->event = EV_NONE;
+    fill_sched(hc, sched, stepped);
+    GSE_CUDA_TRY(cudaMemcpyAsync(ws->ctrl, hc, sizeof(SolveCtrl), cudaMemcpyHostToDevice, s));
+  }
+  int64_t last_iter = 0;
+  while (!done) {
+    if (iter >= max_iters) {
+      status = GSE_NOT_CONVERGED;
+      break;
+    }
+    rc = build_cg_graph(M, level);
+    if (rc != GSE_OK) return rc;
+    GSE_CUDA_TRY(cudaGraphLaunch(ws->cg_exec[level - 1], s));
+    rc = read_ctrl(ws, s);
+    if (rc != GSE_OK) return rc;
+    iter = hc->iter;
+    rep.iters_per_level[level - 1] += iter - last_iter;
+    rep.spmv_count[level - 1] += iter - last_iter;
+    last_iter = iter;
+    rep.rel_residual_recurrence = hc->resid;
+    const int ev = hc->event;
+    bool escalate = false;
+    if (ev == EV_ABORT) {
+      status = GSE_NUMERICAL_ABORT;
+      break;
+    } else if (ev == EV_CONVERGED) {
+      if (!(stepped && level < 3 && sched.verify_at_full)) {
+        status = GSE_OK;
+        break;
+      }
+      double rt = 0;
+      rc = true_resid(M, ws->x, bnorm, rep, &rt, s);
+      if (rc != GSE_OK) return rc;
+      if (rt <= tol) {
+        status = GSE_OK;
+        break;
+      }
+      escalate = true;
+    } else if (ev == EV_ESCALATE) {
+      escalate = true;
+    } else if (ev == EV_MAXITER) {
+      status = GSE_NOT_CONVERGED;
+      break;
+    } else {
+      set_error("internal: CG graph returned without an event");
+      return GSE_ERR_CUDA;
+    }
+    if (escalate) {
+      // R15: restart from the current x at the new level: r = b - A_new x, p = r
+      level++;
+      log_switch(rep, iter, level);
+      rc = launch_spmv(M, level, ws->x, ws->q, nullptr, s);
+      if (rc != GSE_OK) return rc;
+      rep.spmv_count[level - 1]++;
+      k_residual<<<ws->vgrid, 256, 0, s>>>(ws->b, ws->q, ws->r, ws->p, n, ws->partials,
+                                           ws->ticket, &ws->ctrl->rr);
+      GSE_CUDA_TRY(cudaGetLastError());
+      rc = set_field(ws, &SolveCtrl::level, level, s);
+      if (rc != GSE_OK) return rc;
+      rc = set_field(ws, &SolveCtrl::event, (int)EV_NONE, s);
+      if (rc != GSE_OK) return rc;
+      if (iter >= max_iters) {
+        status = GSE_NOT_CONVERGED;
+        break;
+      }
+    }
+  }
+  rep.iterations = iter;
+  rep.converged = (status == GSE_OK);
+  double rt = 0;
+  rc = true_resid(M, ws->x, bnorm, rep, &rt, s);
+  if (rc != GSE_OK) return rc;
+  rep.rel_residual_true = rt;
+  GSE_CUDA_TRY(cudaMemcpyAsync(x, ws->x, n * 8, cudaMemcpyDeviceToDevice, s));
+  GSE_CUDA_TRY(cudaEventRecord(ws->ev1, s));
+  GSE_CUDA_TRY(cudaEventSynchronize(ws->ev1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
+  rep.seconds = ms * 1e-3;
+  return status;
+}
+
+// ---------------------------------------------------------------- GMRES
+static gse_status build_gm_graph(Matrix& M, int level, int restart) {
+  SolverWs* ws = M.ws;
+  if (ws->gm_restart != restart) {
+    for (int L = 0; L < 3; ++L) {
+      if (ws->gm_exec[L]) cudaGraphExecDestroy(ws->gm_exec[L]);
+      if (ws->gm_graph[L]) cudaGraphDestroy(ws->gm_graph[L]);
+      ws->gm_exec[L] = nullptr;
+      ws->gm_graph[L] = nullptr;
+    }
+    ws->gm_restart = restart;
+  }
+  if (ws->gm_exec[level - 1]) return GSE_OK;
+  cudaStream_t cs = ws->cap_stream;
+  const int64_t n = M.rows;
+  SolveCtrl* c = ws->ctrl;
+  double* w = ws->tmp;
+  GSE_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+  gse_status rc = launch_spmv(M, level, ws->x, w, nullptr, cs);
+  k_gm_restart<<<ws->vgrid, 256, 0, cs>>>(c, ws->b, w, n, ws->partials, ws->ticket);
+  k_gm_scale<<<ws->vgrid, 256, 0, cs>>>(c, w, ws->V, n, 0);
+  for (int j = 0; j < restart && rc == GSE_OK; ++j) {
+    rc = launch_spmv_guarded(M, level, ws->V + (size_t)j * n, w, &c->stop, cs);
+    for (int i = 0; i <= j; ++i)
+      k_gm_mgs<<<ws->vgrid, 256, 0, cs>>>(c, w, ws->V, n, i, j, ws->partials, ws->ticket);
+    k_gm_last<<<ws->vgrid, 256, 0, cs>>>(c, ws->ring, w, ws->V, n, j, ws->partials, ws->ticket);
+    if (j + 1 < restart)
+      k_gm_scale<<<ws->vgrid, 256, 0, cs>>>(c, w, ws->V + (size_t)(j + 1) * n, n, 1);
+  }
+  k_gm_backsolve<<<1, 32, 0, cs>>>(c);
+  k_gm_xupdate<<<ws->vgrid, 256, 0, cs>>>(c, ws->x, ws->V, n);
+  cudaGraph_t g;
+  cudaError_t e = cudaStreamEndCapture(cs, &g);
+  if (rc != GSE_OK) return rc;
+  GSE_CUDA_TRY(e);
+  GSE_CUDA_TRY(cudaGraphInstantiate(&ws->gm_exec[level - 1], g, 0));
+  ws->gm_graph[level - 1] = g;
+  return GSE_OK;
+}
+
+gse_status solve_gmres(Matrix& M, const double* b, double* x, double tol, int restart,
+                       int64_t max_iters, const gse_step_schedule& sched, gse_solve_report& rep,
+                       cudaStream_t s) {
+  const int64_t n = M.rows;
+  const int stepped = sched.enabled && M.kind == GSE_KIND_GSE;
+  int level = (M.kind == GSE_KIND_FP64) ? 3 : sched.start_level;
+  gse_status rc = ensure_ws(M, stepped ? sched.t : 0, restart, s);
+  if (rc != GSE_OK) return rc;
+  SolverWs* ws = M.ws;
+  GSE_CUDA_TRY(cudaEventRecord(ws->ev0, s));
+  GSE_CUDA_TRY(cudaMemcpyAsync(ws->b, b, n * 8, cudaMemcpyDeviceToDevice, s));
+  GSE_CUDA_TRY(cudaMemcpyAsync(ws->x, x, n * 8, cudaMemcpyDeviceToDevice, s));
+  k_dot<<<ws->vgrid, 256, 0, s>>>(ws->b, ws->b, n, ws->partials, ws->ticket, &ws->ctrl->dot);
+  GSE_CUDA_TRY(cudaGetLastError());
+  rc = read_ctrl(ws, s);
+  if (rc != GSE_OK) return rc;
+  SolveCtrl* hc = ws->hctrl;
+  const double bnorm = sqrt(hc->dot);
+  if (bnorm == 0.0) {
+    GSE_CUDA_TRY(cudaMemsetAsync(x, 0, n * 8, s));
+    rep.converged = 1;
+    GSE_CUDA_TRY(cudaStreamSynchronize(s));
+    return GSE_OK;
+  }
+  hc->bnorm = bnorm;
+  hc->tol = tol;
+  hc->iter = 0;
+  hc->max_iters = max_iters;
+  hc->level = level;
+  hc->event = EV_NONE;
+  hc->stop = 0;
+  hc->restart = restart;
+  hc->k = 0;
+  fill_sched(hc, sched, stepped);
+  GSE_CUDA_TRY(cudaMemcpyAsync(ws->ctrl, hc, sizeof(SolveCtrl), cudaMemcpyHostToDevice, s));
+  gse_status status = GSE_NOT_CONVERGED;
+  int64_t last_iter = 0, iter = 0;
+  for (;;) {
+    rc = build_gm_graph(M, level, restart);
+    if (rc != GSE_OK) return rc;
+    GSE_CUDA_TRY(cudaGraphLaunch(ws->gm_exec[level - 1], s));
+    rc = read_ctrl(ws, s);
+    if (rc != GSE_OK) return rc;
+    iter = hc->iter;
+    rep.iters_per_level[level - 1] += iter - last_iter;
+    rep.spmv_count[level - 1] += iter - last_iter + 1;  // inner SpMVs + restart residual
+    last_iter = iter;
+    rep.rel_residual_recurrence = hc->resid;
+    const int ev = hc->event;
+    if (ev == EV_ABORT) {
+      status = GSE_NUMERICAL_ABORT;
+      break;
+    }
+    if (ev == EV_EXPLICIT_OK) {
+      if (!(stepped && level < 3 && sched.verify_at_full)) {
+        status = GSE_OK;
+        break;
+      }
+      double rt = 0;
+      rc = true_resid(M, ws->x, bnorm, rep, &rt, s);
+      if (rc != GSE_OK) return rc;
+      if (rt <= tol) {
+        status = GSE_OK;
+        break;
+      }
+      level++;
+      log_switch(rep, iter, level);
+    } else if (ev == EV_MAXITER) {
+      status = GSE_NOT_CONVERGED;
+      break;
+    } else if (ev == EV_ESCALATE) {
+      level++;
+      log_switch(rep, iter, level);
+    }
+    rc = set_field(ws, &SolveCtrl::level, level, s);
+    if (rc != GSE_OK) return rc;
+  }
+  rep.iterations = iter;
+  rep.converged = (status == GSE_OK);
+  double rt = 0;
+  rc = true_resid(M, ws->x, bnorm, rep, &rt, s);
+  if (rc != GSE_OK) return rc;
+  rep.rel_residual_true = rt;
+  GSE_CUDA_TRY(cudaMemcpyAsync(x, ws->x, n * 8, cudaMemcpyDeviceToDevice, s));
+  GSE_CUDA_TRY(cudaEventRecord(ws->ev1, s));
+  GSE_CUDA_TRY(cudaEventSynchronize(ws->ev1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
+  rep.seconds = ms * 1e-3;
+  return status;
+}
+
+}  // namespace gse

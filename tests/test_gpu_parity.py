@@ -1,0 +1,353 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle on the same seeded
+inputs.  Bars (BASELINE.json north_star):
+  * encode / decode: bit-exact (table, col_ei, head, tail1, tail2, side array, decoded FP64);
+  * SpMV: |y_gpu - y_orc| <= 1e-12 * sum_j |dec_L(a_ij) x_j| (FP64 accumulate), 1e-5 (FP32);
+    rows whose sum is 0 must be exactly 0;
+  * solvers: |iters_gpu - iters_orc| <= 2, final true relative residual ratio in [0.1, 10].
+"""
+import numpy as np
+import pytest
+
+import gse_inputs as gi
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def g():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2411_04686_b200 as lib  # fails loudly when the extension is missing
+    return lib
+
+
+def enc_both(g, A, k=8, device_inputs=False):
+    if device_inputs:
+        M = g.gse_encode(torch.from_numpy(A.row_ptr).cuda(), torch.from_numpy(A.col).cuda(),
+                         torch.from_numpy(A.val).cuda(), A.rows, A.cols, k_max=k)
+    else:
+        M = g.gse_encode(A.row_ptr, A.col, A.val, A.rows, A.cols, k_max=k)
+    R = O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val, k)
+    return M, R
+
+
+def spmv_bound(R, x, level, tol):
+    """tol * sum_j |dec_L(a_ij) x_j| per row, via the oracle's SpMV of |A_L| |x|."""
+    absR = O.GseCsr(R.rows, R.cols, R.nnz, R.row_ptr, R.col_ei, R.side_ei,
+                    R.head & np.uint16(0x7FFF), R.tail1, R.tail2, R.table, R.ei_bits,
+                    R.ei_in_column)
+    return tol * O.spmv_gse(absR, np.abs(x), level)
+
+
+MATS = {
+    "poisson2d_const": lambda: gi.poisson2d(32),
+    "poisson2d_varcoef": lambda: gi.poisson2d(32, "varcoef"),
+    "poisson3d_40": lambda: gi.poisson3d(40, "varcoef"),
+    "random_classes": lambda: gi.random_csr(3000, 2500, 9, seed=1, empty_rows=0.05),
+    "random_wide": lambda: gi.random_csr(2000, 3000, 5, seed=2, value_kind="wide"),
+    "random_mixed": lambda: gi.random_csr(2000, 2000, 7, seed=3, value_kind="mixed",
+                                          empty_rows=0.2),
+    "powerlaw_30k": lambda: gi.powerlaw_spd(30000, seed=5),
+    "convdiff_20": lambda: gi.convdiff3d(20),
+}
+
+
+def long_rows_matrix():
+    """rows of length 0, 1, LMAX-1, LMAX, LMAX+1, 2047, 2048, 2049, 5000 (DESIGN.md partition
+    boundaries) interleaved with short rows."""
+    rng = np.random.default_rng(9)
+    lens = [3, 0, 1, 255, 256, 257, 7, 2047, 2048, 2049, 0, 5000, 2, 1784, 1785, 6]
+    lens = lens * 3
+    cols = 6000
+    rp = np.zeros(len(lens) + 1, np.int64)
+    np.cumsum(lens, out=rp[1:])
+    col = np.concatenate([np.sort(rng.choice(cols, L, replace=False)) for L in lens]).astype(np.int32)
+    val = rng.uniform(-2, 2, rp[-1]) * np.ldexp(1.0, rng.integers(-8, 8, rp[-1]))
+    return gi.Csr(len(lens), cols, rp, col, val, "long_rows")
+
+
+MATS["long_rows"] = long_rows_matrix
+
+
+# ------------------------------------------------------------------ encode / decode
+@pytest.mark.parametrize("name", sorted(MATS))
+def test_encode_bit_exact(g, name):
+    A = MATS[name]()
+    M, R = enc_both(g, A, device_inputs=(name.startswith("poisson")))
+    P = g.gse_matrix_copy_planes(M)
+    assert list(P["table"]) == list(R.table)
+    assert M.info["ei_bits"] == R.ei_bits and M.info["ei_in_column"] == R.ei_in_column
+    for k in ("col_ei", "head", "tail1", "tail2"):
+        assert np.array_equal(P[k], getattr(R, k)), k
+
+
+@pytest.mark.parametrize("k", [1, 2, 4, 16, 64])
+def test_encode_k_sweep_bit_exact(g, k):
+    A = gi.powerlaw_spd(5000, seed=k)
+    M, R = enc_both(g, A, k)
+    P = g.gse_matrix_copy_planes(M)
+    assert list(P["table"]) == list(R.table)
+    for key in ("col_ei", "head", "tail1", "tail2"):
+        assert np.array_equal(P[key], getattr(R, key)), key
+
+
+def test_encode_side_array(g):
+    """cols >= 2^(32 - ei_bits): EI in a side array."""
+    rng = np.random.default_rng(4)
+    rows, cols = 300, (1 << 29) + 1000
+    lens = rng.integers(0, 12, rows)
+    rp = np.zeros(rows + 1, np.int64)
+    np.cumsum(lens, out=rp[1:])
+    col = np.concatenate([np.sort(rng.choice(cols, L, replace=False)) for L in lens]).astype(np.int32)
+    val = rng.uniform(-1, 1, rp[-1]) * np.ldexp(1.0, rng.integers(-20, 20, rp[-1]))
+    A = gi.Csr(rows, cols, rp, col, val)
+    M, R = enc_both(g, A)
+    P = g.gse_matrix_copy_planes(M)
+    assert not R.ei_in_column and not M.info["ei_in_column"]
+    for key in ("col_ei", "head", "tail1", "tail2", "side_ei"):
+        assert np.array_equal(P[key], getattr(R, key)), key
+    x = gi.uniform_vec(cols, seed=1)
+    for L in (1, 2, 3):
+        yg = g.gse_spmv(M, x, segments=L)
+        yo = O.spmv_gse(R, x, L)
+        assert np.all(np.abs(yg - yo) <= spmv_bound(R, x, L, 1e-12))
+
+
+@pytest.mark.parametrize("name", ["random_wide", "random_mixed", "poisson2d_varcoef"])
+def test_decode_bit_exact(g, name):
+    A = MATS[name]()
+    M, R = enc_both(g, A)
+    for L in (1, 2, 3):
+        got = g.gse_decode(M, L)
+        want = O.decode_all(R, L)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), L
+
+
+# ------------------------------------------------------------------ SpMV
+@pytest.mark.parametrize("name", sorted(MATS))
+def test_spmv_levels_parity(g, name):
+    A = MATS[name]()
+    M, R = enc_both(g, A)
+    x = gi.uniform_vec(A.cols, seed=7)
+    xt = torch.from_numpy(x).cuda()
+    for L in (1, 2, 3):
+        yg = g.gse_spmv(M, xt, segments=L).cpu().numpy()
+        yo = O.spmv_gse(R, x, L)
+        bound = spmv_bound(R, x, L, 1e-12)
+        bad = np.abs(yg - yo) > bound
+        assert not bad.any(), (L, np.nonzero(bad)[0][:5])
+        assert np.all(yg[bound == 0] == 0.0)
+
+
+@pytest.mark.parametrize("name", ["poisson3d_40", "powerlaw_30k", "long_rows", "random_mixed"])
+def test_spmv_fp64_comparator_parity(g, name):
+    A = MATS[name]()
+    M = g.gse_fp64_matrix(A.row_ptr, A.col, A.val, A.rows, A.cols)
+    F = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+    x = gi.uniform_vec(A.cols, seed=3)
+    yg = g.gse_spmv(M, x, segments=3)
+    yo = O.spmv_fp64(F, x)
+    Fa = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, np.abs(A.val))
+    assert np.all(np.abs(yg - yo) <= 1e-12 * O.spmv_fp64(Fa, np.abs(x)))
+
+
+@pytest.mark.parametrize("name", ["poisson3d_40", "powerlaw_30k", "long_rows", "random_classes"])
+def test_spmv_f32acc_parity(g, name):
+    A = MATS[name]()
+    M, R = enc_both(g, A)
+    x = gi.uniform_vec(A.cols, seed=4)
+    x32 = x.astype(np.float32)
+    for L in (1, 2, 3):
+        y32 = g.gse_spmv_f32acc(M, x32, segments=L)
+        yo = O.spmv_gse(R, x32.astype(np.float64), L)
+        assert np.all(np.abs(y32.astype(np.float64) - yo) <= spmv_bound(R, x32.astype(np.float64), L, 1e-5))
+
+
+def test_spmv_head_exact_poisson_bitwise(g):
+    """Constant Poisson is exact in the head: levels 1/2/3 and FP64 agree bitwise, and
+    short rows are summed in storage order like the oracle."""
+    A = gi.poisson3d(24)
+    M, R = enc_both(g, A)
+    x = gi.uniform_vec(A.cols, seed=5)
+    yo = O.spmv_fp64(O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val), x)
+    for L in (1, 2, 3):
+        assert np.array_equal(g.gse_spmv(M, x, segments=L).view(np.uint64), yo.view(np.uint64))
+
+
+def test_spmv_edge_cases(g):
+    # one row, one column
+    A = gi.from_dense(np.array([[2.5]]))
+    M, _ = enc_both(g, A)
+    assert g.gse_spmv(M, np.array([2.0]), segments=1)[0] == 5.0
+    # all rows empty but one
+    A = gi.random_csr(500, 40, 0.01, seed=2)
+    A.val[:] = 3.0
+    if A.nnz == 0:
+        A = gi.from_dense(np.pad(np.array([[3.0]]), ((0, 499), (0, 39))))
+    M, R = enc_both(g, A)
+    x = np.ones(40)
+    assert np.array_equal(g.gse_spmv(M, x, segments=2), O.spmv_gse(R, x, 2))
+    # zero-size matrix
+    Z = g.gse_fp64_matrix(np.zeros(1, np.int64), np.zeros(0, np.int32), np.zeros(0), 0, 0)
+    assert Z.info["rows"] == 0
+
+
+def test_errors(g):
+    A = gi.poisson2d(8)
+    val = A.val.copy()
+    val[17] = np.nan
+    with pytest.raises(g.GseError) as e:
+        g.gse_encode(A.row_ptr, A.col, val, A.rows, A.cols)
+    assert e.value.status == g.GSE_ERR_NONFINITE and "row" in e.value.detail
+    col = A.col.copy()
+    col[3] = A.cols + 5
+    with pytest.raises(g.GseError) as e:
+        g.gse_encode(A.row_ptr, col, A.val, A.rows, A.cols)
+    assert e.value.status == g.GSE_ERR_INVALID_ARG
+    with pytest.raises(g.GseError) as e:
+        g.gse_encode(A.row_ptr, A.col, np.zeros_like(A.val), A.rows, A.cols)
+    assert e.value.status == g.GSE_ERR_NO_VALUES
+    M = g.gse_encode(A.row_ptr, A.col, A.val, A.rows, A.cols)
+    with pytest.raises(g.GseError):
+        g.gse_spmv(M, np.ones(A.cols), segments=4)
+    big = A.val * 2.0 ** 300
+    Mb = g.gse_encode(A.row_ptr, A.col, big, A.rows, A.cols)
+    with pytest.raises(g.GseError) as e:
+        g.gse_spmv_f32acc(Mb, np.ones(A.cols, np.float32), segments=1)
+    assert e.value.status == g.GSE_ERR_FP32_RANGE
+
+
+# ------------------------------------------------------------------ full-size sampled SpMV
+def test_spmv_full_size_c2_sampled(g):
+    """C2 (3D Poisson 128^3, varcoef) at full size, in bench.py's launch configuration:
+    sampled rows against the oracle computed on just those rows."""
+    A = gi.poisson3d(128, "varcoef")
+    M = g.gse_encode(torch.from_numpy(A.row_ptr).cuda(), torch.from_numpy(A.col).cuda(),
+                     torch.from_numpy(A.val).cuda(), A.rows, A.cols)
+    P = g.gse_matrix_copy_planes(M)
+    rng = np.random.default_rng(0)
+    rows = np.unique(np.concatenate([rng.integers(0, A.rows, 3000), [0, A.rows - 1]]))
+    x = gi.uniform_vec(A.cols, seed=11)
+    xt = torch.from_numpy(x).cuda()
+    # oracle on the sampled rows: build the sub-CSR of those rows with the GPU-independent
+    # oracle encoding of the same values (table from the full matrix)
+    R = O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+    assert list(P["table"]) == list(R.table)
+    sel = np.concatenate([np.arange(A.row_ptr[r], A.row_ptr[r + 1]) for r in rows])
+    rp = np.zeros(rows.size + 1, np.int64)
+    np.cumsum(A.row_ptr[rows + 1] - A.row_ptr[rows], out=rp[1:])
+    sub = O.GseCsr(rows.size, A.cols, sel.size, rp, R.col_ei[sel].copy(), None,
+                   R.head[sel].copy(), R.tail1[sel].copy(), R.tail2[sel].copy(), R.table,
+                   R.ei_bits, R.ei_in_column)
+    for L in (1, 2, 3):
+        yg = g.gse_spmv(M, xt, segments=L).cpu().numpy()[rows]
+        yo = O.spmv_gse(sub, x, L)
+        assert np.all(np.abs(yg - yo) <= spmv_bound(sub, x, L, 1e-12))
+    # the full planes are bit-exact too
+    for k in ("col_ei", "head", "tail1", "tail2"):
+        assert np.array_equal(P[k], getattr(R, k)), k
+
+
+# ------------------------------------------------------------------ solvers
+def _cmp_reports(rg, ro, iters_tol=2):
+    assert rg["status"] == ro.status
+    assert abs(rg["iterations"] - ro.iterations) <= iters_tol, (rg, ro)
+    if ro.rel_residual_true > 0:
+        ratio = rg["rel_residual_true"] / ro.rel_residual_true
+        assert 0.1 <= ratio <= 10, (rg, ro)
+
+
+@pytest.mark.parametrize("variant", ["const", "varcoef"])
+@pytest.mark.parametrize("mode", ["fp64", "fixed3", "stepped", "stepped_scaled"])
+def test_cg_parity_c1(g, variant, mode):
+    A = gi.poisson2d(32, variant)
+    b = gi.ones_rhs(A)
+    if mode == "fp64":
+        M = g.gse_fp64_matrix(A.row_ptr, A.col, A.val, A.rows, A.cols)
+        Rm = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+        sg, so = None, None
+    else:
+        M, Rm = enc_both(g, A)
+        if mode == "fixed3":
+            sg, so = g.fixed_schedule(3), O.fixed_schedule(3)
+        elif mode == "stepped":
+            sg, so = g.gse_default_schedule("cg"), O.schedule("cg")
+        else:
+            sg = g.gse_default_schedule("cg", l=30, t=10, m=10)
+            so = O.schedule("cg", l=30, t=10, m=10)
+    xg, rg = g.gse_solve_cg(M, b, tol=1e-10, max_iters=5000, sched=sg)
+    xo, ro = O.cg(Rm, b, tol=1e-10, max_iters=5000, sched=so)
+    _cmp_reports(rg, ro)
+    assert rg["n_switches"] == ro.n_switches
+    for a, c in zip(rg["switch_iter"], ro.switch_iter):
+        assert abs(a - c) <= 2
+    assert rg["converged"] and rg["rel_residual_true"] <= 1e-10
+
+
+def test_cg_parity_c2_full_size(g):
+    """configs[1]: 3D Poisson 128^3 stepped CG to 1e-10 on one B200 vs the oracle."""
+    A = gi.poisson3d(128)
+    b = gi.ones_rhs(A)
+    M, R = enc_both(g, A, device_inputs=True)
+    bt = torch.from_numpy(b).cuda()
+    xg, rg = g.gse_solve_cg(M, bt, tol=1e-10, sched=g.gse_default_schedule("cg"))
+    O.set_threads(0)
+    xo, ro = O.cg(R, b, tol=1e-10, sched=O.schedule("cg"))
+    _cmp_reports(rg, ro)
+    assert rg["iters_per_level"][0] == rg["iterations"]  # head-exact: level 1 only
+    # independent property: true residual of the GPU solution with the oracle FP64 SpMV
+    F = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+    res = np.linalg.norm(b - O.spmv_fp64(F, xg.cpu().numpy())) / np.linalg.norm(b)
+    assert res <= 1e-10 * 1.001
+
+
+def test_cg_breakdown_abort(g):
+    A = gi.from_dense(np.array([[1.0, 0.0], [0.0, -1.0]]))
+    M = g.gse_fp64_matrix(A.row_ptr, A.col, A.val, 2, 2)
+    x, r = g.gse_solve_cg(M, np.array([1.0, 1.0]), tol=1e-10)
+    assert r["status"] == g.GSE_NUMERICAL_ABORT
+
+
+@pytest.mark.parametrize("mode", ["fp64", "stepped", "stepped_scaled"])
+def test_gmres_parity(g, mode):
+    A = gi.convdiff3d(16)
+    b = gi.ones_rhs(A)
+    if mode == "fp64":
+        M = g.gse_fp64_matrix(A.row_ptr, A.col, A.val, A.rows, A.cols)
+        Rm = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+        sg, so = None, None
+    else:
+        M, Rm = enc_both(g, A)
+        if mode == "stepped":
+            sg, so = g.gse_default_schedule("gmres"), O.schedule("gmres")
+        else:
+            sg = g.gse_default_schedule("gmres", l=30, t=10, m=10)
+            so = O.schedule("gmres", l=30, t=10, m=10)
+    xg, rg = g.gse_solve_gmres(M, b, tol=1e-10, sched=sg)
+    xo, ro = O.gmres(Rm, b, tol=1e-10, sched=so)
+    _cmp_reports(rg, ro)
+    assert rg["n_switches"] == ro.n_switches
+    assert rg["converged"] and rg["rel_residual_true"] <= 1e-10
+
+
+def test_gmres_small_exact(g):
+    A = gi.from_dense(np.array([[2.0]]))
+    M = g.gse_fp64_matrix(A.row_ptr, A.col, A.val, 1, 1)
+    x, r = g.gse_solve_gmres(M, np.array([4.0]), tol=1e-12)
+    assert r["converged"] and r["iterations"] == 1 and abs(x[0] - 2.0) < 1e-15
+
+
+def test_solver_x0_and_host_device_paths(g):
+    A = gi.poisson2d(16, "varcoef")
+    b = gi.ones_rhs(A)
+    M, R = enc_both(g, A)
+    x0 = gi.uniform_vec(A.rows, seed=3)
+    xh, rh = g.gse_solve_cg(M, b, x=x0.copy(), tol=1e-10, sched=g.fixed_schedule(3))
+    xd, rd = g.gse_solve_cg(M, torch.from_numpy(b).cuda(), x=torch.from_numpy(x0.copy()).cuda(),
+                            tol=1e-10, sched=g.fixed_schedule(3))
+    assert rh["iterations"] == rd["iterations"]
+    assert np.array_equal(xh, xd.cpu().numpy())  # deterministic reductions
+    xo, ro = O.cg(R, b, x0=x0, tol=1e-10, sched=O.fixed_schedule(3))
+    _cmp_reports(rh, ro)
