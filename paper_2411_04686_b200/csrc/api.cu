@@ -21,10 +21,28 @@ static void* (*g_alloc)(size_t, void*, void*) = nullptr;
 static void (*g_free)(void*, void*, void*) = nullptr;
 static void* g_ctx = nullptr;
 
+// The default stream-ordered pool returns freed memory to the OS at every synchronisation
+// (release threshold 0), which turns each encode / solver-workspace allocation into fresh
+// page mapping (milliseconds).  Keep freed blocks cached in the pool instead.
+static void keep_pool_cached() {
+  static bool done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
+  done[dev] = true;
+}
+
 void* dev_alloc(size_t bytes, cudaStream_t s) {
   if (bytes == 0) bytes = 16;
   bytes = (bytes + 255) & ~(size_t)255;
   if (g_alloc) return g_alloc(bytes, (void*)s, g_ctx);
+  keep_pool_cached();
   void* p = nullptr;
   if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) {
     cudaGetLastError();

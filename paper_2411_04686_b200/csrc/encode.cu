@@ -12,6 +12,8 @@
 //                   signed zero (R2); d > 63 -> signed zero (R3); split head/tail1/tail2
 //                   (P:163); EI into the column index or the side array.
 #include <cub/cub.cuh>
+#include <cstdlib>
+#include <cstring>
 #include <thrust/iterator/counting_iterator.h>
 
 #include "decode.cuh"
@@ -254,8 +256,59 @@ static int grid_for(int64_t n, int threads, int dev) {
   return (int)(g < 1 ? 1 : g);
 }
 
+// per 32-row group: non-zeros and longest row -> mode statistics
+__global__ void k_group_stats(const uint32_t* __restrict__ rp, int64_t rows,
+                              unsigned long long* __restrict__ acc) {
+  const int64_t ng = (rows + RW_ROWS - 1) / RW_ROWS;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long heavy = 0, wsum = 0, mx = 0, span = 0;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += stride) {
+    const int64_t r0 = g * RW_ROWS;
+    const int64_t r1 = r0 + RW_ROWS < rows ? r0 + RW_ROWS : rows;
+    uint32_t m = 0;
+    for (int64_t r = r0; r < r1; ++r) m = max(m, rp[r + 1] - rp[r]);
+    // staged span of the group: [rp[r0] & ~7, rp[r1]) rounded up to 8-element units
+    const uint32_t sp = ((rp[r1] - (rp[r0] & ~7u)) + 7u) & ~7u;
+    span = max(span, (unsigned long long)sp);
+    heavy += (sp > (uint32_t)RW_TILE) ? 1 : 0;
+    wsum += (unsigned long long)RW_ROWS * m;
+    mx = max(mx, (unsigned long long)m);
+  }
+  if (heavy) atomicAdd(&acc[0], heavy);
+  if (wsum) atomicAdd(&acc[1], wsum);
+  if (mx) atomicMax(&acc[2], mx);
+  if (span) atomicMax(&acc[3], span);
+}
+
+static void choose_mode(Matrix& M) {
+  // Row-walk needs every group staged (no heavy group) and little divergence between the
+  // 32 rows of a group; otherwise the strided-products kernel balances the load.
+  const char* env = getenv("GSE_SPMV_MODE");
+  const bool rw_ok = M.heavy_groups == 0 && M.rows > 0 && M.ei_in_column;
+  int mode = (rw_ok && M.rw_efficiency >= 0.6) ? SPMV_RW : SPMV_SP;
+  if (env && !strcmp(env, "sp")) mode = SPMV_SP;
+  if (env && !strcmp(env, "rw") && rw_ok) mode = SPMV_RW;
+  M.spmv_mode = mode;
+}
+
 gse_status build_partition(Matrix& M, cudaStream_t s) {
   M.n_blocks = 0;
+  M.n_groups = (M.rows + RW_ROWS - 1) / RW_ROWS;
+  if (M.rows > 0) {
+    unsigned long long* acc = dev_alloc_n<unsigned long long>(4, s);
+    if (!acc) return GSE_ERR_OOM;
+    GSE_CUDA_TRY(cudaMemsetAsync(acc, 0, 32, s));
+    k_group_stats<<<grid_for(M.n_groups, 256, M.device), 256, 0, s>>>(M.row_ptr, M.rows, acc);
+    unsigned long long h[4];
+    GSE_CUDA_TRY(cudaMemcpyAsync(h, acc, 32, cudaMemcpyDeviceToHost, s));
+    GSE_CUDA_TRY(cudaStreamSynchronize(s));
+    dev_free(acc, s);
+    M.heavy_groups = (int64_t)h[0];
+    M.rw_efficiency = h[1] ? (double)M.nnz / (double)h[1] : 0.0;
+    M.max_row_len = (int64_t)h[2];
+    M.rw_span = (int64_t)h[3];
+  }
+  choose_mode(M);
   if (M.rows == 0) {
     M.blocks = dev_alloc_n<BlockDesc>(1, s);
     if (!M.blocks) return GSE_ERR_OOM;
@@ -308,14 +361,26 @@ static gse_status convert_row_ptr(Matrix& M, const void* d_row_ptr, int rp64, cu
 void build_decode_table(Matrix& M) {
   memset(&M.htab, 0, sizeof(M.htab));
   const int sL[3] = {48, 32, 0};
-  int emax = 0;
+  int emax = 0, emin = 1 << 30;
   for (int i = 0; i < M.table_len; ++i) {
     const int E = M.table[i];
     emax = E > emax ? E : emax;
+    emin = E < emin ? E : emin;
     for (int L = 0; L < 3; ++L) {
       M.htab.d64[L][i] = (long long)(E - 1086 + sL[L]) * (1LL << 52);
       M.htab.d32[L][i] = (E - 1086 + sL[L]) * (1 << 23);
+      M.htab.sc64[L][i] = ldexp(1.0, E - 1086 + sL[L]);
+      const int k32 = E - 1086 + sL[L];
+      M.htab.sc32[L][i] = (k32 >= -126 && k32 <= 127) ? ldexpf(1.0f, k32) : 0.0f;
     }
+  }
+  // FP64 multiply form: a nonzero D_L is >= 1, so D_L * 2^(E - 1086 + s_L) is exact and
+  // normal (no flush can occur, R11) iff E - 1086 + s_L >= -1022, i.e. E >= 16 / 32 / 64
+  // at levels 1 / 2 / 3.  FP32: the same with the FP32 normal range (>= 2^-126).
+  const int emin_fast64[3] = {16, 32, 64};
+  for (int L = 0; L < 3; ++L) {
+    M.htab.fast64[L] = (M.table_len > 0 && emin >= emin_fast64[L]) ? 1 : 0;
+    M.htab.fast32[L] = (M.table_len > 0 && emin - 1086 + sL[L] >= -126) ? 1 : 0;
   }
   // FP32 accumulation is defined iff every decodable value is < 2^128 (R20): the largest
   // true exponent is E_max - 1 - 1023 <= 127.

@@ -13,16 +13,22 @@
 namespace gse {
 
 // ---------------------------------------------------------------- SpMV partition constants
-// A "block" (one CTA of the SpMV kernel) covers a run of consecutive rows whose starts fall
-// in one CHUNK of the nnz stream (rows <= LMAX nnz), or a single long row (> LMAX nnz).
-// Short blocks hold < CHUNK + LMAX + 7 <= TILE nnz (8-aligned), so one pass of
-// SPMV_THREADS x VEC = TILE slots covers them.
-constexpr int SPMV_THREADS = 256;
-constexpr int VEC = 8;
-constexpr int TILE = SPMV_THREADS * VEC;  // 2048
-constexpr uint32_t LMAX = 256;
-constexpr uint32_t CHUNK = 1784;  // CHUNK + LMAX + 6 <= TILE
-static_assert(CHUNK + LMAX + 6 <= TILE, "short block must fit one pass");
+// A "warp block" (the unit one warp of the SpMV kernel processes) covers a run of
+// consecutive rows whose starts fall in one CHUNK of the nnz stream, all of length <= LMAX,
+// or a single long row (> LMAX nnz).  A short block holds <= CHUNK - 1 + LMAX <= WTILE
+// non-zeros, so one pass of 32 lanes x EPL elements covers it.
+constexpr int SPMV_THREADS = 256;            // 8 independent warps per CTA
+constexpr int SPMV_WARPS = SPMV_THREADS / 32;
+constexpr int EPL = 8;                       // elements per lane per pass
+constexpr int WTILE = 32 * EPL;              // 256 non-zeros per warp pass
+constexpr uint32_t LMAX = 64;
+constexpr uint32_t CHUNK = 192;
+static_assert(CHUNK - 1 + LMAX <= WTILE, "short warp block must fit one pass");
+// Row-walk mode (regular matrices, e.g. stencils): groups of 32 consecutive rows, the
+// group's planes staged into warp-private shared memory with 16-byte loads, lane = row.
+constexpr int RW_ROWS = 32;
+constexpr int RW_TILE = 1024;  // max staged span (8-aligned non-zeros) of a row-walk group
+enum SpmvMode : int { SPMV_SP = 0, SPMV_RW = 1 };
 constexpr int NNZ_PAD = 8;  // plane allocations padded to a multiple of 8 elements (+8)
 
 struct BlockDesc {
@@ -35,6 +41,11 @@ struct BlockDesc {
 struct DecodeTable {
   long long d64[3][64];  // (E - 1086 + s_L) << 52
   int d32[3][64];        // (E - 1086 + s_L) << 23 (FP32 accumulation)
+  // multiply form used by the SpMV when no decoded value can underflow (E >= 16 / 32 / 64
+  // at levels 1 / 2 / 3 for FP64; E - 1086 + s_L >= -126 for FP32): |v| = D_L * scale.
+  double sc64[3][64];
+  float sc32[3][64];
+  int fast64[3], fast32[3];
 };
 
 struct SolverWs;  // solvers.cu
@@ -58,6 +69,12 @@ struct Matrix {
   double* val = nullptr;        // [nnz_pad] FP64 kind
   BlockDesc* blocks = nullptr;  // [n_blocks + 1]
   int64_t n_blocks = 0;
+  int spmv_mode = SPMV_SP;      // chosen at encode from the row-length statistics
+  int64_t n_groups = 0;         // ceil(rows / 32)
+  int64_t heavy_groups = 0;     // groups with > RW_TILE non-zeros
+  int64_t max_row_len = 0;
+  int64_t rw_span = 0;          // max staged span of a group (sizes the RW smem stages)
+  double rw_efficiency = 0.0;   // sum(len) / sum over groups of 32 * max(len)
   DecodeTable* dtab = nullptr;  // device copy
   DecodeTable htab;             // host copy
   SolverWs* ws = nullptr;

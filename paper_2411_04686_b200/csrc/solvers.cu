@@ -18,6 +18,7 @@
 //    cycle (kernels early-exit once the cycle is stopped).  The host only handles events:
 //    level switch with residual replacement (R15), verification with A_3 (R16).
 #include <cmath>
+#include <mutex>
 #include <vector>
 
 #include "gse_internal.cuh"
@@ -429,6 +430,40 @@ __global__ void __launch_bounds__(256) k_gm_xupdate(const SolveCtrl* __restrict_
 
 
 // ---------------------------------------------------------------- workspace
+// Pinned host mirrors of the control block and the capture streams are process-wide
+// caches: cudaMallocHost / cudaStreamCreate cost milliseconds, and a matrix (with its
+// solver workspace) may be created per solve.
+static std::mutex g_cache_mu;
+static std::vector<SolveCtrl*> g_pinned_free;
+static cudaStream_t g_cap_stream[64] = {nullptr};
+
+static SolveCtrl* pinned_ctrl_get() {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  if (!g_pinned_free.empty()) {
+    SolveCtrl* p = g_pinned_free.back();
+    g_pinned_free.pop_back();
+    return p;
+  }
+  SolveCtrl* p = nullptr;
+  if (cudaMallocHost(&p, sizeof(SolveCtrl)) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+static void pinned_ctrl_put(SolveCtrl* p) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_pinned_free.push_back(p);
+}
+
+static cudaStream_t capture_stream(int dev) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!g_cap_stream[dev]) cudaStreamCreateWithFlags(&g_cap_stream[dev], cudaStreamNonBlocking);
+  return g_cap_stream[dev];
+}
+
 static gse_status ensure_ws(Matrix& M, int64_t ring_t, int gm_restart, cudaStream_t s) {
   SolverWs*& ws = M.ws;
   const int64_t n = M.rows;
@@ -451,8 +486,9 @@ static gse_status ensure_ws(Matrix& M, int64_t ring_t, int gm_restart, cudaStrea
         !ws->ticket || !ws->ctrl)
       return GSE_ERR_OOM;
     GSE_CUDA_TRY(cudaMemsetAsync(ws->ticket, 0, 16, s));
-    GSE_CUDA_TRY(cudaMallocHost(&ws->hctrl, sizeof(SolveCtrl)));
-    GSE_CUDA_TRY(cudaStreamCreateWithFlags(&ws->cap_stream, cudaStreamNonBlocking));
+    ws->hctrl = pinned_ctrl_get();
+    ws->cap_stream = capture_stream(M.device);
+    if (!ws->hctrl || !ws->cap_stream) return GSE_ERR_CUDA;
     GSE_CUDA_TRY(cudaEventCreate(&ws->ev0));
     GSE_CUDA_TRY(cudaEventCreate(&ws->ev1));
   }
@@ -485,8 +521,7 @@ void free_solver_ws(Matrix& M) {
     if (p) dev_free(p, s);
   if (ws->ticket) dev_free(ws->ticket, s);
   if (ws->ctrl) dev_free(ws->ctrl, s);
-  if (ws->hctrl) cudaFreeHost(ws->hctrl);
-  if (ws->cap_stream) cudaStreamDestroy(ws->cap_stream);
+  if (ws->hctrl) pinned_ctrl_put(ws->hctrl);
   if (ws->ev0) cudaEventDestroy(ws->ev0);
   if (ws->ev1) cudaEventDestroy(ws->ev1);
   delete ws;

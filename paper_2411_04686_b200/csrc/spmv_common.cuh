@@ -1,0 +1,207 @@
+// spmv_common.cuh -- shared pieces of the two SpMV kernels (spmv_sp.cu: strided products
+// for irregular rows; spmv_rw.cu: row walk over staged planes for regular rows).
+#pragma once
+#include <cstdint>
+
+#include "decode.cuh"
+#include "gse_internal.cuh"
+
+namespace gse {
+
+__device__ __forceinline__ uint32_t ld_nc_u32(const uint32_t* p) {
+  uint32_t r;
+  asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_nc_u16(const uint16_t* p) {
+  unsigned short r;
+  asm("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_nc_u8(const uint8_t* p) {
+  unsigned short r;
+  asm("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=h"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double ld_nc_f64(const double* p) {
+  double r;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+  uint4 r;
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint2 ld_nc_v2(const void* p) {
+  uint2 r;
+  asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+
+template <class T>
+struct SpmvParams {
+  const BlockDesc* __restrict__ blocks;
+  const uint32_t* __restrict__ row_ptr;
+  const uint32_t* __restrict__ col_ei;
+  const uint8_t* __restrict__ side;
+  const uint16_t* __restrict__ head;
+  const uint16_t* __restrict__ tail1;
+  const uint32_t* __restrict__ tail2;
+  const double* __restrict__ val;
+  uint32_t n_blocks;  // SP warp blocks
+  uint32_t rows;
+  uint32_t n_groups;  // RW 32-row groups
+  uint32_t rw_stage;  // RW: elements per staging buffer (>= max group span, multiple of 16)
+  int ei_shift;       // 32 - ei_bits
+  uint32_t col_mask;  // (1 << (32 - ei_bits)) - 1, or ~0u
+  const T* __restrict__ x;
+  T* __restrict__ y;
+  double* partials;
+  unsigned* ticket;
+  double* dot_result;
+  const int* stop;    // optional: skip the launch when *stop != 0 (GMRES cycle graphs)
+  long long d64[64];  // decode deltas of the launched level (integer form, FP64)
+  int d32[64];        // (integer form, FP32)
+  double sc64[64];    // multiply-form scales when the table allows it (FAST)
+  float sc32[64];
+};
+
+// Level-L value of one element.  FAST: |v| = D_L * scale -- exact and never underflowing
+// for this table (build_decode_table), so it equals the bit-exact integer form of
+// decode.cuh on every value except the sign of a zero significand (+0 vs -0), which cannot
+// change a row sum that has a nonzero term.
+template <int L, bool FAST>
+__device__ __forceinline__ double dec64(uint32_t h, uint32_t t1, uint32_t t2,
+                                        const long long* sd, const double* sc, uint32_t ei) {
+  if constexpr (FAST) {
+    const uint32_t neg = h & 0x8000u;
+    double m;
+    if constexpr (L == 1) {
+      const int D = (int)(h & 0x7FFFu);
+      m = (double)(neg ? -D : D);
+    } else if constexpr (L == 2) {
+      const int D = (int)(((h & 0x7FFFu) << 16) | t1);
+      m = (double)(neg ? -D : D);
+    } else {
+      const uint64_t D = ((uint64_t)(h & 0x7FFFu) << 48) | ((uint64_t)t1 << 32) | t2;
+      m = __ull2double_rz(D);
+      m = neg ? -m : m;
+    }
+    return m * sc[ei];
+  } else {
+    if constexpr (L == 1)
+      return decode_l1(h, sd[ei]);
+    else if constexpr (L == 2)
+      return decode_l2(h, t1, sd[ei]);
+    else
+      return decode_l3(h, t1, t2, sd[ei]);
+  }
+}
+
+template <int L, bool FAST>
+__device__ __forceinline__ float dec32(uint32_t h, uint32_t t1, uint32_t t2, const int* sd,
+                                       const float* sc, uint32_t ei) {
+  if constexpr (FAST) {
+    float m;
+    if constexpr (L == 1)
+      m = (float)(int)(h & 0x7FFFu);
+    else if constexpr (L == 2)
+      m = __uint2float_rz(((h & 0x7FFFu) << 16) | t1);
+    else
+      m = __ull2float_rz(((uint64_t)(h & 0x7FFFu) << 48) | ((uint64_t)t1 << 32) | t2);
+    m = (h & 0x8000u) ? -m : m;
+    return m * sc[ei];
+  } else {
+    if constexpr (L == 1)
+      return decode_f32_u32(h & 0x7FFFu, sd[ei], h);
+    else if constexpr (L == 2)
+      return decode_f32_u32(((h & 0x7FFFu) << 16) | t1, sd[ei], h);
+    else
+      return decode_f32(((uint64_t)(h & 0x7FFFu) << 48) | ((uint64_t)t1 << 32) | t2, sd[ei], h);
+  }
+}
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, o);
+  return v;  // lane 0 holds the sum (fixed tree)
+}
+
+// CTA-wide sum of one value per warp (lane 0's), fixed order; then the last CTA to arrive
+// sums all CTA partials in index order -> deterministic scalar.
+__device__ __forceinline__ void finalize_dot(double wsum, double* partials, unsigned* ticket,
+                                             double* result) {
+  __shared__ double red[SPMV_WARPS];
+  __shared__ unsigned s_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[warp] = wsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < SPMV_WARPS; ++i) s += red[i];
+    partials[blockIdx.x] = s;
+    __threadfence();
+    s_last = (atomicAdd(ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double acc = 0.0;
+  for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) acc += __ldcg(partials + i);
+  acc = warp_sum(acc);
+  __syncthreads();
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < SPMV_WARPS; ++i) s += red[i];
+    *result = s;
+    *ticket = 0u;
+  }
+}
+
+// stage the per-EI decode constants into shared memory (once per CTA)
+template <int L, class T>
+__device__ __forceinline__ void stage_tables(const SpmvParams<T>& p, long long* sd64, int* sd32,
+                                             double* sc64, float* sc32) {
+  if constexpr (L >= 1) {
+    const int t = threadIdx.x;
+    if (t < 64) {
+      if constexpr (sizeof(T) == 8) {
+        sd64[t] = p.d64[t];
+        sc64[t] = p.sc64[t];
+      } else {
+        sd32[t] = p.d32[t];
+        sc32[t] = p.sc32[t];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// launchers (spmv_sp.cu / spmv_rw.cu)
+template <class T>
+void launch_sp(const Matrix& M, int level, bool dot, bool fast, const SpmvParams<T>& p,
+               cudaStream_t s);
+template <class T>
+void launch_rw(const Matrix& M, int level, bool dot, bool fast, const SpmvParams<T>& p,
+               cudaStream_t s);
+
+// persistent grid size for a kernel: resident CTAs per SM x SMs, capped by the work units
+template <class K>
+inline int persistent_grid(K kernel, int device, int64_t units_per_cta_work, int* cache) {
+  const int dev = device < 64 ? device : 0;
+  if (!cache[dev]) {
+    int blocks = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kernel, SPMV_THREADS, 0);
+    cache[dev] = (blocks < 1 ? 1 : blocks) * num_sms(device);
+  }
+  const int64_t want = (units_per_cta_work + SPMV_WARPS - 1) / SPMV_WARPS;
+  int g = (int)(want < cache[dev] ? want : cache[dev]);
+  return g < 1 ? 1 : g;
+}
+
+}  // namespace gse

@@ -1,0 +1,264 @@
+// spmv_rw.cu -- "row walk" SpMV kernel for regular row lengths (stencils: configs 1, 2, 4,
+// 5).  SURVEY 8(a) a4-a6; paper Alg. spmv -- a row per thread group -- and
+// P:212 for levels 2-3.
+//
+//  * persistent CTAs of 8 independent warps; a warp owns groups of 32 consecutive rows
+//    with a fixed grid stride;
+//  * the planes of the NEXT group (only the requested ones) are fetched into a
+//    warp-private shared-memory stage by TMA bulk copies (cp.async.bulk, one elected lane,
+//    completion on a per-stage mbarrier) while the warp computes the current group: DRAM
+//    latency leaves the dependent chain and no registers hold data in flight;
+//  * lane = row: lane r walks its row in storage order (the oracle's summation order)
+//    with up to 8 x-gathers in flight.  For stencil rows the j-th element of 32 consecutive
+//    rows lies on one diagonal, so a warp-wide gather touches ~2 lines;
+//  * chosen at encode when every group's span fits RW_TILE and the row lengths of a group
+//    are close (Matrix::rw_efficiency >= 0.6); otherwise spmv_sp.cu runs.
+#include "spmv_common.cuh"
+
+namespace gse {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// bytes per staged element at level L (col_ei + requested planes; L = 0: FP64 values)
+template <int L>
+__host__ __device__ constexpr uint32_t rw_elem_bytes() {
+  return 4u + (L == 0 ? 8u : 0u) + (L >= 1 ? 2u : 0u) + (L >= 2 ? 2u : 0u) + (L == 3 ? 4u : 0u);
+}
+
+template <int L>
+struct Stage {
+  uint32_t* col;
+  double* val;
+  uint16_t* head;
+  uint16_t* tail1;
+  uint32_t* tail2;
+  __device__ Stage(unsigned char* base, uint32_t N) {
+    unsigned char* q = base;
+    col = reinterpret_cast<uint32_t*>(q);
+    q += 4 * N;
+    val = reinterpret_cast<double*>(q);
+    if (L == 0) q += 8 * N;
+    head = reinterpret_cast<uint16_t*>(q);
+    if (L >= 1) q += 2 * N;
+    tail1 = reinterpret_cast<uint16_t*>(q);
+    if (L >= 2) q += 2 * N;
+    tail2 = reinterpret_cast<uint32_t*>(q);
+  }
+};
+
+template <int L, class T>
+__device__ __forceinline__ void issue_stage(const SpmvParams<T>& p, const Stage<L>& st,
+                                            uint64_t* bar, uint32_t s, uint32_t e) {
+  const uint32_t base = s & ~7u;
+  const uint32_t n = (e > base) ? ((e - base + 7u) & ~7u) : 0u;  // 8-element units
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads -> async writes
+  mbar_arrive_expect_tx(bar, n * rw_elem_bytes<L>());
+  if (n == 0) return;
+  bulk_g2s(st.col, p.col_ei + base, 4 * n, bar);
+  if constexpr (L == 0) bulk_g2s(st.val, p.val + base, 8 * n, bar);
+  if constexpr (L >= 1) bulk_g2s(st.head, p.head + base, 2 * n, bar);
+  if constexpr (L >= 2) bulk_g2s(st.tail1, p.tail1 + base, 2 * n, bar);
+  if constexpr (L == 3) bulk_g2s(st.tail2, p.tail2 + base, 4 * n, bar);
+}
+
+template <int L, bool DOT, bool FAST, class T>
+__global__ void __launch_bounds__(SPMV_THREADS) k_spmv_rw(const SpmvParams<T> p) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ __align__(8) uint64_t bars[SPMV_WARPS][2];
+  __shared__ long long sd64[64];
+  __shared__ int sd32[64];
+  __shared__ double sc64[64];
+  __shared__ float sc32[64];
+  if (p.stop && *p.stop) return;
+  stage_tables<L>(p, sd64, sd32, sc64, sc32);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t N = p.rw_stage;
+  const uint32_t SB = N * rw_elem_bytes<L>();
+  unsigned char* wbase = dsm + (size_t)warp * 2 * SB;
+  // (stage views are rebuilt from dsm each time so the compiler keeps them in the shared
+  // window and emits LDS; an array of pointer structs indexed at run time decays to
+  // generic 64-bit loads)
+  if (lane == 0) {
+    mbar_init(&bars[warp][0], 1);
+    mbar_init(&bars[warp][1], 1);
+    // make the initialised barriers visible to the async (TMA) proxy; a cluster-scope
+    // fence.mbarrier_init would also invalidate L1 (CCTL.IVALL)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncwarp();
+
+  double dacc = 0.0;
+  const uint32_t ng = p.n_groups, rows = p.rows;
+  const uint32_t W = gridDim.x * SPMV_WARPS;
+  uint32_t g = blockIdx.x * SPMV_WARPS + warp;
+  auto bounds = [&](uint32_t grp, uint32_t& a, uint32_t& b) {
+    a = 0;
+    b = 0;
+    if (grp < ng) {
+      const uint32_t r = grp * RW_ROWS + lane;
+      if (r < rows) {
+        a = p.row_ptr[r];
+        b = p.row_ptr[r + 1];
+      }
+    }
+  };
+  auto span = [&](uint32_t grp, uint32_t a, uint32_t b, uint32_t& s, uint32_t& e) {
+    const uint32_t r0 = grp * RW_ROWS;
+    const uint32_t nr = rows - r0 < (uint32_t)RW_ROWS ? rows - r0 : (uint32_t)RW_ROWS;
+    s = __shfl_sync(0xFFFFFFFFu, a, 0);
+    e = __shfl_sync(0xFFFFFFFFu, b, nr - 1);
+  };
+  uint32_t ra, rb, na, nb;
+  bounds(g, ra, rb);
+  bounds(g + W, na, nb);
+  if (g < ng) {
+    uint32_t s, e;
+    span(g, ra, rb, s, e);
+    if (lane == 0) issue_stage<L>(p, Stage<L>(wbase, N), &bars[warp][0], s, e);
+  }
+  uint32_t it = 0;
+  for (; g < ng; g += W, ++it) {
+    const uint32_t cur = it & 1u;
+    uint32_t n2a, n2b;
+    bounds(g + 2 * W, n2a, n2b);  // row bounds two groups ahead
+    if (g + W < ng) {             // planes of the next group -> the other stage
+      uint32_t s, e;
+      span(g + W, na, nb, s, e);
+      if (lane == 0) issue_stage<L>(p, Stage<L>(wbase + (cur ^ 1u) * SB, N), &bars[warp][cur ^ 1u], s, e);
+    }
+    const uint32_t r0 = g * RW_ROWS;
+    const uint32_t nr = rows - r0 < (uint32_t)RW_ROWS ? rows - r0 : (uint32_t)RW_ROWS;
+    const uint32_t base = __shfl_sync(0xFFFFFFFFu, ra, 0) & ~7u;
+    mbar_wait(&bars[warp][cur], (it >> 1) & 1u);
+    const Stage<L> st(wbase + cur * SB, N);
+    if (lane < nr) {
+      const uint32_t j1 = rb - base;
+      T sum = 0;
+      for (uint32_t j = ra - base; j < j1; j += 8) {
+        uint32_t c[8];
+        T xv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) c[q] = (j + q < j1) ? st.col[j + q] : 0u;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) xv[q] = (j + q < j1) ? __ldg(p.x + (c[q] & p.col_mask)) : (T)0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (j + q < j1) {
+            const uint32_t jj = j + q;
+            T prod;
+            if constexpr (L == 0) {
+              prod = (T)__dmul_rn(st.val[jj], (double)xv[q]);
+            } else {
+              const uint32_t ei = __funnelshift_rc(c[q], 0u, p.ei_shift);
+              const uint32_t h = st.head[jj];
+              const uint32_t t1 = L >= 2 ? (uint32_t)st.tail1[jj] : 0u;
+              const uint32_t t2 = L == 3 ? st.tail2[jj] : 0u;
+              if constexpr (sizeof(T) == 8)
+                prod = __dmul_rn(dec64<L, FAST>(h, t1, t2, sd64, sc64, ei), xv[q]);
+              else
+                prod = __fmul_rn(dec32<L, FAST>(h, t1, t2, sd32, sc32, ei), xv[q]);
+            }
+            sum += prod;
+          }
+        }
+      }
+      p.y[r0 + lane] = sum;
+      if (DOT) dacc += (double)p.x[r0 + lane] * (double)sum;
+    }
+    __syncwarp();
+    ra = na;
+    rb = nb;
+    na = n2a;
+    nb = n2b;
+  }
+  if constexpr (DOT) finalize_dot(warp_sum(dacc), p.partials, p.ticket, p.dot_result);
+}
+
+template <int L, bool DOT, bool FAST, class T>
+static void go(const Matrix& M, const SpmvParams<T>& p, cudaStream_t s) {
+  static int cache[64] = {0};
+  static uint32_t cache_smem[64] = {0};
+  const int dev = M.device < 64 ? M.device : 0;
+  const size_t smem = (size_t)SPMV_WARPS * 2 * p.rw_stage * rw_elem_bytes<L>();
+  auto kern = k_spmv_rw<L, DOT, FAST, T>;
+  if (cache_smem[dev] != smem) {  // occupancy depends on the stage size of this matrix
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int blocks = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, SPMV_THREADS, smem);
+    cache[dev] = (blocks < 1 ? 1 : blocks) * num_sms(M.device);
+    cache_smem[dev] = (uint32_t)smem;
+  }
+  const int64_t want = (M.n_groups + SPMV_WARPS - 1) / SPMV_WARPS;
+  int g = (int)(want < cache[dev] ? want : cache[dev]);
+  if (g < 1) g = 1;
+  kern<<<g, SPMV_THREADS, smem, s>>>(p);
+}
+
+template <int L, bool DOT, class T>
+static void go_l(const Matrix& M, bool fast, const SpmvParams<T>& p, cudaStream_t s) {
+  if (fast)
+    go<L, DOT, true, T>(M, p, s);
+  else
+    go<L, DOT, false, T>(M, p, s);
+}
+
+template <bool DOT, class T>
+static void go_dot(const Matrix& M, int level, bool fast, const SpmvParams<T>& p,
+                   cudaStream_t s) {
+  if (M.kind == GSE_KIND_FP64) {
+    go<0, DOT, false, T>(M, p, s);
+  } else if (level == 1) {
+    go_l<1, DOT, T>(M, fast, p, s);
+  } else if (level == 2) {
+    go_l<2, DOT, T>(M, fast, p, s);
+  } else {
+    go_l<3, DOT, T>(M, fast, p, s);
+  }
+}
+
+template <>
+void launch_rw<double>(const Matrix& M, int level, bool dot, bool fast,
+                       const SpmvParams<double>& p, cudaStream_t s) {
+  if (dot)
+    go_dot<true, double>(M, level, fast, p, s);
+  else
+    go_dot<false, double>(M, level, fast, p, s);
+}
+
+template <>
+void launch_rw<float>(const Matrix& M, int level, bool dot, bool fast,
+                      const SpmvParams<float>& p, cudaStream_t s) {
+  (void)dot;
+  go_dot<false, float>(M, level, fast, p, s);
+}
+
+}  // namespace gse

@@ -58,7 +58,7 @@ def long_rows_matrix():
     """rows of length 0, 1, LMAX-1, LMAX, LMAX+1, 2047, 2048, 2049, 5000 (DESIGN.md partition
     boundaries) interleaved with short rows."""
     rng = np.random.default_rng(9)
-    lens = [3, 0, 1, 255, 256, 257, 7, 2047, 2048, 2049, 0, 5000, 2, 1784, 1785, 6]
+    lens = [3, 0, 1, 63, 64, 65, 191, 192, 193, 255, 256, 257, 7, 2047, 2048, 2049, 0, 5000, 2, 6]
     lens = lens * 3
     cols = 6000
     rp = np.zeros(len(lens) + 1, np.int64)
