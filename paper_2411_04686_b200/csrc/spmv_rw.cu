@@ -3,14 +3,17 @@
 // P:212 for levels 2-3.
 //
 //  * persistent CTAs of 8 independent warps; a warp owns groups of 32 consecutive rows
-//    with a fixed grid stride;
+//    (lane = row) with a fixed grid stride;
 //  * the planes of the NEXT group (only the requested ones) are fetched into a
 //    warp-private shared-memory stage by TMA bulk copies (cp.async.bulk, one elected lane,
 //    completion on a per-stage mbarrier) while the warp computes the current group: DRAM
 //    latency leaves the dependent chain and no registers hold data in flight;
-//  * lane = row: lane r walks its row in storage order (the oracle's summation order)
-//    with up to 8 x-gathers in flight.  For stencil rows the j-th element of 32 consecutive
-//    rows lies on one diagonal, so a warp-wide gather touches ~2 lines;
+//  * lane = row: a lane walks its row in storage order (the oracle's summation order) with
+//    8 x-gathers in flight, branch-free (slots past the row end contribute exact zeros).
+//    For stencil rows the j-th element of 32 consecutive rows lies on one diagonal, so a
+//    warp-wide gather touches ~2 cache lines;
+//  * decode in multiply form with the sign folded into a shared scale table
+//    (|v| = D_L * scale[EI], exact for the tables that allow it, see build_decode_table);
 //  * chosen at encode when every group's span fits RW_TILE and the row lengths of a group
 //    are close (Matrix::rw_efficiency >= 0.6); otherwise spmv_sp.cu runs.
 #include "spmv_common.cuh"
@@ -54,6 +57,9 @@ __host__ __device__ constexpr uint32_t rw_elem_bytes() {
   return 4u + (L == 0 ? 8u : 0u) + (L >= 1 ? 2u : 0u) + (L >= 2 ? 2u : 0u) + (L == 3 ? 4u : 0u);
 }
 
+// views of one staging buffer (rebuilt from the dynamic shared array each time, so the
+// compiler keeps them in the shared window and emits LDS; pointer structs indexed at run
+// time decay to generic 64-bit loads)
 template <int L>
 struct Stage {
   uint32_t* col;
@@ -90,6 +96,75 @@ __device__ __forceinline__ void issue_stage(const SpmvParams<T>& p, const Stage<
   if constexpr (L == 3) bulk_g2s(st.tail2, p.tail2 + base, 4 * n, bar);
 }
 
+// sum of one row, elements [j0, j1) of the stage, in storage order
+template <int L, bool FAST, class T>
+__device__ __forceinline__ T walk_row(const SpmvParams<T>& p, const Stage<L>& st, uint32_t j0,
+                                      uint32_t j1, const double* ssc64, const float* ssc32,
+                                      const long long* sd64, const int* sd32,
+                                      const double* sc64, const float* sc32) {
+  T sum = 0;
+  for (uint32_t j = j0; j < j1; j += 8) {
+    uint32_t c[8], h[8], t1[8], t2[8];
+    double v0[8];
+    bool ok[8];
+    T xv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      ok[q] = j + q < j1;
+      const uint32_t jj = ok[q] ? j + q : j0;
+      c[q] = st.col[jj];
+      if constexpr (L == 0) v0[q] = st.val[jj];
+      if constexpr (L >= 1) h[q] = st.head[jj];
+      if constexpr (L >= 2) t1[q] = st.tail1[jj];
+      if constexpr (L == 3) t2[q] = st.tail2[jj];
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) xv[q] = __ldg(p.x + (c[q] & p.col_mask));
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      T prod;
+      if constexpr (L == 0) {
+        prod = (T)__dmul_rn(ok[q] ? v0[q] : 0.0, (double)xv[q]);
+      } else if constexpr (FAST) {
+        const uint32_t idx = (__funnelshift_rc(c[q], 0u, p.ei_shift) << 1) | (h[q] >> 15);
+        if constexpr (L == 1) {
+          const uint32_t D = ok[q] ? (h[q] & 0x7FFFu) : 0u;
+          if constexpr (sizeof(T) == 8)
+            prod = __dmul_rn(__dmul_rn((double)D, ssc64[idx]), xv[q]);
+          else
+            prod = __fmul_rn(__fmul_rn((float)D, ssc32[idx]), xv[q]);
+        } else if constexpr (L == 2) {
+          const uint32_t D = ok[q] ? (((h[q] & 0x7FFFu) << 16) | t1[q]) : 0u;
+          if constexpr (sizeof(T) == 8)
+            prod = __dmul_rn(__dmul_rn((double)D, ssc64[idx]), xv[q]);
+          else
+            prod = __fmul_rn(__fmul_rn(__uint2float_rz(D), ssc32[idx]), xv[q]);
+        } else {
+          const uint64_t D =
+              ok[q] ? (((uint64_t)(h[q] & 0x7FFFu) << 48) | ((uint64_t)t1[q] << 32) | t2[q])
+                    : 0ull;
+          if constexpr (sizeof(T) == 8)
+            prod = __dmul_rn(__dmul_rn(__ull2double_rz(D), ssc64[idx]), xv[q]);
+          else
+            prod = __fmul_rn(__fmul_rn(__ull2float_rz(D), ssc32[idx]), xv[q]);
+        }
+      } else {
+        const uint32_t ei = __funnelshift_rc(c[q], 0u, p.ei_shift);
+        const uint32_t tt1 = L >= 2 ? t1[q] : 0u, tt2 = L == 3 ? t2[q] : 0u;
+        if constexpr (sizeof(T) == 8) {
+          const double a = dec64<L, false>(h[q], tt1, tt2, sd64, sc64, ei);
+          prod = __dmul_rn(ok[q] ? a : 0.0, xv[q]);
+        } else {
+          const float a = dec32<L, false>(h[q], tt1, tt2, sd32, sc32, ei);
+          prod = __fmul_rn(ok[q] ? a : 0.0f, xv[q]);
+        }
+      }
+      sum += prod;
+    }
+  }
+  return sum;
+}
+
 template <int L, bool DOT, bool FAST, class T>
 __global__ void __launch_bounds__(SPMV_THREADS) k_spmv_rw(const SpmvParams<T> p) {
   extern __shared__ __align__(128) unsigned char dsm[];
@@ -98,15 +173,22 @@ __global__ void __launch_bounds__(SPMV_THREADS) k_spmv_rw(const SpmvParams<T> p)
   __shared__ int sd32[64];
   __shared__ double sc64[64];
   __shared__ float sc32[64];
+  __shared__ double ssc64[128];  // sign-folded scales: [2 EI + sign] = (sign ? -1 : 1) scale
+  __shared__ float ssc32[128];
   if (p.stop && *p.stop) return;
+  if (threadIdx.x < 128) {
+    const int t = threadIdx.x;
+    if constexpr (sizeof(T) == 8)
+      ssc64[t] = (t & 1) ? -p.sc64[t >> 1] : p.sc64[t >> 1];
+    else
+      ssc32[t] = (t & 1) ? -p.sc32[t >> 1] : p.sc32[t >> 1];
+  }
   stage_tables<L>(p, sd64, sd32, sc64, sc32);
+  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t N = p.rw_stage;
   const uint32_t SB = N * rw_elem_bytes<L>();
   unsigned char* wbase = dsm + (size_t)warp * 2 * SB;
-  // (stage views are rebuilt from dsm each time so the compiler keeps them in the shared
-  // window and emits LDS; an array of pointer structs indexed at run time decays to
-  // generic 64-bit loads)
   if (lane == 0) {
     mbar_init(&bars[warp][0], 1);
     mbar_init(&bars[warp][1], 1);
@@ -120,85 +202,48 @@ __global__ void __launch_bounds__(SPMV_THREADS) k_spmv_rw(const SpmvParams<T> p)
   const uint32_t ng = p.n_groups, rows = p.rows;
   const uint32_t W = gridDim.x * SPMV_WARPS;
   uint32_t g = blockIdx.x * SPMV_WARPS + warp;
-  auto bounds = [&](uint32_t grp, uint32_t& a, uint32_t& b) {
-    a = 0;
-    b = 0;
+  // row bounds of a group of 32 rows: a = rp[r0 + lane], c = rp[r0 + 32] (indices clamped
+  // to rows: rows past the end are empty); a row's end is the next lane's start
+  struct Bounds {
+    uint32_t a, c;
+  };
+  auto bounds = [&](uint32_t grp) {
+    Bounds B{0, 0};
     if (grp < ng) {
-      const uint32_t r = grp * RW_ROWS + lane;
-      if (r < rows) {
-        a = p.row_ptr[r];
-        b = p.row_ptr[r + 1];
-      }
+      const uint32_t r0 = grp * RW_ROWS;
+      B.a = p.row_ptr[min(r0 + lane, rows)];
+      B.c = p.row_ptr[min(r0 + RW_ROWS, rows)];
     }
+    return B;
   };
-  auto span = [&](uint32_t grp, uint32_t a, uint32_t b, uint32_t& s, uint32_t& e) {
-    const uint32_t r0 = grp * RW_ROWS;
-    const uint32_t nr = rows - r0 < (uint32_t)RW_ROWS ? rows - r0 : (uint32_t)RW_ROWS;
-    s = __shfl_sync(0xFFFFFFFFu, a, 0);
-    e = __shfl_sync(0xFFFFFFFFu, b, nr - 1);
-  };
-  uint32_t ra, rb, na, nb;
-  bounds(g, ra, rb);
-  bounds(g + W, na, nb);
-  if (g < ng) {
-    uint32_t s, e;
-    span(g, ra, rb, s, e);
-    if (lane == 0) issue_stage<L>(p, Stage<L>(wbase, N), &bars[warp][0], s, e);
-  }
+  Bounds cur_b = bounds(g), nxt_b = bounds(g + W);
+  if (g < ng && lane == 0)
+    issue_stage<L>(p, Stage<L>(wbase, N), &bars[warp][0], cur_b.a, cur_b.c);
   uint32_t it = 0;
   for (; g < ng; g += W, ++it) {
     const uint32_t cur = it & 1u;
-    uint32_t n2a, n2b;
-    bounds(g + 2 * W, n2a, n2b);  // row bounds two groups ahead
-    if (g + W < ng) {             // planes of the next group -> the other stage
-      uint32_t s, e;
-      span(g + W, na, nb, s, e);
-      if (lane == 0) issue_stage<L>(p, Stage<L>(wbase + (cur ^ 1u) * SB, N), &bars[warp][cur ^ 1u], s, e);
+    const Bounds n2_b = bounds(g + 2 * W);  // two groups ahead
+    if (g + W < ng) {                       // planes of the next group -> the other stage
+      const uint32_t s = __shfl_sync(0xFFFFFFFFu, nxt_b.a, 0);
+      if (lane == 0)
+        issue_stage<L>(p, Stage<L>(wbase + (cur ^ 1u) * SB, N), &bars[warp][cur ^ 1u], s,
+                       nxt_b.c);
     }
     const uint32_t r0 = g * RW_ROWS;
-    const uint32_t nr = rows - r0 < (uint32_t)RW_ROWS ? rows - r0 : (uint32_t)RW_ROWS;
-    const uint32_t base = __shfl_sync(0xFFFFFFFFu, ra, 0) & ~7u;
+    const uint32_t base = __shfl_sync(0xFFFFFFFFu, cur_b.a, 0) & ~7u;
+    uint32_t ea = __shfl_down_sync(0xFFFFFFFFu, cur_b.a, 1);
+    if (lane == 31) ea = cur_b.c;
     mbar_wait(&bars[warp][cur], (it >> 1) & 1u);
     const Stage<L> st(wbase + cur * SB, N);
-    if (lane < nr) {
-      const uint32_t j1 = rb - base;
-      T sum = 0;
-      for (uint32_t j = ra - base; j < j1; j += 8) {
-        uint32_t c[8];
-        T xv[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) c[q] = (j + q < j1) ? st.col[j + q] : 0u;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) xv[q] = (j + q < j1) ? __ldg(p.x + (c[q] & p.col_mask)) : (T)0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          if (j + q < j1) {
-            const uint32_t jj = j + q;
-            T prod;
-            if constexpr (L == 0) {
-              prod = (T)__dmul_rn(st.val[jj], (double)xv[q]);
-            } else {
-              const uint32_t ei = __funnelshift_rc(c[q], 0u, p.ei_shift);
-              const uint32_t h = st.head[jj];
-              const uint32_t t1 = L >= 2 ? (uint32_t)st.tail1[jj] : 0u;
-              const uint32_t t2 = L == 3 ? st.tail2[jj] : 0u;
-              if constexpr (sizeof(T) == 8)
-                prod = __dmul_rn(dec64<L, FAST>(h, t1, t2, sd64, sc64, ei), xv[q]);
-              else
-                prod = __fmul_rn(dec32<L, FAST>(h, t1, t2, sd32, sc32, ei), xv[q]);
-            }
-            sum += prod;
-          }
-        }
-      }
-      p.y[r0 + lane] = sum;
-      if (DOT) dacc += (double)p.x[r0 + lane] * (double)sum;
+    const T sa = walk_row<L, FAST, T>(p, st, cur_b.a - base, ea - base, ssc64, ssc32, sd64, sd32,
+                                      sc64, sc32);
+    if (r0 + lane < rows) {
+      p.y[r0 + lane] = sa;
+      if (DOT) dacc += (double)p.x[r0 + lane] * (double)sa;
     }
     __syncwarp();
-    ra = na;
-    rb = nb;
-    na = n2a;
-    nb = n2b;
+    cur_b = nxt_b;
+    nxt_b = n2_b;
   }
   if constexpr (DOT) finalize_dot(warp_sum(dacc), p.partials, p.ticket, p.dot_result);
 }

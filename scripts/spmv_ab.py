@@ -20,9 +20,14 @@ def timeit(fn, reps=30):
     torch.cuda.synchronize()
     return statistics.median(s.elapsed_time(e) for s, e in evs) * 1e-3
 
-mats = {"c2": lambda: gi.poisson3d(128)}
+mats = {f"p3d_{N}": (lambda N=N: gi.poisson3d(N)) for N in [int(v) for v in os.environ.get("AB_NS", "128").split(",")]}
 if os.environ.get("AB_POWERLAW", "1") == "1":
     mats["pl2m"] = lambda: gi.powerlaw_spd(int(os.environ.get("AB_PL_N", "2000000")))
+src = torch.empty(256 * 1024 * 1024, dtype=torch.float32, device="cuda")
+dst = torch.empty_like(src)
+tcopy = timeit(lambda: dst.copy_(src), 10)
+print(json.dumps({"tag": tag, "copy_GBps": round(2 * src.numel() * 4 / tcopy / 1e9, 1)}), flush=True)
+del src, dst
 for name, mk in mats.items():
     A = mk()
     dev = lambda a: torch.from_numpy(a).cuda()
