@@ -123,7 +123,7 @@ struct DotOut {
   double* result = nullptr;     // deterministic sum of partials
 };
 gse_status launch_spmv(const Matrix& M, int level, const double* x, double* y,
-                       const DotOut* dot, cudaStream_t s);
+                       const DotOut* dot, cudaStream_t s, const int* stop = nullptr);
 gse_status launch_spmv_guarded(const Matrix& M, int level, const double* x, double* y,
                                const int* stop, cudaStream_t s);
 gse_status launch_spmv_f32(const Matrix& M, int level, const float* x, float* y,

@@ -18,6 +18,7 @@
 //    cycle (kernels early-exit once the cycle is stopped).  The host only handles events:
 //    level switch with residual replacement (R15), verification with A_3 (R16).
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -203,17 +204,39 @@ __global__ void __launch_bounds__(256) k_cg_update(SolveCtrl* __restrict__ c, do
                                                    const double* __restrict__ p,
                                                    const double* __restrict__ q, int64_t n,
                                                    double* partials, unsigned* ticket,
-                                                   cudaGraphConditionalHandle handle) {
+                                                   cudaGraphConditionalHandle handle,
+                                                   int in_graph) {
+  if (c->event != EV_NONE) return;  // host-driven mode: iterations after an event are no-ops
   const double pq = c->pq, rr = c->rr;
   const bool ok = (pq > 0.0) && isfinite(pq);
   const double alpha = rr / pq;
   double acc = 0.0;
   if (ok) {
-    GRID_LOOP(i, n) {
-      x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
-      const double ri = __dsub_rn(r[i], __dmul_rn(alpha, q[i]));
-      r[i] = ri;
-      acc = __dadd_rn(acc, __dmul_rn(ri, ri));
+    // ILP: 4 elements (stride apart) loaded before any is computed; per-thread element order
+    // (and so the reduction order) is the plain grid-stride order
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += 4 * stride) {
+      double xv[4], pv[4], rv[4], qv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t j = i + k * stride;
+        if (j < n) {
+          xv[k] = x[j];
+          pv[k] = p[j];
+          rv[k] = r[j];
+          qv[k] = q[j];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t j = i + k * stride;
+        if (j < n) {
+          x[j] = __dadd_rn(xv[k], __dmul_rn(alpha, pv[k]));
+          const double ri = __dsub_rn(rv[k], __dmul_rn(alpha, qv[k]));
+          r[j] = ri;
+          acc = __dadd_rn(acc, __dmul_rn(ri, ri));
+        }
+      }
     }
   }
   double tot;
@@ -241,7 +264,7 @@ __global__ void __launch_bounds__(256) k_cg_update(SolveCtrl* __restrict__ c, do
     }
     c->event = ev;
     if (ev != EV_NONE) {
-      cudaGraphSetConditional(handle, 0u);
+      if (in_graph) cudaGraphSetConditional(handle, 0u);
     } else {
       c->beta = tot / rr;
       c->rr = tot;
@@ -255,7 +278,23 @@ __global__ void __launch_bounds__(256) k_cg_xpay(const SolveCtrl* __restrict__ c
                                                  const double* __restrict__ r, int64_t n) {
   if (c->event != EV_NONE) return;
   const double beta = c->beta;
-  GRID_LOOP(i, n) p[i] = __dadd_rn(r[i], __dmul_rn(beta, p[i]));
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += 4 * stride) {
+    double pv[4], rv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t j = i + k * stride;
+      if (j < n) {
+        pv[k] = p[j];
+        rv[k] = r[j];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t j = i + k * stride;
+      if (j < n) p[j] = __dadd_rn(rv[k], __dmul_rn(beta, pv[k]));
+    }
+  }
 }
 
 // ---------------------------------------------------------------- GMRES kernels
@@ -470,7 +509,7 @@ static gse_status ensure_ws(Matrix& M, int64_t ring_t, int gm_restart, cudaStrea
   if (!ws) {
     ws = new SolverWs();
     ws->n = n;
-    ws->vgrid = num_sms(M.device) * 4;
+    ws->vgrid = num_sms(M.device) * 8;
     const size_t nn = (size_t)(n > 0 ? n : 1);
     ws->x = dev_alloc_n<double>(nn, s);
     ws->r = dev_alloc_n<double>(nn, s);
@@ -552,6 +591,16 @@ static DotOut dot_to(SolverWs* ws, double* target) {
   return d;
 }
 
+// GSE_NO_GRAPH=1: drive solver iterations from the host instead of CUDA graphs (ncu cannot
+// profile kernel nodes of graphs with conditional nodes; also a fallback)
+static bool no_graph() {
+  static const bool v = [] {
+    const char* e = getenv("GSE_NO_GRAPH");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
 // ---------------------------------------------------------------- CG graph per level
 static gse_status build_cg_graph(Matrix& M, int level) {
   SolverWs* ws = M.ws;
@@ -573,9 +622,9 @@ static gse_status build_cg_graph(Matrix& M, int level) {
                                              cudaStreamCaptureModeRelaxed));
   const int64_t n = M.rows;
   DotOut d = dot_to(ws, &ws->ctrl->pq);
-  gse_status rc = launch_spmv(M, level, ws->p, ws->q, &d, cs);
+  gse_status rc = launch_spmv(M, level, ws->p, ws->q, &d, cs, &ws->ctrl->event);
   k_cg_update<<<ws->vgrid, 256, 0, cs>>>(ws->ctrl, ws->ring, ws->x, ws->r, ws->p, ws->q, n,
-                                         ws->partials, ws->ticket, h);
+                                         ws->partials, ws->ticket, h, 1);
   k_cg_xpay<<<ws->vgrid, 256, 0, cs>>>(ws->ctrl, ws->p, ws->r, n);
   cudaGraph_t captured;
   cudaError_t e = cudaStreamEndCapture(cs, &captured);
@@ -702,9 +751,26 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
       status = GSE_NOT_CONVERGED;
       break;
     }
-    rc = build_cg_graph(M, level);
-    if (rc != GSE_OK) return rc;
-    GSE_CUDA_TRY(cudaGraphLaunch(ws->cg_exec[level - 1], s));
+    if (no_graph()) {
+      // host-driven iterations (profiling / fallback): batches of 16, then poll the event
+      do {
+        DotOut d = dot_to(ws, &ws->ctrl->pq);
+        for (int b = 0; b < 16; ++b) {
+          rc = launch_spmv(M, level, ws->p, ws->q, &d, s, &ws->ctrl->event);
+          if (rc != GSE_OK) return rc;
+          k_cg_update<<<ws->vgrid, 256, 0, s>>>(ws->ctrl, ws->ring, ws->x, ws->r, ws->p, ws->q,
+                                                n, ws->partials, ws->ticket, 0, 0);
+          k_cg_xpay<<<ws->vgrid, 256, 0, s>>>(ws->ctrl, ws->p, ws->r, n);
+        }
+        GSE_CUDA_TRY(cudaGetLastError());
+        rc = read_ctrl(ws, s);
+        if (rc != GSE_OK) return rc;
+      } while (hc->event == EV_NONE);
+    } else {
+      rc = build_cg_graph(M, level);
+      if (rc != GSE_OK) return rc;
+      GSE_CUDA_TRY(cudaGraphLaunch(ws->cg_exec[level - 1], s));
+    }
     rc = read_ctrl(ws, s);
     if (rc != GSE_OK) return rc;
     iter = hc->iter;

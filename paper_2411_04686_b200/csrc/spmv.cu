@@ -71,12 +71,14 @@ static bool empty_matrix(const Matrix& M) {
 }
 
 gse_status launch_spmv(const Matrix& M, int level, const double* x, double* y,
-                       const DotOut* dot, cudaStream_t s) {
+                       const DotOut* dot, cudaStream_t s, const int* stop) {
   if (empty_matrix(M)) {
     if (dot) GSE_CUDA_TRY(cudaMemsetAsync(dot->result, 0, sizeof(double), s));
     return GSE_OK;
   }
-  dispatch<double>(M, level, dot != nullptr, make_params<double>(M, level, x, y, dot), s);
+  SpmvParams<double> p = make_params<double>(M, level, x, y, dot);
+  p.stop = stop;
+  dispatch<double>(M, level, dot != nullptr, p, s);
   GSE_CUDA_TRY(cudaGetLastError());
   return GSE_OK;
 }

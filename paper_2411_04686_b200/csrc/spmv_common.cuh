@@ -8,36 +8,54 @@
 
 namespace gse {
 
+// Matrix planes are streamed once per SpMV: every plane load carries an L2 evict-first
+// policy so the 126 MB L2 keeps the solver vectors (x, r, p, q) resident instead
+// (DESIGN.md "L2 residency").
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ uint32_t ld_nc_u32(const uint32_t* p) {
   uint32_t r;
-  asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+      : "=r"(r)
+      : "l"(p), "l"(l2_evict_first()));
   return r;
 }
 __device__ __forceinline__ uint32_t ld_nc_u16(const uint16_t* p) {
   unsigned short r;
-  asm("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(r) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;"
+      : "=h"(r)
+      : "l"(p), "l"(l2_evict_first()));
   return r;
 }
 __device__ __forceinline__ uint32_t ld_nc_u8(const uint8_t* p) {
   unsigned short r;
-  asm("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=h"(r) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u8 %0, [%1], %2;"
+      : "=h"(r)
+      : "l"(p), "l"(l2_evict_first()));
   return r;
 }
 __device__ __forceinline__ double ld_nc_f64(const double* p) {
   double r;
-  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+      : "=d"(r)
+      : "l"(p), "l"(l2_evict_first()));
   return r;
 }
 __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
   uint4 r;
-  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
       : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-      : "l"(p));
+      : "l"(p), "l"(l2_evict_first()));
   return r;
 }
 __device__ __forceinline__ uint2 ld_nc_v2(const void* p) {
   uint2 r;
-  asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+      : "=r"(r.x), "=r"(r.y)
+      : "l"(p), "l"(l2_evict_first()));
   return r;
 }
 
