@@ -210,12 +210,39 @@ gse_status gse_set_allocator(void* (*alloc)(size_t bytes, void* stream, void* ct
  * exchange the halo and allreduce dot products over NCCL.
  * ------------------------------------------------------------------------------------- */
 gse_status gse_nccl_unique_id(void* id128 /* host, 128 bytes */);
+/* NCCL backend: one process per GPU; rank 0 creates the unique id, the caller broadcasts
+ * it (e.g. torch.distributed), every rank calls this collectively.  nranks <= 16. */
 gse_status gse_dist_create(const void* nccl_unique_id /* host, 128 B */, int rank, int nranks,
                            int device, gse_dist* out);
+/* Thread backend: nranks host threads of ONE process (one GPU or several), collectives by
+ * device copies + events + host barriers.  Runs the same distributed code path as NCCL and
+ * is how the multi-rank path is tested on a single GPU.  Create the group once, then each
+ * thread calls gse_dist_create_thread with its rank; all collective calls must be made by
+ * all threads in the same order. */
+gse_status gse_dist_thread_group_create(int nranks, void** group);
+void gse_dist_thread_group_free(void* group);
+gse_status gse_dist_create_thread(void* group, int rank, int device, gse_dist* out);
+/* Collective over the ranks of D: encode this rank's row block.  local_rows holds rows
+ * [row_begin, row_begin + local_rows->rows) of a square global_rows x global_rows matrix
+ * with GLOBAL column ids (host or device arrays); ranks own contiguous blocks in rank order.
+ * The exponent histogram is summed over ranks before the table is chosen, so all ranks
+ * share one table (R21); columns are renumbered locally (owned first, then the halo in
+ * global order).  gse_spmv on the result takes / returns the rank's slices (x: local_rows
+ * entries); gse_solve_cg runs the distributed CG (halo exchange + allreduces); GMRES and
+ * FP32 accumulation are single-GPU only (GSE_ERR_WRONG_FORMAT). */
 gse_status gse_encode_dist(gse_dist D, const gse_csr_f64* local_rows, int64_t row_begin,
                            int64_t global_rows, const gse_encode_opts* opts, gse_matrix* out,
                            void* stream);
 void gse_dist_free(gse_dist D);
+/* Host-only planning helper (no GPU, no communicator): the local renumbering used by
+ * gse_encode_dist.  col[nnz] global ids of a rank owning rows [row_begin, row_begin+n_local);
+ * rank_rows[nranks+1] = row offsets of all ranks.  Outputs: local_col[nnz] (owned -> col -
+ * row_begin, halo -> n_local + position in halo_cols), *n_halo, halo_cols[<= nnz] (sorted
+ * unique non-owned ids; may be NULL), recv_count[nranks] (halo entries owned by each rank;
+ * may be NULL). */
+gse_status gse_dist_plan(int64_t nnz, const int32_t* col, int64_t row_begin, int64_t n_local,
+                         int nranks, const int64_t* rank_rows, int32_t* local_col,
+                         int64_t* n_halo, int64_t* halo_cols, int64_t* recv_count);
 
 #ifdef __cplusplus
 }

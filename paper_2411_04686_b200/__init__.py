@@ -35,7 +35,8 @@ ABI_SYMBOLS = (
     "gse_decode", "gse_spmv", "gse_spmv_f32acc", "gse_default_schedule", "gse_solve_cg",
     "gse_solve_gmres", "gse_matrix_free", "gse_status_string", "gse_last_error_detail",
     "gse_set_allocator", "gse_nccl_unique_id", "gse_dist_create", "gse_encode_dist",
-    "gse_dist_free",
+    "gse_dist_free", "gse_dist_thread_group_create", "gse_dist_thread_group_free",
+    "gse_dist_create_thread", "gse_dist_plan",
 )
 
 
@@ -109,6 +110,17 @@ def _declare(L):
     L.gse_status_string.restype = C.c_char_p
     L.gse_last_error_detail.argtypes = []
     L.gse_last_error_detail.restype = C.c_char_p
+    L.gse_nccl_unique_id.argtypes = [vp]
+    L.gse_dist_create.argtypes = [vp, i32, i32, i32, C.POINTER(vp)]
+    L.gse_dist_thread_group_create.argtypes = [i32, C.POINTER(vp)]
+    L.gse_dist_thread_group_free.argtypes = [vp]
+    L.gse_dist_thread_group_free.restype = None
+    L.gse_dist_create_thread.argtypes = [vp, i32, i32, C.POINTER(vp)]
+    L.gse_encode_dist.argtypes = [vp, C.POINTER(CsrF64), i64, i64, C.POINTER(EncodeOpts),
+                                  C.POINTER(vp), vp]
+    L.gse_dist_free.argtypes = [vp]
+    L.gse_dist_free.restype = None
+    L.gse_dist_plan.argtypes = [i64, vp, i64, i64, i32, vp, vp, C.POINTER(i64), vp, vp]
 
 
 _declare(_lib)
@@ -373,6 +385,87 @@ def gse_solve_gmres(A: Matrix, b, x=None, tol: float = 1e-10, restart: int = 30,
 
 def gse_matrix_free(A: Matrix):
     A.close()
+
+
+# ---------------------------------------------------------------------------- multi-GPU
+class Dist:
+    """Owning handle of a gse_dist (one rank's communicator)."""
+
+    def __init__(self, handle: int):
+        self.handle = C.c_void_p(handle)
+
+    def close(self):
+        if self.handle and self.handle.value:
+            _lib.gse_dist_free(self.handle)
+            self.handle = C.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def gse_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib.gse_nccl_unique_id(buf), "gse_nccl_unique_id")
+    return buf.raw
+
+
+def gse_dist_create(unique_id: bytes, rank: int, nranks: int, device: int) -> Dist:
+    """NCCL backend (one process per GPU)."""
+    buf = C.create_string_buffer(bytes(unique_id), 128)
+    out = C.c_void_p()
+    _check(_lib.gse_dist_create(buf, rank, nranks, device, C.byref(out)), "gse_dist_create")
+    return Dist(out.value)
+
+
+def gse_dist_thread_group_create(nranks: int) -> int:
+    out = C.c_void_p()
+    _check(_lib.gse_dist_thread_group_create(nranks, C.byref(out)),
+           "gse_dist_thread_group_create")
+    return out.value
+
+
+def gse_dist_thread_group_free(group: int):
+    _lib.gse_dist_thread_group_free(C.c_void_p(group))
+
+
+def gse_dist_create_thread(group: int, rank: int, device: int = 0) -> Dist:
+    """Thread backend: `rank` of a thread group in this process."""
+    out = C.c_void_p()
+    _check(_lib.gse_dist_create_thread(C.c_void_p(group), rank, device, C.byref(out)),
+           "gse_dist_create_thread")
+    return Dist(out.value)
+
+
+def gse_encode_dist(D: Dist, row_ptr, col_idx, values, row_begin: int, global_rows: int,
+                    k_max: int = 8, stream=None) -> Matrix:
+    """Collective: encode this rank's row block (global column ids)."""
+    rows = int((row_ptr.numel() if _is_torch(row_ptr) else row_ptr.size) - 1)
+    A = _csr(rows, global_rows, row_ptr, col_idx, values)
+    opts = EncodeOpts(k_max, -1, 0, 0)
+    out = C.c_void_p()
+    _check(_lib.gse_encode_dist(D.handle, C.byref(A), row_begin, global_rows, C.byref(opts),
+                                C.byref(out), _stream(values, col_idx, row_ptr, stream=stream)),
+           "gse_encode_dist")
+    return Matrix(out.value)
+
+
+def gse_dist_plan(col, row_begin: int, n_local: int, rank_rows):
+    """Host-only local renumbering / halo plan (no GPU): returns (local_col, halo_cols,
+    recv_count) as numpy arrays."""
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    rr = np.ascontiguousarray(rank_rows, dtype=np.int64)
+    nranks = rr.size - 1
+    local = np.empty(max(col.size, 1), np.int32)
+    halo = np.empty(max(col.size, 1), np.int64)
+    recv = np.zeros(nranks, np.int64)
+    nh = C.c_int64()
+    _check(_lib.gse_dist_plan(col.size, col.ctypes.data, row_begin, n_local, nranks,
+                              rr.ctypes.data, local.ctypes.data, C.byref(nh), halo.ctypes.data,
+                              recv.ctypes.data), "gse_dist_plan")
+    return local[: col.size].copy(), halo[: nh.value].copy(), recv
 
 
 def lib():

@@ -195,7 +195,8 @@ static void destroy_matrix(Matrix& M) {
 }
 
 gse_status create_from_csr(const gse_csr_f64* A, int kind, int k_max, int device,
-                           gse_matrix* out, cudaStream_t s, Matrix** mout) {
+                           gse_matrix* out, cudaStream_t s, Matrix** mout, Comm* comm,
+                           const int32_t* local_col_host) {
   gse_status rc = check_csr(A);
   if (rc != GSE_OK) return rc;
   if (!out) {
@@ -213,7 +214,8 @@ gse_status create_from_csr(const gse_csr_f64* A, int kind, int k_max, int device
     rc = st.in((const long long*)A->row_ptr, (size_t)A->rows + 1, dev, (const long long**)&rp);
   else
     rc = st.in((const int*)A->row_ptr, (size_t)A->rows + 1, dev, (const int**)&rp);
-  if (rc == GSE_OK) rc = st.in(A->col_idx, (size_t)A->nnz, dev, &col);
+  if (rc == GSE_OK)
+    rc = st.in(local_col_host ? local_col_host : A->col_idx, (size_t)A->nnz, dev, &col);
   if (rc == GSE_OK) rc = st.in(A->values, (size_t)A->nnz, dev, &val);
   if (rc != GSE_OK) return rc;
   gse_matrix h = new gse_matrix_s();
@@ -224,7 +226,7 @@ gse_status create_from_csr(const gse_csr_f64* A, int kind, int k_max, int device
   M.nnz = A->nnz;
   M.k_max = k_max;
   if (kind == GSE_KIND_GSE)
-    rc = encode_matrix(M, *A, rp, A->row_ptr_64, col, val, s);
+    rc = encode_matrix(M, *A, rp, A->row_ptr_64, col, val, s, comm);
   else
     rc = fp64_matrix(M, rp, A->row_ptr_64, col, val, s);
   if (rc == GSE_OK) rc = st.finish();
@@ -321,11 +323,13 @@ gse_status gse_encode(const gse_csr_f64* A, const gse_encode_opts* opts, gse_mat
     set_error("sampled table extraction is not implemented (sample_block_rows must be 0)");
     return GSE_ERR_INVALID_ARG;
   }
-  return create_from_csr(A, GSE_KIND_GSE, o.k_max, o.device, out, (cudaStream_t)stream, nullptr);
+  return create_from_csr(A, GSE_KIND_GSE, o.k_max, o.device, out, (cudaStream_t)stream, nullptr,
+                         nullptr, nullptr);
 }
 
 gse_status gse_fp64_matrix(const gse_csr_f64* A, int device, gse_matrix* out, void* stream) {
-  return create_from_csr(A, GSE_KIND_FP64, 1, device, out, (cudaStream_t)stream, nullptr);
+  return create_from_csr(A, GSE_KIND_FP64, 1, device, out, (cudaStream_t)stream, nullptr, nullptr,
+                         nullptr);
 }
 
 gse_status gse_matrix_get_info(gse_matrix A, gse_matrix_info* info) {
@@ -419,11 +423,8 @@ gse_status gse_spmv(gse_matrix A, const double* x, double* y, int segments, void
     set_error("an FP64-CSR matrix is read at full precision only (segments = 3)");
     return GSE_ERR_WRONG_FORMAT;
   }
-  if (M.dist) {
-    set_error("distributed SpMV: use the dist entry points");
-    return GSE_ERR_WRONG_FORMAT;
-  }
-  if ((M.cols > 0 && !x) || (M.rows > 0 && !y)) {
+  const int64_t xlen = M.dist ? dist_n_local(M) : M.cols;  // dist: x is the rank's slice
+  if ((xlen > 0 && !x) || (M.rows > 0 && !y)) {
     set_error("x or y is NULL");
     return GSE_ERR_INVALID_ARG;
   }
@@ -432,9 +433,16 @@ gse_status gse_spmv(gse_matrix A, const double* x, double* y, int segments, void
   Staging st(s);
   const double* dx = nullptr;
   double* dy = nullptr;
-  gse_status rc = st.in(x, (size_t)M.cols, M.device, &dx);
+  gse_status rc = st.in(x, (size_t)xlen, M.device, &dx);
   if (rc == GSE_OK) rc = st.out(y, (size_t)M.rows, M.device, false, &dy);
   if (rc != GSE_OK) return rc;
+  if (M.dist) {  // owned entries -> x_ext, halo exchange, SpMV over the local column space
+    double* xe = dist_xext(M);
+    if (xlen) GSE_CUDA_TRY(cudaMemcpyAsync(xe, dx, 8 * xlen, cudaMemcpyDeviceToDevice, s));
+    rc = dist_halo_exchange(M, xe, s);
+    if (rc != GSE_OK) return rc;
+    dx = xe;
+  }
   rc = launch_spmv(M, segments, dx, dy, nullptr, s);
   if (rc != GSE_OK) return rc;
   rc = st.out_done(y, dy, (size_t)M.rows);
@@ -448,8 +456,8 @@ gse_status gse_spmv_f32acc(gse_matrix A, const float* x, float* y, int segments,
     return GSE_ERR_INVALID_ARG;
   }
   const Matrix& M = A->m;
-  if (M.kind != GSE_KIND_GSE) {
-    set_error("FP32 accumulation is defined for GSE matrices");
+  if (M.kind != GSE_KIND_GSE || M.dist) {
+    set_error("FP32 accumulation is defined for single-GPU GSE matrices");
     return GSE_ERR_WRONG_FORMAT;
   }
   if (!M.fp32_ok) {
@@ -483,9 +491,13 @@ static gse_status solve_common(gse_matrix A, const double* b, double* x, double 
     return GSE_ERR_INVALID_ARG;
   }
   Matrix& M = A->m;
-  if (M.rows != M.cols) {
+  if (!M.dist && M.rows != M.cols) {  // (a distributed matrix was checked square at encode)
     set_error("solvers need a square matrix");
     return GSE_ERR_DIM_MISMATCH;
+  }
+  if (M.dist && gmres) {
+    set_error("distributed GMRES is not implemented (distributed CG is)");
+    return GSE_ERR_WRONG_FORMAT;
   }
   if (!(tol > 0.0) || max_iters < 0 || (M.rows > 0 && (!b || !x))) {
     set_error("invalid tol (must be > 0), max_iters or NULL b/x");

@@ -1,30 +1,642 @@
-// dist.cu -- row-partitioned multi-GPU support.  Placeholder: the NCCL path
-// lands in a later commit; the entry points exist so the ABI is stable.
+// dist.cu -- row-partitioned multi-GPU execution (the paper is single-GPU).
+//
+// One process (or thread) per GPU rank.  A rank owns rows [row_begin, row_begin + n_local)
+// and keeps GLOBAL column ids only at encode time:
+//  * the shared-exponent table is global: the exponent histograms are summed over ranks
+//    before the table is selected (R21), so every rank encodes with the identical table;
+//  * columns are renumbered locally: owned -> [0, n_local), halo -> n_local + position in the
+//    sorted list of referenced non-owned columns (grouped by owner rank because ownership
+//    ranges are contiguous); the EI is embedded into the LOCAL index;
+//  * every SpMV packs the owned entries peers need and exchanges halos (NCCL grouped
+//    send/recv, or device copies in the thread backend) into x_ext[n_local ...];
+//  * dot products are local partials + an allreduce; all ranks see identical sums, so the
+//    residual monitor takes identical decisions everywhere without extra synchronisation.
+//
+// Two communication backends with one interface:
+//  * NcclComm: NCCL over NVLink / NVSwitch (one process per GPU, unique id bootstrap);
+//  * ThreadComm: P host threads in one process sharing one or more GPUs (streams + events +
+//    device copies).  It runs the identical distributed code path on a single GPU, which is
+//    how the P-rank CG is parity-tested on the one-GPU test box.
+#include <nccl.h>
+
+#include <algorithm>
+#include <condition_variable>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
 #include "gse_internal.cuh"
 
 namespace gse {
-struct DistCtx {};
-gse_status dist_halo_exchange(const Matrix&, double*, cudaStream_t) { return GSE_ERR_NCCL; }
-gse_status dist_allreduce_sum(const Matrix&, double*, int, cudaStream_t) { return GSE_ERR_NCCL; }
-void free_dist(Matrix& M) { M.dist = nullptr; }
+
+// ---------------------------------------------------------------- communicator interface
+struct Comm {
+  int rank = 0, nranks = 1, device = 0;
+  virtual ~Comm() {}
+  virtual gse_status allreduce_sum_f64(double* d, int count, cudaStream_t s) = 0;
+  virtual gse_status allreduce_sum_u64(unsigned long long* d, int count, cudaStream_t s) = 0;
+  // synchronous host-level helpers (setup only)
+  virtual gse_status host_allgather(int64_t v, std::vector<int64_t>& out) = 0;
+  virtual gse_status host_alltoallv(const std::vector<std::vector<int64_t>>& send,
+                                    std::vector<std::vector<int64_t>>& recv) = 0;
+  // halo exchange: send_buf[send_off[p] .. +send_cnt[p]) -> rank p; receive from rank p into
+  // recv_base + recv_off[p]
+  virtual gse_status exchange(const double* send_buf, const std::vector<int64_t>& send_cnt,
+                              const std::vector<int64_t>& send_off, double* recv_base,
+                              const std::vector<int64_t>& recv_cnt,
+                              const std::vector<int64_t>& recv_off, cudaStream_t s) = 0;
+};
+
+// ---------------------------------------------------------------- NCCL backend
+static gse_status nccl_status(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return GSE_OK;
+  set_error(std::string(what) + ": " + ncclGetErrorString(r));
+  return GSE_ERR_NCCL;
+}
+#define GSE_NCCL_TRY(expr)                                      \
+  do {                                                          \
+    gse_status _s = nccl_status((expr), #expr);                 \
+    if (_s != GSE_OK) return _s;                                \
+  } while (0)
+
+struct NcclComm : Comm {
+  ncclComm_t comm = nullptr;
+  cudaStream_t setup = nullptr;
+  ~NcclComm() override {
+    if (comm) ncclCommDestroy(comm);
+    if (setup) cudaStreamDestroy(setup);
+  }
+  gse_status allreduce_sum_f64(double* d, int count, cudaStream_t s) override {
+    GSE_NCCL_TRY(ncclAllReduce(d, d, count, ncclDouble, ncclSum, comm, s));
+    return GSE_OK;
+  }
+  gse_status allreduce_sum_u64(unsigned long long* d, int count, cudaStream_t s) override {
+    GSE_NCCL_TRY(ncclAllReduce(d, d, count, ncclUint64, ncclSum, comm, s));
+    return GSE_OK;
+  }
+  gse_status host_allgather(int64_t v, std::vector<int64_t>& out) override {
+    int64_t* buf = dev_alloc_n<int64_t>((size_t)nranks + 1, setup);
+    if (!buf) return GSE_ERR_OOM;
+    GSE_CUDA_TRY(cudaMemcpyAsync(buf + rank, &v, 8, cudaMemcpyHostToDevice, setup));
+    GSE_NCCL_TRY(ncclAllGather(buf + rank, buf, 1, ncclInt64, comm, setup));
+    out.assign(nranks, 0);
+    GSE_CUDA_TRY(cudaMemcpyAsync(out.data(), buf, 8 * nranks, cudaMemcpyDeviceToHost, setup));
+    GSE_CUDA_TRY(cudaStreamSynchronize(setup));
+    dev_free(buf, setup);
+    return GSE_OK;
+  }
+  gse_status host_alltoallv(const std::vector<std::vector<int64_t>>& send,
+                            std::vector<std::vector<int64_t>>& recv) override {
+    // counts first (every rank learns what it receives), then the payloads
+    recv.assign(nranks, {});
+    std::vector<int64_t> rc(nranks, 0);
+    std::vector<int64_t> mine(nranks);
+    for (int p = 0; p < nranks; ++p) mine[p] = (int64_t)send[p].size();
+    int64_t* dcnt = dev_alloc_n<int64_t>((size_t)nranks * nranks, setup);
+    if (!dcnt) return GSE_ERR_OOM;
+    GSE_CUDA_TRY(cudaMemcpyAsync(dcnt + (size_t)rank * nranks, mine.data(), 8 * nranks,
+                                 cudaMemcpyHostToDevice, setup));
+    GSE_NCCL_TRY(ncclAllGather(dcnt + (size_t)rank * nranks, dcnt, nranks, ncclInt64, comm, setup));
+    std::vector<int64_t> all((size_t)nranks * nranks);
+    GSE_CUDA_TRY(cudaMemcpyAsync(all.data(), dcnt, 8 * all.size(), cudaMemcpyDeviceToHost, setup));
+    GSE_CUDA_TRY(cudaStreamSynchronize(setup));
+    dev_free(dcnt, setup);
+    int64_t tot_s = 0, tot_r = 0;
+    for (int p = 0; p < nranks; ++p) {
+      rc[p] = all[(size_t)p * nranks + rank];
+      tot_s += mine[p];
+      tot_r += rc[p];
+    }
+    int64_t* sbuf = dev_alloc_n<int64_t>((size_t)tot_s + 1, setup);
+    int64_t* rbuf = dev_alloc_n<int64_t>((size_t)tot_r + 1, setup);
+    if (!sbuf || !rbuf) return GSE_ERR_OOM;
+    int64_t off = 0;
+    for (int p = 0; p < nranks; ++p) {
+      if (mine[p])
+        GSE_CUDA_TRY(cudaMemcpyAsync(sbuf + off, send[p].data(), 8 * mine[p],
+                                     cudaMemcpyHostToDevice, setup));
+      off += mine[p];
+    }
+    GSE_NCCL_TRY(ncclGroupStart());
+    int64_t so = 0, ro = 0;
+    for (int p = 0; p < nranks; ++p) {
+      if (mine[p]) GSE_NCCL_TRY(ncclSend(sbuf + so, mine[p], ncclInt64, p, comm, setup));
+      if (rc[p]) GSE_NCCL_TRY(ncclRecv(rbuf + ro, rc[p], ncclInt64, p, comm, setup));
+      so += mine[p];
+      ro += rc[p];
+    }
+    GSE_NCCL_TRY(ncclGroupEnd());
+    std::vector<int64_t> flat((size_t)tot_r);
+    if (tot_r)
+      GSE_CUDA_TRY(cudaMemcpyAsync(flat.data(), rbuf, 8 * tot_r, cudaMemcpyDeviceToHost, setup));
+    GSE_CUDA_TRY(cudaStreamSynchronize(setup));
+    dev_free(sbuf, setup);
+    dev_free(rbuf, setup);
+    ro = 0;
+    for (int p = 0; p < nranks; ++p) {
+      recv[p].assign(flat.begin() + ro, flat.begin() + ro + rc[p]);
+      ro += rc[p];
+    }
+    return GSE_OK;
+  }
+  gse_status exchange(const double* send_buf, const std::vector<int64_t>& send_cnt,
+                      const std::vector<int64_t>& send_off, double* recv_base,
+                      const std::vector<int64_t>& recv_cnt, const std::vector<int64_t>& recv_off,
+                      cudaStream_t s) override {
+    GSE_NCCL_TRY(ncclGroupStart());
+    for (int p = 0; p < nranks; ++p) {
+      if (p == rank) continue;
+      if (send_cnt[p])
+        GSE_NCCL_TRY(ncclSend(send_buf + send_off[p], send_cnt[p], ncclDouble, p, comm, s));
+      if (recv_cnt[p])
+        GSE_NCCL_TRY(ncclRecv(recv_base + recv_off[p], recv_cnt[p], ncclDouble, p, comm, s));
+    }
+    GSE_NCCL_TRY(ncclGroupEnd());
+    return GSE_OK;
+  }
+};
+
+// ---------------------------------------------------------------- thread backend
+struct ThreadGroup {
+  int n = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long generation = 0;
+  std::vector<const void*> ptr;   // per-rank published device pointers
+  std::vector<cudaEvent_t> ev;    // per-rank "published data ready" events
+  std::vector<cudaEvent_t> ev2;   // per-rank "done reading peers" events
+  std::vector<const std::vector<int64_t>*> vec;  // per-rank host vectors (setup)
+  std::vector<const std::vector<std::vector<int64_t>>*> vv;
+  std::vector<int64_t> scalar;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const long long gen = generation;
+    if (++arrived == n) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != gen; });
+    }
+  }
+};
+
+struct RankPtrs {
+  const double* p[16];
+};
+__global__ void k_sum_ranks(RankPtrs rp, int nranks, int count, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  double s = 0.0;
+  for (int r = 0; r < nranks; ++r) s += rp.p[r][i];  // rank order: deterministic
+  out[i] = s;
+}
+struct RankPtrsU {
+  const unsigned long long* p[16];
+};
+__global__ void k_sum_ranks_u64(RankPtrsU rp, int nranks, int count, unsigned long long* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  unsigned long long s = 0;
+  for (int r = 0; r < nranks; ++r) s += rp.p[r][i];
+  out[i] = s;
+}
+
+struct ThreadComm : Comm {
+  ThreadGroup* g = nullptr;
+  cudaEvent_t my_ev = nullptr, my_ev2 = nullptr;
+  double* tmp = nullptr;
+  int tmp_cap = 0;
+  ~ThreadComm() override {
+    if (my_ev) cudaEventDestroy(my_ev);
+    if (my_ev2) cudaEventDestroy(my_ev2);
+    if (tmp) cudaFree(tmp);
+  }
+  gse_status ensure_tmp(int count) {
+    if (count <= tmp_cap) return GSE_OK;
+    if (tmp) cudaFree(tmp);
+    tmp_cap = count < 4096 ? 4096 : count;
+    GSE_CUDA_TRY(cudaMalloc(&tmp, (size_t)tmp_cap * 8));
+    return GSE_OK;
+  }
+  // publish `p` (device) + an event on s; after all ranks published, s waits for everyone
+  void publish_and_wait(const void* p, cudaStream_t s) {
+    cudaEventRecord(my_ev, s);
+    {
+      std::lock_guard<std::mutex> lk(g->mu);
+      g->ptr[rank] = p;
+      g->ev[rank] = my_ev;
+    }
+    g->barrier();
+    for (int r = 0; r < nranks; ++r)
+      if (r != rank) cudaStreamWaitEvent(s, g->ev[r], 0);
+  }
+  // after reading peers' data: nobody may overwrite published buffers until all are done
+  void done_reading(cudaStream_t s) {
+    cudaEventRecord(my_ev2, s);
+    {
+      std::lock_guard<std::mutex> lk(g->mu);
+      g->ev2[rank] = my_ev2;
+    }
+    g->barrier();
+    for (int r = 0; r < nranks; ++r)
+      if (r != rank) cudaStreamWaitEvent(s, g->ev2[r], 0);
+    g->barrier();  // ev2 slots may be reused only after every rank enqueued its waits
+  }
+  gse_status allreduce_sum_f64(double* d, int count, cudaStream_t s) override {
+    gse_status rc = ensure_tmp(count);
+    if (rc != GSE_OK) return rc;
+    publish_and_wait(d, s);
+    RankPtrs rp{};
+    for (int r = 0; r < nranks; ++r) rp.p[r] = static_cast<const double*>(g->ptr[r]);
+    k_sum_ranks<<<(count + 255) / 256, 256, 0, s>>>(rp, nranks, count, tmp);
+    done_reading(s);
+    GSE_CUDA_TRY(cudaMemcpyAsync(d, tmp, (size_t)count * 8, cudaMemcpyDeviceToDevice, s));
+    return GSE_OK;
+  }
+  gse_status allreduce_sum_u64(unsigned long long* d, int count, cudaStream_t s) override {
+    gse_status rc = ensure_tmp(count);
+    if (rc != GSE_OK) return rc;
+    publish_and_wait(d, s);
+    RankPtrsU rp{};
+    for (int r = 0; r < nranks; ++r) rp.p[r] = static_cast<const unsigned long long*>(g->ptr[r]);
+    k_sum_ranks_u64<<<(count + 255) / 256, 256, 0, s>>>(rp, nranks, count,
+                                                        reinterpret_cast<unsigned long long*>(tmp));
+    done_reading(s);
+    GSE_CUDA_TRY(cudaMemcpyAsync(d, tmp, (size_t)count * 8, cudaMemcpyDeviceToDevice, s));
+    return GSE_OK;
+  }
+  gse_status host_allgather(int64_t v, std::vector<int64_t>& out) override {
+    {
+      std::lock_guard<std::mutex> lk(g->mu);
+      g->scalar[rank] = v;
+    }
+    g->barrier();
+    out = g->scalar;
+    g->barrier();
+    return GSE_OK;
+  }
+  gse_status host_alltoallv(const std::vector<std::vector<int64_t>>& send,
+                            std::vector<std::vector<int64_t>>& recv) override {
+    {
+      std::lock_guard<std::mutex> lk(g->mu);
+      g->vv[rank] = &send;
+    }
+    g->barrier();
+    recv.assign(nranks, {});
+    for (int p = 0; p < nranks; ++p) recv[p] = (*g->vv[p])[rank];
+    g->barrier();
+    return GSE_OK;
+  }
+  gse_status exchange(const double* send_buf, const std::vector<int64_t>& send_cnt,
+                      const std::vector<int64_t>& send_off, double* recv_base,
+                      const std::vector<int64_t>& recv_cnt, const std::vector<int64_t>& recv_off,
+                      cudaStream_t s) override {
+    {
+      std::lock_guard<std::mutex> lk(g->mu);
+      g->vec[rank] = &send_off;
+    }
+    publish_and_wait(send_buf, s);
+    for (int p = 0; p < nranks; ++p) {
+      if (p == rank || !recv_cnt[p]) continue;
+      const double* src = static_cast<const double*>(g->ptr[p]) + (*g->vec[p])[rank];
+      GSE_CUDA_TRY(cudaMemcpyAsync(recv_base + recv_off[p], src, 8 * recv_cnt[p],
+                                   cudaMemcpyDeviceToDevice, s));
+    }
+    done_reading(s);
+    return GSE_OK;
+  }
+};
+
+// ---------------------------------------------------------------- distributed matrix state
+struct DistCtx {
+  Comm* comm = nullptr;          // not owned (owned by the gse_dist handle)
+  int64_t row_begin = 0, n_local = 0, global_rows = 0, n_halo = 0;
+  std::vector<int64_t> rank_rows;   // nranks + 1 row offsets
+  std::vector<int64_t> send_cnt, send_off, recv_cnt, recv_off;
+  int32_t* d_send_idx = nullptr;    // local indices of owned entries to send (grouped by peer)
+  double* d_send_buf = nullptr;
+  double* d_xext = nullptr;         // n_local + n_halo, used by gse_spmv on this matrix
+  int64_t send_total = 0;
+};
+
+}  // namespace gse
+
+struct gse_dist_s {
+  gse::Comm* comm = nullptr;
+};
+
+namespace gse {
+
+__global__ void k_pack(const double* __restrict__ x, const int32_t* __restrict__ idx, int64_t n,
+                       double* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = x[idx[i]];
+}
+
+// x_ext[0 .. n_local) must hold the owned entries; fills x_ext[n_local ..) from the peers
+gse_status dist_halo_exchange(const Matrix& M, double* x_ext, cudaStream_t s) {
+  DistCtx* D = M.dist;
+  if (!D) return GSE_OK;
+  if (D->send_total > 0) {
+    int g = (int)std::min<int64_t>((D->send_total + 255) / 256, (int64_t)num_sms(M.device) * 4);
+    k_pack<<<g, 256, 0, s>>>(x_ext, D->d_send_idx, D->send_total, D->d_send_buf);
+    GSE_CUDA_TRY(cudaGetLastError());
+  }
+  return D->comm->exchange(D->d_send_buf, D->send_cnt, D->send_off, x_ext + D->n_local,
+                           D->recv_cnt, D->recv_off, s);
+}
+
+gse_status dist_allreduce_sum(const Matrix& M, double* d_vals, int count, cudaStream_t s) {
+  if (!M.dist) return GSE_OK;
+  return M.dist->comm->allreduce_sum_f64(d_vals, count, s);
+}
+
+gse_status dist_allreduce_hist(const Matrix& M, unsigned long long* d, int count, cudaStream_t s) {
+  if (!M.dist) return GSE_OK;
+  return M.dist->comm->allreduce_sum_u64(d, count, s);
+}
+
+void free_dist(Matrix& M) {
+  DistCtx* D = M.dist;
+  if (!D) return;
+  dev_free(D->d_send_idx, nullptr);
+  dev_free(D->d_send_buf, nullptr);
+  dev_free(D->d_xext, nullptr);
+  delete D;
+  M.dist = nullptr;
+}
+
+int64_t dist_ext_cols(const Matrix& M) { return M.dist ? M.dist->n_local + M.dist->n_halo : M.cols; }
+
+// ---------------------------------------------------------------- plan (host, setup time)
+// Local renumbering of one rank's column ids (see the file comment).  Returns the sorted
+// halo list and the local column array.  Pure host code (also exported for CPU tests).
+gse_status build_plan_host(int64_t nnz, const int32_t* col, int64_t row_begin, int64_t n_local,
+                           int nranks, const int64_t* rank_rows, int32_t* local_col,
+                           std::vector<int64_t>& halo, std::vector<int64_t>& recv_cnt) {
+  const int64_t row_end = row_begin + n_local;
+  halo.clear();
+  for (int64_t i = 0; i < nnz; ++i) {
+    const int64_t c = col[i];
+    if (c < row_begin || c >= row_end) halo.push_back(c);
+  }
+  std::sort(halo.begin(), halo.end());
+  halo.erase(std::unique(halo.begin(), halo.end()), halo.end());
+  if ((int64_t)halo.size() + n_local >= (1LL << 31)) {
+    set_error("local column space exceeds 2^31");
+    return GSE_ERR_INVALID_ARG;
+  }
+  for (int64_t i = 0; i < nnz; ++i) {
+    const int64_t c = col[i];
+    if (c >= row_begin && c < row_end) {
+      local_col[i] = (int32_t)(c - row_begin);
+    } else {
+      const int64_t pos = std::lower_bound(halo.begin(), halo.end(), c) - halo.begin();
+      local_col[i] = (int32_t)(n_local + pos);
+    }
+  }
+  recv_cnt.assign(nranks, 0);
+  int owner = 0;
+  for (int64_t c : halo) {
+    while (owner < nranks - 1 && c >= rank_rows[owner + 1]) ++owner;
+    recv_cnt[owner]++;
+  }
+  return GSE_OK;
+}
+
+gse_status comm_allreduce_u64(Comm* c, unsigned long long* d, int count, cudaStream_t s) {
+  return c ? c->allreduce_sum_u64(d, count, s) : GSE_OK;
+}
+
+gse_status comm_any(Comm* c, int local_flag, int* any) {
+  *any = local_flag;
+  if (!c) return GSE_OK;
+  std::vector<int64_t> all;
+  gse_status st = c->host_allgather(local_flag, all);
+  if (st != GSE_OK) return st;
+  for (int64_t v : all) *any |= (v != 0);
+  return GSE_OK;
+}
+
+double* dist_xext(const Matrix& M) { return M.dist ? M.dist->d_xext : nullptr; }
+int64_t dist_n_local(const Matrix& M) { return M.dist ? M.dist->n_local : M.rows; }
+
 }  // namespace gse
 
 using namespace gse;
+
 extern "C" {
-gse_status gse_nccl_unique_id(void*) {
-  set_error("multi-GPU path not built yet");
-  return GSE_ERR_NCCL;
+
+gse_status gse_nccl_unique_id(void* id128) {
+  if (!id128) {
+    set_error("id buffer is NULL");
+    return GSE_ERR_INVALID_ARG;
+  }
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return nccl_status(r, "ncclGetUniqueId");
+  memcpy(id128, &id, sizeof(id) < 128 ? sizeof(id) : 128);
+  return GSE_OK;
 }
-gse_status gse_dist_create(const void*, int, int, int, gse_dist* out) {
-  if (out) *out = nullptr;
-  set_error("multi-GPU path not built yet");
-  return GSE_ERR_NCCL;
+
+gse_status gse_dist_create(const void* nccl_unique_id, int rank, int nranks, int device,
+                           gse_dist* out) {
+  if (!out || !nccl_unique_id || nranks < 1 || rank < 0 || rank >= nranks || nranks > 16) {
+    set_error("invalid dist arguments (nranks in [1, 16])");
+    return GSE_ERR_INVALID_ARG;
+  }
+  *out = nullptr;
+  cudaSetDevice(device);
+  NcclComm* c = new NcclComm();
+  c->rank = rank;
+  c->nranks = nranks;
+  c->device = device;
+  ncclUniqueId id;
+  memcpy(&id, nccl_unique_id, sizeof(id));
+  ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return nccl_status(r, "ncclCommInitRank");
+  }
+  cudaStreamCreateWithFlags(&c->setup, cudaStreamNonBlocking);
+  gse_dist d = new gse_dist_s();
+  d->comm = c;
+  *out = d;
+  return GSE_OK;
 }
-gse_status gse_encode_dist(gse_dist, const gse_csr_f64*, int64_t, int64_t, const gse_encode_opts*,
-                           gse_matrix* out, void*) {
-  if (out) *out = nullptr;
-  set_error("multi-GPU path not built yet");
-  return GSE_ERR_NCCL;
+
+gse_status gse_dist_thread_group_create(int nranks, void** group) {
+  if (!group || nranks < 1 || nranks > 16) {
+    set_error("nranks must be in [1, 16]");
+    return GSE_ERR_INVALID_ARG;
+  }
+  ThreadGroup* g = new ThreadGroup();
+  g->n = nranks;
+  g->ptr.assign(nranks, nullptr);
+  g->ev.assign(nranks, nullptr);
+  g->ev2.assign(nranks, nullptr);
+  g->vec.assign(nranks, nullptr);
+  g->vv.assign(nranks, nullptr);
+  g->scalar.assign(nranks, 0);
+  *group = g;
+  return GSE_OK;
 }
-void gse_dist_free(gse_dist) {}
+
+void gse_dist_thread_group_free(void* group) { delete static_cast<ThreadGroup*>(group); }
+
+gse_status gse_dist_create_thread(void* group, int rank, int device, gse_dist* out) {
+  ThreadGroup* g = static_cast<ThreadGroup*>(group);
+  if (!out || !g || rank < 0 || rank >= g->n) {
+    set_error("invalid thread-group rank");
+    return GSE_ERR_INVALID_ARG;
+  }
+  cudaSetDevice(device);
+  ThreadComm* c = new ThreadComm();
+  c->g = g;
+  c->rank = rank;
+  c->nranks = g->n;
+  c->device = device;
+  if (cudaEventCreateWithFlags(&c->my_ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->my_ev2, cudaEventDisableTiming) != cudaSuccess) {
+    delete c;
+    return cuda_status(cudaGetLastError(), "cudaEventCreate");
+  }
+  gse_dist d = new gse_dist_s();
+  d->comm = c;
+  *out = d;
+  return GSE_OK;
 }
+
+void gse_dist_free(gse_dist D) {
+  if (!D) return;
+  delete D->comm;
+  delete D;
+}
+
+gse_status gse_dist_plan(int64_t nnz, const int32_t* col, int64_t row_begin, int64_t n_local,
+                         int nranks, const int64_t* rank_rows, int32_t* local_col,
+                         int64_t* n_halo, int64_t* halo_cols, int64_t* recv_count) {
+  if (nnz < 0 || (nnz > 0 && (!col || !local_col)) || !rank_rows || !n_halo || nranks < 1) {
+    set_error("invalid plan arguments");
+    return GSE_ERR_INVALID_ARG;
+  }
+  std::vector<int64_t> halo, rc;
+  gse_status st =
+      build_plan_host(nnz, col, row_begin, n_local, nranks, rank_rows, local_col, halo, rc);
+  if (st != GSE_OK) return st;
+  *n_halo = (int64_t)halo.size();
+  if (halo_cols) std::copy(halo.begin(), halo.end(), halo_cols);
+  if (recv_count) std::copy(rc.begin(), rc.end(), recv_count);
+  return GSE_OK;
+}
+
+gse_status gse_encode_dist(gse_dist Dh, const gse_csr_f64* A, int64_t row_begin,
+                           int64_t global_rows, const gse_encode_opts* opts, gse_matrix* out,
+                           void* stream) {
+  if (!Dh || !A || !out) {
+    set_error("NULL argument");
+    return GSE_ERR_INVALID_ARG;
+  }
+  *out = nullptr;
+  Comm* comm = Dh->comm;
+  cudaSetDevice(comm->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n_local = A->rows;
+  if (row_begin < 0 || row_begin + n_local > global_rows || A->cols != global_rows) {
+    set_error("rank rows must lie in [0, global_rows) and cols == global_rows (square)");
+    return GSE_ERR_DIM_MISMATCH;
+  }
+  // row partition of all ranks (contiguous, in rank order)
+  std::vector<int64_t> begins, counts;
+  gse_status st = comm->host_allgather(row_begin, begins);
+  if (st == GSE_OK) st = comm->host_allgather(n_local, counts);
+  if (st != GSE_OK) return st;
+  std::vector<int64_t> rank_rows(comm->nranks + 1, 0);
+  for (int r = 0; r < comm->nranks; ++r) {
+    if (begins[r] != rank_rows[r]) {
+      set_error("ranks must own contiguous row blocks in rank order");
+      return GSE_ERR_INVALID_ARG;
+    }
+    rank_rows[r + 1] = begins[r] + counts[r];
+  }
+  if (rank_rows[comm->nranks] != global_rows) {
+    set_error("row blocks do not cover [0, global_rows)");
+    return GSE_ERR_DIM_MISMATCH;
+  }
+  // columns to the host, local renumbering + halo plan
+  std::vector<int32_t> col_h((size_t)A->nnz), local_col((size_t)A->nnz);
+  if (A->nnz) {
+    GSE_CUDA_TRY(cudaMemcpyAsync(col_h.data(), A->col_idx, 4 * (size_t)A->nnz, cudaMemcpyDefault, s));
+    GSE_CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  for (int64_t i = 0; i < A->nnz; ++i)
+    if (col_h[i] < 0 || col_h[i] >= global_rows) {
+      set_error("column index out of range");
+      return GSE_ERR_INVALID_ARG;
+    }
+  std::vector<int64_t> halo, recv_cnt;
+  st = build_plan_host(A->nnz, col_h.data(), row_begin, n_local, comm->nranks, rank_rows.data(),
+                       local_col.data(), halo, recv_cnt);
+  if (st != GSE_OK) return st;
+  // tell every owner which of its entries this rank needs
+  std::vector<std::vector<int64_t>> want(comm->nranks), give;
+  {
+    size_t o = 0;
+    for (int p = 0; p < comm->nranks; ++p) {
+      want[p].assign(halo.begin() + o, halo.begin() + o + recv_cnt[p]);
+      o += recv_cnt[p];
+    }
+  }
+  st = comm->host_alltoallv(want, give);
+  if (st != GSE_OK) return st;
+  // encode the local rows with local column ids and the GLOBAL table
+  gse_csr_f64 L = *A;
+  L.cols = n_local + (int64_t)halo.size();
+  gse_encode_opts o = {8, comm->device, 0, 0};
+  if (opts) o = *opts;
+  o.device = comm->device;
+  Matrix* M = nullptr;
+  st = create_from_csr(&L, GSE_KIND_GSE, o.k_max, o.device, out, s, &M, comm, local_col.data());
+  if (st != GSE_OK) return st;
+  DistCtx* D = new DistCtx();
+  D->comm = comm;
+  D->row_begin = row_begin;
+  D->n_local = n_local;
+  D->global_rows = global_rows;
+  D->n_halo = (int64_t)halo.size();
+  D->rank_rows = rank_rows;
+  D->recv_cnt = recv_cnt;
+  D->recv_off.assign(comm->nranks, 0);
+  D->send_cnt.assign(comm->nranks, 0);
+  D->send_off.assign(comm->nranks, 0);
+  int64_t ro = 0, so = 0;
+  std::vector<int32_t> send_idx;
+  for (int p = 0; p < comm->nranks; ++p) {
+    D->recv_off[p] = ro;
+    ro += recv_cnt[p];
+    D->send_off[p] = so;
+    D->send_cnt[p] = (int64_t)give[p].size();
+    so += D->send_cnt[p];
+    for (int64_t c : give[p]) send_idx.push_back((int32_t)(c - row_begin));
+  }
+  D->send_total = so;
+  D->d_send_idx = dev_alloc_n<int32_t>((size_t)so + 1, s);
+  D->d_send_buf = dev_alloc_n<double>((size_t)so + 1, s);
+  D->d_xext = dev_alloc_n<double>((size_t)(n_local + D->n_halo) + 1, s);
+  if (!D->d_send_idx || !D->d_send_buf || !D->d_xext) {
+    delete D;
+    gse_matrix_free(*out);
+    *out = nullptr;
+    return GSE_ERR_OOM;
+  }
+  if (so)
+    GSE_CUDA_TRY(cudaMemcpyAsync(D->d_send_idx, send_idx.data(), 4 * so, cudaMemcpyHostToDevice, s));
+  GSE_CUDA_TRY(cudaStreamSynchronize(s));
+  M->dist = D;
+  return GSE_OK;
+}
+
+}  // extern "C"

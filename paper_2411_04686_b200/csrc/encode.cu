@@ -421,7 +421,7 @@ static std::string row_col_of(const void* d_row_ptr, int rp64, const int32_t* d_
 }
 
 gse_status encode_matrix(Matrix& M, const gse_csr_f64& A, const void* d_row_ptr, int rp64,
-                         const int32_t* d_col, const double* d_val, cudaStream_t s) {
+                         const int32_t* d_col, const double* d_val, cudaStream_t s, Comm* comm) {
   M.kind = GSE_KIND_GSE;
   int eb = 0;
   while ((1 << eb) < M.k_max) ++eb;
@@ -444,6 +444,12 @@ gse_status encode_matrix(Matrix& M, const gse_csr_f64& A, const void* d_row_ptr,
     k_hist<<<g, 512, 0, s>>>(d_val, M.nnz, st);
     GSE_CUDA_TRY(cudaGetLastError());
   }
+  if (comm) {
+    // distributed encode: one GLOBAL table (R21) -- sum the histograms (and the zero
+    // counts, which follow hist[] in EncodeStatus) over all ranks before the selection
+    rc = comm_allreduce_u64(comm, st->hist, 2048 + 1, s);
+    if (rc != GSE_OK) return rc;
+  }
   k_select<<<1, 1024, 0, s>>>(st, M.k_max);
   GSE_CUDA_TRY(cudaGetLastError());
 
@@ -452,6 +458,18 @@ gse_status encode_matrix(Matrix& M, const gse_csr_f64& A, const void* d_row_ptr,
   EncodeStatus* h = (EncodeStatus*)malloc(sizeof(EncodeStatus));
   GSE_CUDA_TRY(cudaMemcpyAsync(h, st, sizeof(EncodeStatus), cudaMemcpyDeviceToHost, s));
   GSE_CUDA_TRY(cudaStreamSynchronize(s));
+  if (comm) {  // every rank fails together
+    int any = 0;
+    const int mine = (h->bad_structure || h->first_nonfinite != ~0ull) ? 1 : 0;
+    rc = comm_any(comm, mine, &any);
+    if (rc != GSE_OK) return rc;
+    if (any && !mine) {
+      free(h);
+      dev_free(st, s);
+      set_error("encode failed on another rank (invalid structure or non-finite value)");
+      return GSE_ERR_INVALID_ARG;
+    }
+  }
   if (h->bad_structure) {
     free(h);
     dev_free(st, s);
@@ -513,6 +531,15 @@ gse_status encode_matrix(Matrix& M, const gse_csr_f64& A, const void* d_row_ptr,
   GSE_CUDA_TRY(cudaMemcpyAsync(&badc, &st->first_bad_col, 8, cudaMemcpyDeviceToHost, s));
   GSE_CUDA_TRY(cudaStreamSynchronize(s));
   dev_free(st, s);
+  if (comm) {
+    int any = 0;
+    rc = comm_any(comm, badc != ~0ull ? 1 : 0, &any);
+    if (rc != GSE_OK) return rc;
+    if (any && badc == ~0ull) {
+      set_error("column index out of range on another rank");
+      return GSE_ERR_INVALID_ARG;
+    }
+  }
   if (badc != ~0ull) {
     set_error("column index out of range at " +
               row_col_of(d_row_ptr, rp64, d_col, M.rows, (int64_t)badc, s));

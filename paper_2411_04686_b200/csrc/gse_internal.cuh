@@ -50,6 +50,7 @@ struct DecodeTable {
 
 struct SolverWs;  // solvers.cu
 struct DistCtx;   // dist.cu
+struct Comm;      // dist.cu: NCCL or thread-group collectives of one rank
 
 struct Matrix {
   int kind = GSE_KIND_GSE;
@@ -110,7 +111,8 @@ int num_sms(int device);
 // encode.cu
 gse_status build_partition(Matrix& M, cudaStream_t s);
 gse_status encode_matrix(Matrix& M, const gse_csr_f64& A, const void* d_row_ptr, int rp64,
-                         const int32_t* d_col, const double* d_val, cudaStream_t s);
+                         const int32_t* d_col, const double* d_val, cudaStream_t s,
+                         Comm* comm = nullptr);
 gse_status fp64_matrix(Matrix& M, const void* d_row_ptr, int rp64, const int32_t* d_col,
                        const double* d_val, cudaStream_t s);
 void build_decode_table(Matrix& M);
@@ -140,7 +142,15 @@ void free_solver_ws(Matrix& M);
 // dist.cu
 gse_status dist_halo_exchange(const Matrix& M, double* x_local_ext, cudaStream_t s);
 gse_status dist_allreduce_sum(const Matrix& M, double* d_vals, int count, cudaStream_t s);
+gse_status comm_allreduce_u64(Comm* c, unsigned long long* d, int count, cudaStream_t s);
+gse_status comm_any(Comm* c, int local_flag, int* any);  // host: OR over ranks
+double* dist_xext(const Matrix& M);
+int64_t dist_ext_cols(const Matrix& M);
+int64_t dist_n_local(const Matrix& M);
 void free_dist(Matrix& M);
+gse_status create_from_csr(const gse_csr_f64* A, int kind, int k_max, int device,
+                           gse_matrix* out, cudaStream_t s, Matrix** mout, Comm* comm,
+                           const int32_t* local_col_host);
 
 }  // namespace gse
 

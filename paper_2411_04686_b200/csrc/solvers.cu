@@ -41,6 +41,8 @@ struct SolveCtrl {
   double bnorm, tol;
   double rr, rr_new, pq, beta, resid;
   double dot;  // scratch reduction target
+  double rr_part;  // distributed CG: this rank's r.r partial (allreduced before k_cg_events)
+  int upd_ok;
   long long iter, max_iters;
   int level, event, stop, stepped, max_level;
   long long l, t, m, ndec_limit;
@@ -198,6 +200,40 @@ __global__ void __launch_bounds__(256) k_residual(const double* __restrict__ b,
 }
 
 // ---------------------------------------------------------------- CG kernels
+// residual, monitor and events after CG iteration j (one thread)
+__device__ void cg_events(SolveCtrl* c, double* ring, double tot, bool ok,
+                          cudaGraphConditionalHandle handle, int in_graph) {
+  const double rr = c->rr;
+  const long long j = c->iter + 1;
+  c->iter = j;
+  int ev = EV_NONE;
+  if (!ok) {
+    ev = EV_ABORT;
+  } else {
+    const double resid = sqrt(tot) / c->bnorm;
+    c->resid = resid;
+    c->rr_new = tot;
+    if (!isfinite(resid)) {
+      ev = EV_ABORT;
+    } else {
+      ring_push(c, ring, resid);
+      if (resid <= c->tol)
+        ev = EV_CONVERGED;
+      else if (monitor_check(c, ring, j, resid))
+        ev = EV_ESCALATE;
+      else if (j >= c->max_iters)
+        ev = EV_MAXITER;
+    }
+  }
+  c->event = ev;
+  if (ev != EV_NONE) {
+    if (in_graph) cudaGraphSetConditional(handle, 0u);
+  } else {
+    c->beta = tot / rr;
+    c->rr = tot;
+  }
+}
+
 // x += alpha p ; r -= alpha q ; rr_new = r.r ; monitor ; events
 __global__ void __launch_bounds__(256) k_cg_update(SolveCtrl* __restrict__ c, double* ring,
                                                    double* __restrict__ x, double* __restrict__ r,
@@ -205,7 +241,7 @@ __global__ void __launch_bounds__(256) k_cg_update(SolveCtrl* __restrict__ c, do
                                                    const double* __restrict__ q, int64_t n,
                                                    double* partials, unsigned* ticket,
                                                    cudaGraphConditionalHandle handle,
-                                                   int in_graph) {
+                                                   int in_graph, int defer) {
   if (c->event != EV_NONE) return;  // host-driven mode: iterations after an event are no-ops
   const double pq = c->pq, rr = c->rr;
   const bool ok = (pq > 0.0) && isfinite(pq);
@@ -241,35 +277,19 @@ __global__ void __launch_bounds__(256) k_cg_update(SolveCtrl* __restrict__ c, do
   }
   double tot;
   if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0) {
-    const long long j = c->iter + 1;
-    c->iter = j;
-    int ev = EV_NONE;
-    if (!ok) {
-      ev = EV_ABORT;
+    if (defer) {  // distributed: r.r is this rank's partial; k_cg_events runs after the allreduce
+      c->rr_part = tot;
+      c->upd_ok = ok ? 1 : 0;
     } else {
-      const double resid = sqrt(tot) / c->bnorm;
-      c->resid = resid;
-      c->rr_new = tot;
-      if (!isfinite(resid)) {
-        ev = EV_ABORT;
-      } else {
-        ring_push(c, ring, resid);
-        if (resid <= c->tol)
-          ev = EV_CONVERGED;
-        else if (monitor_check(c, ring, j, resid))
-          ev = EV_ESCALATE;
-        else if (j >= c->max_iters)
-          ev = EV_MAXITER;
-      }
-    }
-    c->event = ev;
-    if (ev != EV_NONE) {
-      if (in_graph) cudaGraphSetConditional(handle, 0u);
-    } else {
-      c->beta = tot / rr;
-      c->rr = tot;
+      cg_events(c, ring, tot, ok, handle, in_graph);
     }
   }
+}
+
+// distributed CG: the event logic on the allreduced r.r (all ranks decide identically)
+__global__ void k_cg_events(SolveCtrl* __restrict__ c, double* ring) {
+  if (threadIdx.x != 0 || blockIdx.x != 0 || c->event != EV_NONE) return;
+  cg_events(c, ring, c->rr_part, c->upd_ok != 0, 0, 0);
 }
 
 // p = r + beta p (skipped when an event is pending: the host restarts / stops)
@@ -513,7 +533,8 @@ static gse_status ensure_ws(Matrix& M, int64_t ring_t, int gm_restart, cudaStrea
     const size_t nn = (size_t)(n > 0 ? n : 1);
     ws->x = dev_alloc_n<double>(nn, s);
     ws->r = dev_alloc_n<double>(nn, s);
-    ws->p = dev_alloc_n<double>(nn, s);
+    // p is gathered by the SpMV: distributed -> owned + halo entries
+    ws->p = dev_alloc_n<double>((size_t)dist_ext_cols(M) + 1, s);
     ws->q = dev_alloc_n<double>(nn, s);
     ws->b = dev_alloc_n<double>(nn, s);
     ws->tmp = dev_alloc_n<double>(nn, s);
@@ -624,7 +645,7 @@ static gse_status build_cg_graph(Matrix& M, int level) {
   DotOut d = dot_to(ws, &ws->ctrl->pq);
   gse_status rc = launch_spmv(M, level, ws->p, ws->q, &d, cs, &ws->ctrl->event);
   k_cg_update<<<ws->vgrid, 256, 0, cs>>>(ws->ctrl, ws->ring, ws->x, ws->r, ws->p, ws->q, n,
-                                         ws->partials, ws->ticket, h, 1);
+                                         ws->partials, ws->ticket, h, 1, 0);
   k_cg_xpay<<<ws->vgrid, 256, 0, cs>>>(ws->ctrl, ws->p, ws->r, n);
   cudaGraph_t captured;
   cudaError_t e = cudaStreamEndCapture(cs, &captured);
@@ -659,15 +680,41 @@ static void log_switch(gse_solve_report& rep, int64_t j, int lvl) {
 }
 
 // true relative residual ||b - A_3 x|| / ||b|| (x = ws->x); uses ws->tmp / ws->q
+// SpMV of a vector held in the rank-local layout: single GPU -> as is; distributed -> the
+// owned entries are copied to x_ext and the halo is exchanged first
+static gse_status spmv_local(Matrix& M, int level, const double* v, double* out,
+                             const DotOut* dot, cudaStream_t s, const int* stop = nullptr) {
+  const double* in = v;
+  if (M.dist) {
+    double* xe = dist_xext(M);
+    if (v != xe)
+      GSE_CUDA_TRY(cudaMemcpyAsync(xe, v, 8 * M.rows, cudaMemcpyDeviceToDevice, s));
+    gse_status rc = dist_halo_exchange(M, xe, s);
+    if (rc != GSE_OK) return rc;
+    in = xe;
+  }
+  return launch_spmv(M, level, in, out, dot, s, stop);
+}
+
+// r = b - A_level x (p = r when p != null); *out = ||r||^2 (allreduced over ranks)
+static gse_status residual(Matrix& M, int level, const double* x, double* r, double* p,
+                           double* out, gse_solve_report& rep, cudaStream_t s) {
+  SolverWs* ws = M.ws;
+  gse_status rc = spmv_local(M, level, x, ws->q, nullptr, s);
+  if (rc != GSE_OK) return rc;
+  rep.spmv_count[level - 1]++;
+  k_residual<<<ws->vgrid, 256, 0, s>>>(ws->b, ws->q, r, p, M.rows, ws->partials, ws->ticket,
+                                       out);
+  GSE_CUDA_TRY(cudaGetLastError());
+  return dist_allreduce_sum(M, out, 1, s);
+}
+
+// true relative residual ||b - A_3 x|| / ||b||
 static gse_status true_resid(Matrix& M, const double* x, double bnorm, gse_solve_report& rep,
                              double* out, cudaStream_t s) {
   SolverWs* ws = M.ws;
-  gse_status rc = launch_spmv(M, 3, x, ws->tmp, nullptr, s);
+  gse_status rc = residual(M, 3, x, ws->tmp, nullptr, &ws->ctrl->dot, rep, s);
   if (rc != GSE_OK) return rc;
-  rep.spmv_count[2]++;
-  k_residual<<<ws->vgrid, 256, 0, s>>>(ws->b, ws->tmp, ws->tmp, nullptr, M.rows, ws->partials,
-                                       ws->ticket, &ws->ctrl->dot);
-  GSE_CUDA_TRY(cudaGetLastError());
   rc = read_ctrl(ws, s);
   if (rc != GSE_OK) return rc;
   *out = sqrt(ws->hctrl->dot) / bnorm;
@@ -676,9 +723,10 @@ static gse_status true_resid(Matrix& M, const double* x, double bnorm, gse_solve
 
 gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t max_iters,
                     const gse_step_schedule& sched, gse_solve_report& rep, cudaStream_t s) {
-  const int64_t n = M.rows;
+  const int64_t n = M.rows;  // local rows (distributed: this rank's slice)
   const int stepped = sched.enabled && M.kind == GSE_KIND_GSE;
   int level = (M.kind == GSE_KIND_FP64) ? 3 : sched.start_level;
+  const bool dist = M.dist != nullptr;
   gse_status rc = ensure_ws(M, stepped ? sched.t : 0, 0, s);
   if (rc != GSE_OK) return rc;
   SolverWs* ws = M.ws;
@@ -687,12 +735,11 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
   GSE_CUDA_TRY(cudaMemcpyAsync(ws->x, x, n * 8, cudaMemcpyDeviceToDevice, s));
   // ||b||, r0 = b - A_L x0, p0 = r0, rr
   k_dot<<<ws->vgrid, 256, 0, s>>>(ws->b, ws->b, n, ws->partials, ws->ticket, &ws->ctrl->dot);
-  rc = launch_spmv(M, level, ws->x, ws->q, nullptr, s);
-  if (rc != GSE_OK) return rc;
-  rep.spmv_count[level - 1]++;
-  k_residual<<<ws->vgrid, 256, 0, s>>>(ws->b, ws->q, ws->r, ws->p, n, ws->partials, ws->ticket,
-                                       &ws->ctrl->rr);
   GSE_CUDA_TRY(cudaGetLastError());
+  rc = dist_allreduce_sum(M, &ws->ctrl->dot, 1, s);
+  if (rc != GSE_OK) return rc;
+  rc = residual(M, level, ws->x, ws->r, ws->p, &ws->ctrl->rr, rep, s);
+  if (rc != GSE_OK) return rc;
   rc = read_ctrl(ws, s);
   if (rc != GSE_OK) return rc;
   SolveCtrl* hc = ws->hctrl;
@@ -723,11 +770,8 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
       } else {
         level = 3;
         log_switch(rep, 0, level);
-        rc = launch_spmv(M, level, ws->x, ws->q, nullptr, s);
+        rc = residual(M, level, ws->x, ws->r, ws->p, &ws->ctrl->rr, rep, s);
         if (rc != GSE_OK) return rc;
-        rep.spmv_count[level - 1]++;
-        k_residual<<<ws->vgrid, 256, 0, s>>>(ws->b, ws->q, ws->r, ws->p, n, ws->partials,
-                                             ws->ticket, &ws->ctrl->rr);
       }
     }
   }
@@ -751,15 +795,38 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
       status = GSE_NOT_CONVERGED;
       break;
     }
-    if (no_graph()) {
+    if (dist) {
+      // distributed: host-driven batches (every rank issues the same collectives); halo of
+      // p, SpMV + local p.q, allreduce, update + local r.r, allreduce, events, p update
+      do {
+        DotOut d = dot_to(ws, &ws->ctrl->pq);
+        for (int bt = 0; bt < 16; ++bt) {
+          rc = dist_halo_exchange(M, ws->p, s);
+          if (rc != GSE_OK) return rc;
+          rc = launch_spmv(M, level, ws->p, ws->q, &d, s, &ws->ctrl->event);
+          if (rc != GSE_OK) return rc;
+          rc = dist_allreduce_sum(M, &ws->ctrl->pq, 1, s);
+          if (rc != GSE_OK) return rc;
+          k_cg_update<<<ws->vgrid, 256, 0, s>>>(ws->ctrl, ws->ring, ws->x, ws->r, ws->p, ws->q,
+                                                n, ws->partials, ws->ticket, 0, 0, 1);
+          rc = dist_allreduce_sum(M, &ws->ctrl->rr_part, 1, s);
+          if (rc != GSE_OK) return rc;
+          k_cg_events<<<1, 32, 0, s>>>(ws->ctrl, ws->ring);
+          k_cg_xpay<<<ws->vgrid, 256, 0, s>>>(ws->ctrl, ws->p, ws->r, n);
+        }
+        GSE_CUDA_TRY(cudaGetLastError());
+        rc = read_ctrl(ws, s);
+        if (rc != GSE_OK) return rc;
+      } while (hc->event == EV_NONE);
+    } else if (no_graph()) {
       // host-driven iterations (profiling / fallback): batches of 16, then poll the event
       do {
         DotOut d = dot_to(ws, &ws->ctrl->pq);
-        for (int b = 0; b < 16; ++b) {
+        for (int bt = 0; bt < 16; ++bt) {
           rc = launch_spmv(M, level, ws->p, ws->q, &d, s, &ws->ctrl->event);
           if (rc != GSE_OK) return rc;
           k_cg_update<<<ws->vgrid, 256, 0, s>>>(ws->ctrl, ws->ring, ws->x, ws->r, ws->p, ws->q,
-                                                n, ws->partials, ws->ticket, 0, 0);
+                                                n, ws->partials, ws->ticket, 0, 0, 0);
           k_cg_xpay<<<ws->vgrid, 256, 0, s>>>(ws->ctrl, ws->p, ws->r, n);
         }
         GSE_CUDA_TRY(cudaGetLastError());
@@ -802,19 +869,15 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
       status = GSE_NOT_CONVERGED;
       break;
     } else {
-      set_error("internal: CG graph returned without an event");
+      set_error("internal: CG loop returned without an event");
       return GSE_ERR_CUDA;
     }
     if (escalate) {
       // R15: restart from the current x at the new level: r = b - A_new x, p = r
       level++;
       log_switch(rep, iter, level);
-      rc = launch_spmv(M, level, ws->x, ws->q, nullptr, s);
+      rc = residual(M, level, ws->x, ws->r, ws->p, &ws->ctrl->rr, rep, s);
       if (rc != GSE_OK) return rc;
-      rep.spmv_count[level - 1]++;
-      k_residual<<<ws->vgrid, 256, 0, s>>>(ws->b, ws->q, ws->r, ws->p, n, ws->partials,
-                                           ws->ticket, &ws->ctrl->rr);
-      GSE_CUDA_TRY(cudaGetLastError());
       rc = set_field(ws, &SolveCtrl::level, level, s);
       if (rc != GSE_OK) return rc;
       rc = set_field(ws, &SolveCtrl::event, (int)EV_NONE, s);

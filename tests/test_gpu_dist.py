@@ -1,0 +1,136 @@
+"""Row-partitioned path on one GPU via the thread backend (P host threads, one stream each):
+the same distributed code (global table by histogram allreduce, local renumbering, halo
+exchange, allreduced dots) as the NCCL backend, checked against the single-GPU path and the
+oracle:
+  * every rank's table equals the global table; head/tail planes of the row blocks
+    concatenate to the global planes (bit-exact); EI bits equal;
+  * P-rank SpMV within the SpMV tolerance of the oracle;
+  * P-rank stepped CG: iterations within 2 of the single-GPU solve, true residual <= tol.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+import gse_inputs as gi
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def g():
+    assert torch.cuda.is_available()
+    import paper_2411_04686_b200 as lib
+    return lib
+
+
+def partition(n, P):
+    return [round(i * n / P) for i in range(P + 1)]
+
+
+def run_ranks(P, fn):
+    """run fn(rank, dist_handle, stream) on P threads of one thread group"""
+    import paper_2411_04686_b200 as g
+    grp = g.gse_dist_thread_group_create(P)
+    out, errs = [None] * P, []
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            D = g.gse_dist_create_thread(grp, r, 0)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                out[r] = fn(r, D, st)
+            st.synchronize()
+            D.close()
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append((r, repr(e)))
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    g.gse_dist_thread_group_free(grp)
+    assert not errs, errs
+    return out
+
+
+def slab(A, a, b):
+    rp = (A.row_ptr[a:b + 1] - A.row_ptr[a]).astype(np.int64)
+    sl = slice(A.row_ptr[a], A.row_ptr[b])
+    return rp, A.col[sl].copy(), A.val[sl].copy()
+
+
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("name", ["poisson", "powerlaw"])
+def test_dist_encode_and_spmv(g, P, name):
+    A = gi.poisson3d(16, "varcoef") if name == "poisson" else gi.powerlaw_spd(20000, seed=4)
+    R = O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+    x = gi.uniform_vec(A.cols, seed=5)
+    rr = partition(A.rows, P)
+
+    def fn(r, D, st):
+        a, b = rr[r], rr[r + 1]
+        rp, col, val = slab(A, a, b)
+        dev = lambda v: torch.from_numpy(v).cuda()
+        M = g.gse_encode_dist(D, dev(rp), dev(col), dev(val), a, A.rows, stream=st.cuda_stream)
+        P_ = g.gse_matrix_copy_planes(M)
+        ys = [g.gse_spmv(M, dev(x[a:b].copy()), segments=L, stream=st.cuda_stream)
+              for L in (1, 2, 3)]
+        torch.cuda.synchronize()
+        res = (P_, [y.cpu().numpy() for y in ys], M.info)
+        M.close()
+        return res
+
+    outs = run_ranks(P, fn)
+    for r, (P_, ys, info) in enumerate(outs):
+        assert list(P_["table"]) == list(R.table)
+        a, b = rr[r], rr[r + 1]
+        sl = slice(A.row_ptr[a], A.row_ptr[b])
+        for k in ("head", "tail1", "tail2"):
+            assert np.array_equal(P_[k], getattr(R, k)[sl]), k
+        assert np.array_equal(P_["col_ei"] >> 29, R.col_ei[sl] >> 29)
+        for L, y in zip((1, 2, 3), ys):
+            yo = O.spmv_gse(R, x, L)[a:b]
+            absR = O.GseCsr(R.rows, R.cols, R.nnz, R.row_ptr, R.col_ei, R.side_ei,
+                            R.head & np.uint16(0x7FFF), R.tail1, R.tail2, R.table, R.ei_bits,
+                            R.ei_in_column)
+            bound = 1e-12 * O.spmv_gse(absR, np.abs(x), L)[a:b]
+            assert np.all(np.abs(y - yo) <= bound), (r, L)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("variant", ["const", "varcoef"])
+def test_dist_cg(g, P, variant):
+    A = gi.poisson3d(20, variant)
+    b = gi.ones_rhs(A)
+    M1 = g.gse_encode(A.row_ptr, A.col, A.val, A.rows, A.cols)
+    sched = lambda: g.gse_default_schedule("cg", l=30, t=10, m=10)
+    _, r1 = g.gse_solve_cg(M1, b, tol=1e-10, sched=sched())
+    rr = partition(A.rows, P)
+
+    def fn(r, D, st):
+        a, bb = rr[r], rr[r + 1]
+        rp, col, val = slab(A, a, bb)
+        dev = lambda v: torch.from_numpy(v).cuda()
+        M = g.gse_encode_dist(D, dev(rp), dev(col), dev(val), a, A.rows, stream=st.cuda_stream)
+        x, rep = g.gse_solve_cg(M, dev(b[a:bb].copy()), tol=1e-10, sched=sched(),
+                                stream=st.cuda_stream)
+        torch.cuda.synchronize()
+        M.close()
+        return x.cpu().numpy(), rep
+
+    outs = run_ranks(P, fn)
+    reps = [rep for _, rep in outs]
+    x = np.concatenate([xx for xx, _ in outs])
+    for rep in reps:  # every rank took the same decisions
+        assert rep["iterations"] == reps[0]["iterations"]
+        assert rep["switch_iter"] == reps[0]["switch_iter"]
+    rep = reps[0]
+    assert rep["converged"] and abs(rep["iterations"] - r1["iterations"]) <= 2, (rep, r1)
+    F = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+    res = np.linalg.norm(b - O.spmv_fp64(F, x)) / np.linalg.norm(b)
+    assert res <= 1e-10 * 1.01
