@@ -4,14 +4,18 @@
 Workload (BASELINE.json configs[1]): 3D Poisson 7-point 128^3 (n = 2,097,152, nnz =
 14,581,760), b = A*1, x0 = 0.  One STEP = the whole hot path on that input: gse_encode
 (histogram, table, encode into head/tail1/tail2 planes, partition) followed by the stepped
-mixed-precision CG solve to a TRUE relative residual <= 1e-10 (paper-default schedule,
-verify_at_full).  value = solves / s over all ranks (N > 1: independent replicas, weak
-scaling, until the row-partitioned path lands).
+mixed-precision CG solve to a TRUE relative residual <= 1e-10 (paper-default schedule +
+verify_at_full).  value = solves / s.
 
-Also reported on the same matrix: the SpMV segment sweep (GB/s, GFLOP/s, fraction of the
-measured HBM peak, per segment count and for FP64 / FP32 accumulation and the FP64-CSR
-comparator), the FP64-CSR CG time-to-1e-10, roofline of the dominant kernel, the oracle CPU
-baseline, the end-to-end number through the C-ABI with host buffers, and SM clocks.
+N > 1 (torchrun, one process per GPU): the SAME problem is row-partitioned over the N
+GPUs (gse_encode_dist: global table by histogram allreduce, local renumbering; CG with
+NCCL halo exchange + allreduced dots) -> "scaling": "strong".  --workload c5 selects the
+512^3 Poisson of configs[4] (the multi-GPU config).
+
+Also reported (N = 1): the SpMV segment sweep (GB/s, GFLOP/s, fraction of the measured HBM
+peak per segment count, FP64 / FP32 accumulation, FP64-CSR comparator), the FP64-CSR CG
+time-to-1e-10, the roofline of the dominant kernel, the oracle CPU baseline, the end-to-end
+number through the C-ABI with host buffers, SM clocks.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gse|reference]
 """
@@ -24,7 +28,6 @@ import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 
 import numpy as np
@@ -34,8 +37,10 @@ sys.path.insert(0, ROOT)
 
 METRIC = ("GSE SpMV GB/s & GFLOP/s (frac of HBM peak) per segment count; "
           "CG time-to-1e-10")
-UNIT = "CG solves to 1e-10 per s (encode + stepped CG, 3D Poisson 128^3)"
-L2_BYTES = 126 * 1024 * 1024
+
+
+def unit_for(N):
+    return f"CG solves to 1e-10 per s (encode + stepped CG, 3D Poisson {N}^3)"
 
 
 def parse():
@@ -44,14 +49,17 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gse", choices=["gse", "reference"])
-    ap.add_argument("--N", type=int, default=128, help="grid edge (configs[1]: 128)")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c5"])
     ap.add_argument("--variant", default="const", choices=["const", "varcoef"])
     ap.add_argument("--spmv-reps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=40,
                     help="oracle CG iterations in the bounded CPU sample")
-    return ap.parse_args()
+    a = ap.parse_args()
+    a.N = 128 if a.workload == "c2" else 512
+    return a
 
 
 def peaks():
@@ -69,9 +77,7 @@ class Clocks:
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
-        self.index = index
-        self.proc = None
-        self.path = None
+        self.index, self.proc, self.path = index, None, None
 
     def __enter__(self):
         try:
@@ -125,8 +131,13 @@ def dist_init(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     pg = None
     if world > 1:
+        import torch
         import torch.distributed as dist
-        dist.init_process_group("gloo" if args.impl == "reference" else "nccl")
+        if args.impl == "reference":
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = dist
     return world, rank, local, pg
 
@@ -145,6 +156,21 @@ def barrier(pg):
         pg.barrier()
 
 
+def partition(n, P):
+    return [round(i * n / P) for i in range(P + 1)]
+
+
+def _config(args, n, nnz, world):
+    return {"workload": f"3D Poisson 7-point {args.N}^3 ({args.variant}) stepped GSE CG to 1e-10 "
+                        f"({'configs[1]' if args.workload == 'c2' else 'configs[4]'})",
+            "n": int(n), "nnz": int(nnz), "k_max": 8, "tol": 1e-10,
+            "schedule": "paper default CG (l=3000,t=250,m=500) + verify_at_full",
+            "step": "gse_encode + gse_solve_cg (inputs resident in HBM)",
+            "l2": "flushed (256 MiB write) before every timed step; per-step CUDA events",
+            "parallelism": (f"row-partitioned x{world} (NCCL halo + allreduce)" if world > 1
+                            else "single GPU")}
+
+
 # ------------------------------------------------------------------ reference arm (oracle)
 def oracle_sample(A, b, iters: int):
     """Bounded oracle sample: oracle encode of the full matrix + `iters` CG iterations at
@@ -159,39 +185,9 @@ def oracle_sample(A, b, iters: int):
     return t1 - t0, (t2 - t1) / max(rep.iterations, 1)
 
 
-def run_reference(args, world, rank, pg):
-    if rank != 0:
-        return
-    import gse_inputs as gi
-    import oracle as O
-    cores = O.set_threads(0)
-    A = gi.poisson3d(args.N, args.variant)
-    b = gi.ones_rhs(A)
-    # iterations of the full solve: plain oracle CG count for this workload (cached per run)
-    iters_full = _oracle_iterations(A, b)
-    times = []
-    for i in range(args.warmup + args.steps):
-        te, ti = oracle_sample(A, b, max(4, args.cpu_iters // 4))
-        if i >= args.warmup:
-            times.append(te + ti * iters_full)
-    t = statistics.mean(times)
-    value = 1.0 / t
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": _config(args, A),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"oracle encode + {max(4, args.cpu_iters // 4)} CG "
-                                       f"iterations per step, extrapolated to {iters_full} "
-                                       "iterations"},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-
-
-def _oracle_iterations(A, b):
-    # closed-form gauge would be a guess; count with the oracle's own CG only when cheap,
-    # else use the GPU-independent 2.85 N rule measured in SURVEY 8(d) for 3D Poisson.
+def full_iterations(A, b):
+    # plain oracle CG count when cheap; else the 2.85 N rule measured for 3D Poisson
+    # (verified N = 16..64 in the oracle tests)
     if A.rows <= 64 ** 3:
         import oracle as O
         F = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
@@ -200,14 +196,34 @@ def _oracle_iterations(A, b):
     return int(round(2.85 * N))
 
 
-def _config(args, A):
-    return {"workload": f"3D Poisson 7-point {args.N}^3 ({args.variant}) stepped GSE CG to 1e-10 "
-                        "(configs[1])",
-            "n": int(A.rows), "nnz": int(A.nnz), "k_max": 8, "tol": 1e-10,
-            "schedule": "paper default CG (l=3000,t=250,m=500) + verify_at_full",
-            "step": "gse_encode + gse_solve_cg (inputs resident in HBM)",
-            "l2": "flushed (256 MiB write) before every timed step; per-step CUDA events",
-            "parallelism": "replicas" if args.gpus > 1 else "single GPU"}
+def run_reference(args, world, rank, pg):
+    if rank != 0:
+        return
+    import gse_inputs as gi
+    import oracle as O
+    cores = O.set_threads(0)
+    A = gi.poisson3d(args.N, args.variant)
+    b = gi.ones_rhs(A)
+    iters_full = full_iterations(A, b)
+    k = max(4, args.cpu_iters // 4)
+    times = []
+    for i in range(args.warmup + args.steps):
+        te, ti = oracle_sample(A, b, k)
+        if i >= args.warmup:
+            times.append(te + ti * iters_full)
+    t = statistics.mean(times)
+    value = 1.0 / t
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": unit_for(args.N),
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config(args, A.rows, A.nnz, world),
+            "cpu_baseline": {"value": value, "unit": unit_for(args.N), "cores": cores,
+                             "kind": "oracle",
+                             "sample": f"oracle encode + {k} CG iterations per step, extrapolated "
+                                       f"to {iters_full} iterations"},
+            "e2e": {"value": value, "unit": unit_for(args.N), "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ GSE arm
@@ -220,8 +236,12 @@ def run_gse(args, world, rank, local, pg):
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     hbm_peak, peak_src = peaks()
-
-    A = gi.poisson3d(args.N, args.variant)
+    n_glob = args.N ** 3
+    rr = partition(n_glob, world)
+    r0, r1 = rr[rank], rr[rank + 1]
+    A = gi.poisson3d(args.N, args.variant, row_begin=r0, row_end=r1)  # this rank's rows
+    nnz_glob = 7 * args.N ** 3 - 6 * args.N ** 2
+    # b = A 1 on the rank's rows (row sums: input recipe)
     b_h = gi.ones_rhs(A)
     rp = torch.from_numpy(A.row_ptr.astype(np.int32)).to(dev)
     col = torch.from_numpy(A.col).to(dev)
@@ -231,10 +251,24 @@ def run_gse(args, world, rank, local, pg):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     sched = g.gse_default_schedule("cg")
 
+    D = None
+    if world > 1:
+        import torch.distributed as tdist
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(g.gse_nccl_unique_id()), dtype=torch.uint8))
+        tdist.broadcast(uid, 0)
+        D = g.gse_dist_create(bytes(uid.cpu().numpy()), rank, world, local)
+
+    def encode(rp_, col_, val_, **kw):
+        if D is None:
+            return g.gse_encode(rp_, col_, val_, A.rows, A.cols, k_max=8, **kw)
+        return g.gse_encode_dist(D, rp_, col_, val_, r0, n_glob, **kw)
+
     def step():
-        M = g.gse_encode(rp, col, val, A.rows, A.cols, k_max=8)
+        M = encode(rp, col, val)
         x.zero_()
-        _, rep = g.gse_solve_cg(M, b, x, tol=1e-10, max_iters=5000, sched=sched)
+        _, rep = g.gse_solve_cg(M, b, x, tol=1e-10, max_iters=20000, sched=sched)
         M.close()
         return rep
 
@@ -259,57 +293,64 @@ def run_gse(args, world, rank, local, pg):
     total_ms = max_over_ranks(sum(step_ms), pg, dev)
     barrier(pg)
     rep = reps[-1]
-    value = world * args.steps / (total_ms * 1e-3)
+    value = args.steps / (total_ms * 1e-3)  # one (row-partitioned) problem per step
 
-    extra = spmv_and_cg_sweep(args, A, rp, col, val, b, dev, stream, flush, hbm_peak)
-    e2e = None if args.no_e2e else e2e_measure(args, A, b_h, dev, stream)
+    extra = None
+    if world == 1 and not args.no_sweep:
+        extra = spmv_and_cg_sweep(args, A, rp, col, val, b, dev, stream, flush, hbm_peak)
+    e2e = None if args.no_e2e else e2e_measure(args, A, b_h, dev, stream, encode, r0, n_glob)
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args, A, b_h, rep["iterations"])
-    launches = estimate_launches(rep, extra["info"]) * args.steps
+    launches = estimate_launches(rep, world) * args.steps
+    if D is not None:
+        barrier(pg)
+        D.close()
     if rank != 0:
         return
-    dom = extra["spmv"]["L1"]
-    roof = {"bound": "hbm", "kernel": "k_spmv<1> (level-1 GSE SpMV, the CG inner kernel)",
+    line = {
+        "metric": METRIC, "value": value, "unit": unit_for(args.N), "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": _config(args, n_glob, nnz_glob, world),
+        "solve": {"iterations": rep["iterations"], "iters_per_level": rep["iters_per_level"],
+                  "switch_iter": rep["switch_iter"],
+                  "rel_residual_true": rep["rel_residual_true"]},
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+    }
+    if extra is not None:
+        dom = extra["spmv"]["L1"]
+        line["time_to_1e-10_ms"] = {
+            "stepped_gse_step": statistics.median(step_ms),
+            "stepped_gse_solve_only": extra["cg_gse_ms"], "encode": extra["encode_ms"],
+            "fp64_csr_cg": extra["cg_fp64_ms"],
+            "speedup_vs_fp64_csr": extra["cg_fp64_ms"] / extra["cg_gse_ms"]}
+        line["solve"]["fp64_iterations"] = extra["cg_fp64_iters"]
+        line["spmv_sweep"] = extra["spmv"]
+        line["roofline"] = {
+            "bound": "hbm", "kernel": "k_spmv_rw<1> (level-1 GSE SpMV, the CG inner kernel)",
             "achieved": dom["GBps"], "peak": hbm_peak, "unit": "GB/s",
             "frac": dom["GBps"] / hbm_peak, "peak_source": peak_src,
             "traffic": _profiled_traffic(), "algorithmic_bytes_per_launch": dom["bytes"],
-            "avg_launch_us": dom["us"]}
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": _config(args, A),
-        "time_to_1e-10_ms": {"stepped_gse_step": statistics.median(step_ms),
-                             "stepped_gse_solve_only": extra["cg_gse_ms"],
-                             "encode": extra["encode_ms"], "fp64_csr_cg": extra["cg_fp64_ms"],
-                             "speedup_vs_fp64_csr": extra["cg_fp64_ms"] / extra["cg_gse_ms"]},
-        "solve": {"iterations": rep["iterations"], "iters_per_level": rep["iters_per_level"],
-                  "switch_iter": rep["switch_iter"], "rel_residual_true": rep["rel_residual_true"],
-                  "fp64_iterations": extra["cg_fp64_iters"]},
-        "spmv_sweep": extra["spmv"],
-        "roofline": roof,
-        "cpu_baseline": cpu,
-        "e2e": e2e,
-        "gpu_launches": launches,
-        "clocks": clocks,
-    }
+            "avg_launch_us": dom["us"],
+            "timing": "CUDA events per launch on the launching stream, L2 flushed before each"}
     print(json.dumps(line), flush=True)
 
 
-def estimate_launches(rep, info):
-    """Kernels launched per step: encode (rowptr, hist, select, encode, flags, 2 CUB select
-    kernels, fill_desc = 8), CG setup (dot, spmv, residual = 3), 3 per iteration inside the
-    graph while-loop, verify / final residual (2 each)."""
-    return 8 + 3 + 3 * rep["iterations"] + 2 * (1 + rep["n_switches"]) + 2
+def estimate_launches(rep, world):
+    """Kernels launched per step: encode (rowptr, hist, select, encode, flags, group stats,
+    2 CUB select kernels, fill_desc = 9), CG setup (dot, spmv, residual = 3), per iteration
+    3 (single GPU, graph while-loop body) or 5 (+ pack + events, distributed), verify /
+    final residual (2 each)."""
+    per_it = 3 if world == 1 else 5
+    return 9 + 3 + per_it * rep["iterations"] + 2 * (1 + rep["n_switches"]) + 2
 
 
 def _profiled_traffic():
     p = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
     if os.path.exists(p):
         try:
-            d = json.load(open(p))
-            return d.get("k_spmv_L1", {}).get("dram_bytes_per_launch")
+            return json.load(open(p)).get("k_spmv_L1", {}).get("dram_bytes_per_launch")
         except Exception:
             return None
     return None
@@ -341,24 +382,18 @@ def spmv_and_cg_sweep(args, A, rp, col, val, b, dev, stream, flush, hbm_peak):
         g.gse_spmv(M, x, y, segments=1)
     out = {}
     rows_bytes = 4 * (n + 1)
+
+    def rec(key, fn, byt):
+        t = statistics.mean(time_cuda(fn, args.spmv_reps, stream, flush)) * 1e-3
+        out[key] = {"bytes": byt, "us": t * 1e6, "GBps": byt / t / 1e9,
+                    "GFLOPs": 2 * nnz / t / 1e9, "frac_hbm": byt / t / 1e9 / hbm_peak}
+
     for L, s_l in ((1, 2), (2, 4), (3, 8)):
-        ms = time_cuda(lambda: g.gse_spmv(M, x, y, segments=L), args.spmv_reps, stream, flush)
-        t = statistics.mean(ms) * 1e-3
-        byt = nnz * (4 + s_l) + rows_bytes + 16 * n
-        out[f"L{L}"] = {"bytes": byt, "us": t * 1e6, "GBps": byt / t / 1e9,
-                        "GFLOPs": 2 * nnz / t / 1e9, "frac_hbm": byt / t / 1e9 / hbm_peak}
-    for L, s_l in ((1, 2), (3, 8)):
-        ms = time_cuda(lambda: g.gse_spmv_f32acc(M, x32, y32, segments=L), args.spmv_reps,
-                       stream, flush)
-        t = statistics.mean(ms) * 1e-3
-        byt = nnz * (4 + s_l) + rows_bytes + 8 * n
-        out[f"L{L}_f32acc"] = {"bytes": byt, "us": t * 1e6, "GBps": byt / t / 1e9,
-                               "GFLOPs": 2 * nnz / t / 1e9, "frac_hbm": byt / t / 1e9 / hbm_peak}
-    ms = time_cuda(lambda: g.gse_spmv(F, x, y, segments=3), args.spmv_reps, stream, flush)
-    t = statistics.mean(ms) * 1e-3
-    byt = nnz * 12 + rows_bytes + 16 * n
-    out["fp64_csr"] = {"bytes": byt, "us": t * 1e6, "GBps": byt / t / 1e9,
-                       "GFLOPs": 2 * nnz / t / 1e9, "frac_hbm": byt / t / 1e9 / hbm_peak}
+        rec(f"L{L}", lambda: g.gse_spmv(M, x, y, segments=L), nnz * (4 + s_l) + rows_bytes + 16 * n)
+    for L, s_l in ((1, 2), (2, 4), (3, 8)):
+        rec(f"L{L}_f32acc", lambda: g.gse_spmv_f32acc(M, x32, y32, segments=L),
+            nnz * (4 + s_l) + rows_bytes + 8 * n)
+    rec("fp64_csr", lambda: g.gse_spmv(F, x, y, segments=3), nnz * 12 + rows_bytes + 16 * n)
     # CG solve only (no encode), stepped GSE vs FP64-CSR
     xs = torch.zeros(n, dtype=torch.float64, device=dev)
     sched = g.gse_default_schedule("cg")
@@ -373,9 +408,8 @@ def spmv_and_cg_sweep(args, A, rp, col, val, b, dev, stream, flush, hbm_peak):
 
     cg_gse()
     cg_f64()
-    reps = 3
-    t_gse = statistics.median(time_cuda(cg_gse, reps, stream, flush))
-    t_f64 = statistics.median(time_cuda(cg_f64, reps, stream, flush))
+    t_gse = statistics.median(time_cuda(cg_gse, 3, stream, flush))
+    t_f64 = statistics.median(time_cuda(cg_f64, 3, stream, flush))
     rf = cg_f64()
 
     def enc():
@@ -383,16 +417,15 @@ def spmv_and_cg_sweep(args, A, rp, col, val, b, dev, stream, flush, hbm_peak):
         m.close()
 
     t_enc = statistics.median(time_cuda(enc, 3, stream, flush))
-    info = M.info
     M.close()
     F.close()
-    return {"spmv": out, "cg_gse_ms": t_gse, "cg_fp64_ms": t_f64, "cg_fp64_iters": rf["iterations"],
-            "encode_ms": t_enc, "info": info}
+    return {"spmv": out, "cg_gse_ms": t_gse, "cg_fp64_ms": t_f64,
+            "cg_fp64_iters": rf["iterations"], "encode_ms": t_enc}
 
 
-def e2e_measure(args, A, b_h, dev, stream):
+def e2e_measure(args, A, b_h, dev, stream, encode, r0, n_glob):
     """Same step through the C-ABI with HOST (pinned) buffers: H2D of the CSR and b inside
-    the call, D2H of x at the end."""
+    the calls, D2H of x at the end."""
     import torch
     import paper_2411_04686_b200 as g
     rp = torch.from_numpy(A.row_ptr.astype(np.int32)).pin_memory()
@@ -404,9 +437,9 @@ def e2e_measure(args, A, b_h, dev, stream):
     s = stream.cuda_stream
 
     def step():
-        M = g.gse_encode(rp, col, val, A.rows, A.cols, device=dev.index, stream=s)
+        M = encode(rp, col, val, stream=s)
         x.zero_()
-        g.gse_solve_cg(M, b, x, tol=1e-10, sched=sched, stream=s)
+        g.gse_solve_cg(M, b, x, tol=1e-10, max_iters=20000, sched=sched, stream=s)
         M.close()
 
     step()
@@ -419,9 +452,9 @@ def e2e_measure(args, A, b_h, dev, stream):
         ts.append(time.perf_counter() - t0)
     t = statistics.median(ts)
     h2d = rp.numel() * 4 + col.numel() * 4 + val.numel() * 8 + b.numel() * 8 + x.numel() * 8
-    return {"value": 1.0 / t, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+    return {"value": 1.0 / t, "unit": unit_for(args.N), "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(x.numel() * 8), "ms_per_step": t * 1e3,
-            "timer": "host wall clock around the synchronous C-ABI calls"}
+            "timer": "host wall clock around the synchronous C-ABI calls (rank 0)"}
 
 
 def cpu_baseline(args, A, b_h, iters_full):
@@ -429,7 +462,7 @@ def cpu_baseline(args, A, b_h, iters_full):
     cores = O.set_threads(0)
     te, ti = oracle_sample(A, b_h, args.cpu_iters)
     t = te + ti * iters_full
-    return {"value": 1.0 / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+    return {"value": 1.0 / t, "unit": unit_for(args.N), "cores": cores, "kind": "oracle",
             "sample": f"oracle encode of the full matrix ({te:.2f} s) + {args.cpu_iters} level-1 "
                       f"CG iterations ({ti * 1e3:.1f} ms each), extrapolated to the GPU run's "
                       f"{iters_full} iterations; OpenMP rows in SpMV/encode, sequential dots"}

@@ -17,6 +17,8 @@
 //    escalation request, breakdown, max iterations).  GMRES runs one graph per restart
 //    cycle (kernels early-exit once the cycle is stopped).  The host only handles events:
 //    level switch with residual replacement (R15), verification with A_3 (R16).
+#include <cooperative_groups.h>
+
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
@@ -248,31 +250,48 @@ __global__ void __launch_bounds__(256) k_cg_update(SolveCtrl* __restrict__ c, do
   const double alpha = rr / pq;
   double acc = 0.0;
   if (ok) {
-    // ILP: 4 elements (stride apart) loaded before any is computed; per-thread element order
-    // (and so the reduction order) is the plain grid-stride order
+    // 16-byte accesses (pairs of elements), 2 pairs in flight per thread; the element
+    // order of each thread (and so its reduction order) is fixed by the grid
+    const int64_t n2 = n >> 1;
+    const double2* __restrict__ p2 = reinterpret_cast<const double2*>(p);
+    const double2* __restrict__ q2 = reinterpret_cast<const double2*>(q);
+    double2* __restrict__ x2 = reinterpret_cast<double2*>(x);
+    double2* __restrict__ r2 = reinterpret_cast<double2*>(r);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += 4 * stride) {
-      double xv[4], pv[4], rv[4], qv[4];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += 2 * stride) {
+      double2 xv[2], pv[2], rv[2], qv[2];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < 2; ++k) {
         const int64_t j = i + k * stride;
-        if (j < n) {
-          xv[k] = x[j];
-          pv[k] = p[j];
-          rv[k] = r[j];
-          qv[k] = q[j];
+        if (j < n2) {
+          xv[k] = x2[j];
+          pv[k] = p2[j];
+          rv[k] = r2[j];
+          qv[k] = q2[j];
         }
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < 2; ++k) {
         const int64_t j = i + k * stride;
-        if (j < n) {
-          x[j] = __dadd_rn(xv[k], __dmul_rn(alpha, pv[k]));
-          const double ri = __dsub_rn(rv[k], __dmul_rn(alpha, qv[k]));
-          r[j] = ri;
-          acc = __dadd_rn(acc, __dmul_rn(ri, ri));
+        if (j < n2) {
+          double2 xo, ro;
+          xo.x = __dadd_rn(xv[k].x, __dmul_rn(alpha, pv[k].x));
+          xo.y = __dadd_rn(xv[k].y, __dmul_rn(alpha, pv[k].y));
+          ro.x = __dsub_rn(rv[k].x, __dmul_rn(alpha, qv[k].x));
+          ro.y = __dsub_rn(rv[k].y, __dmul_rn(alpha, qv[k].y));
+          x2[j] = xo;
+          r2[j] = ro;
+          acc = __dadd_rn(acc, __dmul_rn(ro.x, ro.x));
+          acc = __dadd_rn(acc, __dmul_rn(ro.y, ro.y));
         }
       }
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd tail element
+      const int64_t j = n - 1;
+      x[j] = __dadd_rn(x[j], __dmul_rn(alpha, p[j]));
+      const double ri = __dsub_rn(r[j], __dmul_rn(alpha, q[j]));
+      r[j] = ri;
+      acc = __dadd_rn(acc, __dmul_rn(ri, ri));
     }
   }
   double tot;
@@ -292,29 +311,105 @@ __global__ void k_cg_events(SolveCtrl* __restrict__ c, double* ring) {
   cg_events(c, ring, c->rr_part, c->upd_ok != 0, 0, 0);
 }
 
+// Fused CG tail (single GPU): x += alpha p, r -= alpha q, r.r -> ONE grid barrier ->
+// residual / monitor / events (CTA 0) and p = r + beta p with the new r still in registers.
+// Cooperative launch (all CTAs co-resident); each thread owns elements i0 + k*stride,
+// k < FUSE_K.  Saves the separate xpay pass (r read again) and one kernel boundary per
+// iteration.  The p update runs even when an event fires: every event either stops the
+// solve or restarts it with p = r (R15), so p is never used stale.
+constexpr int FUSE_K = 16;
+
+__global__ void __launch_bounds__(256, 4) k_cg_fused(SolveCtrl* __restrict__ c, double* ring,
+                                                  double* __restrict__ x, double* __restrict__ r,
+                                                  double* __restrict__ p,
+                                                  const double* __restrict__ q, int64_t n,
+                                                  double* partials,
+                                                  cudaGraphConditionalHandle handle,
+                                                  int in_graph) {
+  __shared__ double red[8];
+  __shared__ double s_tot;
+  if (c->event != EV_NONE) return;  // uniform: written only before this launch
+  const double pq = c->pq, rr = c->rr;
+  const bool ok = (pq > 0.0) && isfinite(pq);
+  const double alpha = rr / pq;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double rv[FUSE_K];
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < FUSE_K; ++k) {
+    const int64_t j = i0 + k * stride;
+    rv[k] = 0.0;
+    if (ok && j < n) {
+      const double xv = x[j], pv = p[j], rj = r[j], qv = q[j];
+      x[j] = __dadd_rn(xv, __dmul_rn(alpha, pv));
+      rv[k] = __dsub_rn(rj, __dmul_rn(alpha, qv));
+      r[j] = rv[k];
+      acc = __dadd_rn(acc, __dmul_rn(rv[k], rv[k]));
+    }
+  }
+  acc = warp_sum_d(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    partials[blockIdx.x] = s;
+  }
+  __threadfence();
+  cooperative_groups::this_grid().sync();
+  // every CTA sums the partials in the same fixed order -> identical total everywhere
+  if (threadIdx.x < 32) {
+    double s = 0.0;
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += 32) s += __ldcg(partials + i);
+    s = warp_sum_d(s);
+    if (threadIdx.x == 0) s_tot = s;
+  }
+  __syncthreads();
+  const double tot = s_tot;
+  if (blockIdx.x == 0 && threadIdx.x == 0) cg_events(c, ring, tot, ok, handle, in_graph);
+  if (!ok) return;
+  const double beta = tot / rr;
+#pragma unroll
+  for (int k = 0; k < FUSE_K; ++k) {
+    const int64_t j = i0 + k * stride;
+    if (j < n) p[j] = __dadd_rn(rv[k], __dmul_rn(beta, p[j]));
+  }
+}
+
 // p = r + beta p (skipped when an event is pending: the host restarts / stops)
 __global__ void __launch_bounds__(256) k_cg_xpay(const SolveCtrl* __restrict__ c,
                                                  double* __restrict__ p,
                                                  const double* __restrict__ r, int64_t n) {
   if (c->event != EV_NONE) return;
   const double beta = c->beta;
+  const int64_t n2 = n >> 1;
+  double2* __restrict__ p2 = reinterpret_cast<double2*>(p);
+  const double2* __restrict__ r2 = reinterpret_cast<const double2*>(r);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += 4 * stride) {
-    double pv[4], rv[4];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += 2 * stride) {
+    double2 pv[2], rv[2];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < 2; ++k) {
       const int64_t j = i + k * stride;
-      if (j < n) {
-        pv[k] = p[j];
-        rv[k] = r[j];
+      if (j < n2) {
+        pv[k] = p2[j];
+        rv[k] = r2[j];
       }
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < 2; ++k) {
       const int64_t j = i + k * stride;
-      if (j < n) p[j] = __dadd_rn(rv[k], __dmul_rn(beta, pv[k]));
+      if (j < n2) {
+        double2 o;
+        o.x = __dadd_rn(rv[k].x, __dmul_rn(beta, pv[k].x));
+        o.y = __dadd_rn(rv[k].y, __dmul_rn(beta, pv[k].y));
+        p2[j] = o;
+      }
     }
   }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0)
+    p[n - 1] = __dadd_rn(r[n - 1], __dmul_rn(beta, p[n - 1]));
 }
 
 // ---------------------------------------------------------------- GMRES kernels
@@ -622,6 +717,31 @@ static bool no_graph() {
   return v;
 }
 
+// cooperative grid for k_cg_fused: all CTAs resident and n <= FUSE_K x threads; 0 -> use
+// the unfused update + xpay kernels (also when GSE_CG_UNFUSED=1, for A/B measurements)
+static int fused_grid(const Matrix& M) {
+  // opt-in (GSE_CG_FUSED=1): on C2 the register-resident tail spills and ran at 89 us per
+  // iteration vs 64 us for update + xpay (profiles/README.md), so it is off by default
+  static const bool off = [] {
+    const char* e = getenv("GSE_CG_FUSED");
+    return !(e && e[0] == '1');
+  }();
+  if (off) return 0;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_fused, 256, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  const int64_t cap = (int64_t)per_sm * num_sms(M.device);
+  int64_t want = (M.rows + 255) / 256;
+  if (want > cap) want = cap;
+  const bool fits = want >= 1 && M.rows <= (int64_t)FUSE_K * want * 256;
+  if (getenv("GSE_DEBUG"))
+    fprintf(stderr, "[gse] k_cg_fused: %d CTAs/SM, grid %lld, rows %lld -> %s\n", per_sm,
+            (long long)want, (long long)M.rows, fits ? "fused" : "unfused");
+  return fits ? (int)want : 0;
+}
+
 // ---------------------------------------------------------------- CG graph per level
 static gse_status build_cg_graph(Matrix& M, int level) {
   SolverWs* ws = M.ws;
@@ -644,9 +764,29 @@ static gse_status build_cg_graph(Matrix& M, int level) {
   const int64_t n = M.rows;
   DotOut d = dot_to(ws, &ws->ctrl->pq);
   gse_status rc = launch_spmv(M, level, ws->p, ws->q, &d, cs, &ws->ctrl->event);
-  k_cg_update<<<ws->vgrid, 256, 0, cs>>>(ws->ctrl, ws->ring, ws->x, ws->r, ws->p, ws->q, n,
-                                         ws->partials, ws->ticket, h, 1, 0);
-  k_cg_xpay<<<ws->vgrid, 256, 0, cs>>>(ws->ctrl, ws->p, ws->r, n);
+  const int fg = fused_grid(M);
+  if (fg > 0) {
+    // cooperative fused tail (one grid barrier), see k_cg_fused
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(fg);
+    cfg.blockDim = dim3(256);
+    cfg.stream = cs;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t le = cudaLaunchKernelEx(&cfg, k_cg_fused, ws->ctrl, ws->ring, ws->x, ws->r,
+                                        ws->p, (const double*)ws->q, n, ws->partials, h, 1);
+    if (le != cudaSuccess) {
+      cudaStreamEndCapture(cs, nullptr);
+      return cuda_status(le, "cooperative k_cg_fused");
+    }
+  } else {
+    k_cg_update<<<ws->vgrid, 256, 0, cs>>>(ws->ctrl, ws->ring, ws->x, ws->r, ws->p, ws->q, n,
+                                           ws->partials, ws->ticket, h, 1, 0);
+    k_cg_xpay<<<ws->vgrid, 256, 0, cs>>>(ws->ctrl, ws->p, ws->r, n);
+  }
   cudaGraph_t captured;
   cudaError_t e = cudaStreamEndCapture(cs, &captured);
   if (rc != GSE_OK) return rc;

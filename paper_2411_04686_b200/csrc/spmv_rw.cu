@@ -85,7 +85,10 @@ template <int L, class T>
 __device__ __forceinline__ void issue_stage(const SpmvParams<T>& p, const Stage<L>& st,
                                             uint64_t* bar, uint32_t s, uint32_t e) {
   const uint32_t base = s & ~7u;
-  const uint32_t n = (e > base) ? ((e - base + 7u) & ~7u) : 0u;  // 8-element units
+  // 8-element units, plus 8 more: row walks read 8 slots unconditionally, and the over-copied
+  // elements are real stored entries (or the zero padding after nnz), so every gathered
+  // column stays in bounds; their products are masked to exact zeros
+  const uint32_t n = (e > base) ? ((e - base + 7u) & ~7u) + 8u : 0u;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads -> async writes
   mbar_arrive_expect_tx(bar, n * rw_elem_bytes<L>());
   if (n == 0) return;
@@ -108,18 +111,32 @@ __device__ __forceinline__ T walk_row(const SpmvParams<T>& p, const Stage<L>& st
     double v0[8];
     bool ok[8];
     T xv[8];
+    // 8 slots read unconditionally at immediate offsets: the stage holds >= 8 over-copied
+    // stored entries past every row (issue_stage), so the columns are valid; slots past
+    // the row end are masked to exact zeros below
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       ok[q] = j + q < j1;
-      const uint32_t jj = ok[q] ? j + q : j0;
-      c[q] = st.col[jj];
-      if constexpr (L == 0) v0[q] = st.val[jj];
-      if constexpr (L >= 1) h[q] = st.head[jj];
-      if constexpr (L >= 2) t1[q] = st.tail1[jj];
-      if constexpr (L == 3) t2[q] = st.tail2[jj];
+      c[q] = st.col[j + q];
+      if constexpr (L == 0) v0[q] = st.val[j + q];
+      if constexpr (L >= 1) h[q] = st.head[j + q];
+      if constexpr (L >= 2) t1[q] = st.tail1[j + q];
+      if constexpr (L == 3) t2[q] = st.tail2[j + q];
     }
+    // all 8 gathers issued before any product (ld.global.nc, volatile asm keeps the order)
 #pragma unroll
-    for (int q = 0; q < 8; ++q) xv[q] = __ldg(p.x + (c[q] & p.col_mask));
+    for (int q = 0; q < 8; ++q) {
+      const T* a = p.x + (c[q] & p.col_mask);
+      if constexpr (sizeof(T) == 8) {
+        double v;
+        asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(a));
+        xv[q] = v;
+      } else {
+        float v;
+        asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(a));
+        xv[q] = v;
+      }
+    }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       T prod;
@@ -166,7 +183,7 @@ __device__ __forceinline__ T walk_row(const SpmvParams<T>& p, const Stage<L>& st
 }
 
 template <int L, bool DOT, bool FAST, class T>
-__global__ void __launch_bounds__(SPMV_THREADS) k_spmv_rw(const SpmvParams<T> p) {
+__global__ void __launch_bounds__(SPMV_THREADS, 3) k_spmv_rw(const SpmvParams<T> p) {
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t bars[SPMV_WARPS][2];
   __shared__ long long sd64[64];
