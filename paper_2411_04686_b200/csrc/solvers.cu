@@ -467,9 +467,43 @@ __global__ void __launch_bounds__(256) k_gm_mgs(SolveCtrl* __restrict__ c, doubl
   const int m = c->restart;
   const double* vi = V + (size_t)i * n;
   double acc = 0.0;
-  if (i > 0) {
-    const double h = c->H[(i - 1) * m + j];
-    const double* vp = V + (size_t)(i - 1) * n;
+  // 16-byte accesses, 2 pairs in flight per thread (V rows are n doubles apart: pairs are
+  // 16-byte aligned only for even n, else the scalar loop)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const double h = i > 0 ? c->H[(i - 1) * m + j] : 0.0;
+  const double* vp = V + (size_t)(i > 0 ? i - 1 : 0) * n;
+  if ((n & 1) == 0) {
+    const int64_t n2 = n >> 1;
+    double2* w2 = reinterpret_cast<double2*>(w);
+    const double2* vi2 = reinterpret_cast<const double2*>(vi);
+    const double2* vp2 = reinterpret_cast<const double2*>(vp);
+    for (int64_t q = t0; q < n2; q += 2 * stride) {
+      double2 wv[2], a[2], bp[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int64_t e = q + k * stride;
+        if (e < n2) {
+          wv[k] = w2[e];
+          a[k] = vi2[e];
+          if (i > 0) bp[k] = vp2[e];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int64_t e = q + k * stride;
+        if (e < n2) {
+          if (i > 0) {
+            wv[k].x = __dsub_rn(wv[k].x, __dmul_rn(h, bp[k].x));
+            wv[k].y = __dsub_rn(wv[k].y, __dmul_rn(h, bp[k].y));
+            w2[e] = wv[k];
+          }
+          acc = __dadd_rn(acc, __dmul_rn(wv[k].x, a[k].x));
+          acc = __dadd_rn(acc, __dmul_rn(wv[k].y, a[k].y));
+        }
+      }
+    }
+  } else if (i > 0) {
     GRID_LOOP(q, n) {
       const double wv = __dsub_rn(w[q], __dmul_rn(h, vp[q]));
       w[q] = wv;
@@ -492,10 +526,38 @@ __global__ void __launch_bounds__(256) k_gm_last(SolveCtrl* __restrict__ c, doub
   const double h = c->H[j * m + j];
   const double* vj = V + (size_t)j * n;
   double acc = 0.0;
-  GRID_LOOP(q, n) {
-    const double wv = __dsub_rn(w[q], __dmul_rn(h, vj[q]));
-    w[q] = wv;
-    acc = __dadd_rn(acc, __dmul_rn(wv, wv));
+  if ((n & 1) == 0) {
+    const int64_t n2 = n >> 1, stride = (int64_t)gridDim.x * blockDim.x;
+    double2* w2 = reinterpret_cast<double2*>(w);
+    const double2* vj2 = reinterpret_cast<const double2*>(vj);
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n2; q += 2 * stride) {
+      double2 wv[2], a[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int64_t e = q + k * stride;
+        if (e < n2) {
+          wv[k] = w2[e];
+          a[k] = vj2[e];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int64_t e = q + k * stride;
+        if (e < n2) {
+          wv[k].x = __dsub_rn(wv[k].x, __dmul_rn(h, a[k].x));
+          wv[k].y = __dsub_rn(wv[k].y, __dmul_rn(h, a[k].y));
+          w2[e] = wv[k];
+          acc = __dadd_rn(acc, __dmul_rn(wv[k].x, wv[k].x));
+          acc = __dadd_rn(acc, __dmul_rn(wv[k].y, wv[k].y));
+        }
+      }
+    }
+  } else {
+    GRID_LOOP(q, n) {
+      const double wv = __dsub_rn(w[q], __dmul_rn(h, vj[q]));
+      w[q] = wv;
+      acc = __dadd_rn(acc, __dmul_rn(wv, wv));
+    }
   }
   double tot;
   if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0) {

@@ -34,10 +34,19 @@ __device__ __forceinline__ void products(const SpmvParams<T>& p, const long long
     if constexpr (L == 3) t2[k] = ok ? ld_nc_u32(p.tail2 + i) : 0u;
     if constexpr (SIDE && L >= 1) ei[k] = ok ? (ld_nc_u8(p.side + i) & 63u) : 0u;
   }
+  // all EPL gathers issued back to back (masked slots gather x[0], always valid) before any
+  // product: volatile asm keeps them together, the register budget of the launch bounds
+  // lets ptxas keep them in flight
 #pragma unroll
   for (int k = 0; k < EPL; ++k) {
     const bool ok = first + 32u * k < e;
-    xv[k] = ok ? __ldg(p.x + (c[k] & p.col_mask)) : (T)0;
+    const T* a = p.x + (c[k] & p.col_mask);
+    T v;
+    if constexpr (sizeof(T) == 8)
+      asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(a));
+    else
+      asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(a));
+    xv[k] = ok ? v : (T)0;
   }
 #pragma unroll
   for (int k = 0; k < EPL; ++k) {
@@ -54,7 +63,7 @@ __device__ __forceinline__ void products(const SpmvParams<T>& p, const long long
 }
 
 template <int L, bool SIDE, bool DOT, bool FAST, class T>
-__global__ void __launch_bounds__(SPMV_THREADS) k_spmv_sp(const SpmvParams<T> p) {
+__global__ void __launch_bounds__(SPMV_THREADS, 3) k_spmv_sp(const SpmvParams<T> p) {
   __shared__ __align__(16) T wprod[SPMV_WARPS][WTILE];
   __shared__ long long sd64[64];
   __shared__ int sd32[64];
