@@ -104,25 +104,29 @@ __global__ void __launch_bounds__(SPMV_THREADS, 3) k_spmv_sp(const SpmvParams<T>
         if (DOT) dacc += (double)p.x[r0] * (double)acc;
       }
     } else {
-      uint32_t ra = 0, rb = 0;
-      if (lane < nrows) {
-        ra = p.row_ptr[r0 + lane];
-        rb = p.row_ptr[r0 + lane + 1];
-      }
       T v[EPL];
       products<L, SIDE, FAST, T>(p, sd64, sd32, sc64, sc32, s + lane, e, v);
 #pragma unroll
       for (int k = 0; k < EPL; ++k) wp[lane + 32 * k] = v[k];
       __syncwarp();
-      for (uint32_t rr = lane; rr < nrows; rr += 32) {
-        if (rr >= 32) {
-          ra = p.row_ptr[r0 + rr];
-          rb = p.row_ptr[r0 + rr + 1];
-        }
+      // lpr lanes per row (power of two, 32 / nrows rounded down): with few, longer rows
+      // (power-law blocks hold ~10 rows) the sequential sums shrink by lpr; lane-per-row
+      // (lpr = 1, storage order) for stencil-like blocks.  Fixed lane->element map and a
+      // fixed shuffle tree: deterministic.
+      const uint32_t lpr = nrows >= 16 ? 1u : nrows >= 8 ? 2u : nrows >= 4 ? 4u : 8u;
+      const uint32_t rpw = 32u / lpr, sub = lane & (lpr - 1), grp = lane / lpr;
+      for (uint32_t base_r = 0; base_r < nrows; base_r += rpw) {
+        const uint32_t rr = base_r + grp;
         T sum = 0;
-        for (uint32_t j = ra - s; j < rb - s; ++j) sum += wp[j];
-        p.y[r0 + rr] = sum;
-        if (DOT) dacc += (double)p.x[r0 + rr] * (double)sum;
+        if (rr < nrows) {
+          const uint32_t ra = p.row_ptr[r0 + rr], rb = p.row_ptr[r0 + rr + 1];
+          for (uint32_t j = ra - s + sub; j < rb - s; j += lpr) sum += wp[j];
+        }
+        for (uint32_t o = lpr >> 1; o > 0; o >>= 1) sum += __shfl_down_sync(0xFFFFFFFFu, sum, o, lpr);
+        if (rr < nrows && sub == 0) {
+          p.y[r0 + rr] = sum;
+          if (DOT) dacc += (double)p.x[r0 + rr] * (double)sum;
+        }
       }
       __syncwarp();
     }

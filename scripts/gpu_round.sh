@@ -11,7 +11,7 @@ timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_$TAG.json 2>
 # launch list of the same workload (host-driven CG so ncu can see the kernels)
 GSE_NO_GRAPH=1 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
   --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv \
-  python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --spmv-reps 3 > /dev/null 2>&1
+  python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-sweep > /dev/null 2>&1
 # full capture of the dominant kernel (level-1 SpMV of the CG: DOT variant) + levels 2/3
 PROF_CG_ITERS=4 GSE_NO_GRAPH=1 timeout 900 ncu --set full --clock-control none --import-source on \
   -k regex:k_spmv -c 5 -o gpurun_out/prof_$TAG python scripts/prof_spmv.py > gpurun_out/prof_$TAG.log 2>&1
