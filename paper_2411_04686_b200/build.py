@@ -13,6 +13,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills"]
+# developer A/B knob: extra nvcc flags (e.g. -D switches); a change forces a rebuild
+EXTRA = os.environ.get("GSE_NVCC_EXTRA", "").split()
+STAMP = os.path.join(HERE, "build", "flags.txt")
 
 
 def sources():
@@ -28,6 +31,12 @@ def stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
+    try:
+        if open(STAMP).read() != " ".join(EXTRA):
+            return True
+    except OSError:
+        if EXTRA:
+            return True
     return any(os.path.getmtime(p) > t for p in deps())
 
 
@@ -40,7 +49,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(HERE, "..", "include"), "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *EXTRA, "-I", os.path.join(HERE, "..", "include"), "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((subprocess.Popen(cmd), src))
@@ -52,6 +61,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lnccl"]
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:
+        f.write(" ".join(EXTRA))
     return LIB
 
 

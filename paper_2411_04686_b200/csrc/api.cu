@@ -1,6 +1,7 @@
 // api.cu -- the extern "C" entry points of include/gse.h: argument validation, host/device
 // pointer staging, device selection, error detail, allocator hook.  No arithmetic of the
 // method lives here; every step runs in the kernels of encode.cu / spmv.cu / solvers.cu.
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -83,6 +84,14 @@ int num_sms(int device) {
     cache[device] = v > 0 ? v : 148;
   }
   return cache[device];
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("GSE_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
 }
 
 struct DeviceGuard {

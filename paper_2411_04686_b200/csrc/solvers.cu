@@ -20,6 +20,7 @@
 #include <cooperative_groups.h>
 
 #include <cmath>
+#include <cstddef>
 #include <cstdlib>
 #include <mutex>
 #include <vector>
@@ -44,6 +45,7 @@ struct SolveCtrl {
   double rr, rr_new, pq, beta, resid;
   double dot;  // scratch reduction target
   double rr_part;  // distributed CG: this rank's r.r partial (allreduced before k_cg_events)
+  double alpha;    // CG: step of the current iteration, applied to x by k_cg_xpay (0: none)
   int upd_ok;
   long long iter, max_iters;
   int level, event, stop, stepped, max_level;
@@ -77,6 +79,24 @@ struct SolverWs {
   int gm_restart = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
+
+// The scalar head of SolveCtrl (everything before the GMRES arrays).  The single thread
+// that runs the CG event logic works on a shared-memory snapshot loaded by warp 0 at
+// kernel start (overlapped with the vector pass) and writes it back: done directly on
+// global memory the logic is a chain of ~20 dependent L2 round trips (~7 us per iteration).
+constexpr int CTRL_HEAD_WORDS = (int)(offsetof(SolveCtrl, restart) / 8);
+static_assert(offsetof(SolveCtrl, restart) % 8 == 0, "SolveCtrl head must be 8-byte words");
+
+__device__ __forceinline__ void ctrl_load_head(const SolveCtrl* c, unsigned long long* sm) {
+  if (threadIdx.x < 32) {
+    const unsigned long long* g = reinterpret_cast<const unsigned long long*>(c);
+    for (int i = threadIdx.x; i < CTRL_HEAD_WORDS; i += 32) sm[i] = __ldcg(g + i);
+  }
+}
+__device__ __forceinline__ void ctrl_store_head(SolveCtrl* c, const unsigned long long* sm) {
+  unsigned long long* g = reinterpret_cast<unsigned long long*>(c);
+  for (int i = 0; i < CTRL_HEAD_WORDS; ++i) g[i] = sm[i];
+}
 
 // ---------------------------------------------------------------- reductions
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -175,9 +195,11 @@ __device__ int monitor_check(const SolveCtrl* c, const double* ring, long long j
 
 // ---------------------------------------------------------------- generic vector kernels
 // tot = a . b  (into *out)
-__global__ void __launch_bounds__(256) k_dot(const double* __restrict__ a,
+__global__ void __launch_bounds__(256, 4) k_dot(const double* __restrict__ a,
                                              const double* __restrict__ b, int64_t n,
                                              double* partials, unsigned* ticket, double* out) {
+  pdl_wait();
+  pdl_trigger();
   double acc = 0.0;
   GRID_LOOP(i, n) acc = __dadd_rn(acc, __dmul_rn(a[i], b[i]));
   double tot;
@@ -185,11 +207,13 @@ __global__ void __launch_bounds__(256) k_dot(const double* __restrict__ a,
 }
 
 // r = b - Ax ; (optionally p = r) ; *out = r.r
-__global__ void __launch_bounds__(256) k_residual(const double* __restrict__ b,
+__global__ void __launch_bounds__(256, 4) k_residual(const double* __restrict__ b,
                                                   const double* Ax,  // may alias r
                                                   double* r, double* __restrict__ p,
                                                   int64_t n, double* partials, unsigned* ticket,
                                                   double* out) {
+  pdl_wait();
+  pdl_trigger();
   double acc = 0.0;
   GRID_LOOP(i, n) {
     const double v = __dsub_rn(b[i], Ax[i]);
@@ -236,50 +260,51 @@ __device__ void cg_events(SolveCtrl* c, double* ring, double tot, bool ok,
   }
 }
 
-// x += alpha p ; r -= alpha q ; rr_new = r.r ; monitor ; events
-__global__ void __launch_bounds__(256) k_cg_update(SolveCtrl* __restrict__ c, double* ring,
-                                                   double* __restrict__ x, double* __restrict__ r,
-                                                   const double* __restrict__ p,
+// r -= alpha q ; rr_new = r.r ; monitor ; events.  x += alpha p is deferred to k_cg_xpay,
+// which reads p anyway (same arithmetic, one vector pass less per iteration); alpha is
+// handed over in c->alpha (0 when this iteration did not update).
+__global__ void __launch_bounds__(256, 4) k_cg_update(SolveCtrl* __restrict__ c, double* ring,
+                                                   double* __restrict__ r,
                                                    const double* __restrict__ q, int64_t n,
                                                    double* partials, unsigned* ticket,
                                                    cudaGraphConditionalHandle handle,
                                                    int in_graph, int defer) {
-  if (c->event != EV_NONE) return;  // host-driven mode: iterations after an event are no-ops
+  pdl_wait();
+  pdl_trigger();
+  __shared__ unsigned long long sctrl[CTRL_HEAD_WORDS];
+  if (c->event != EV_NONE) {  // host-driven mode: iterations after an event are no-ops
+    if (blockIdx.x == 0 && threadIdx.x == 0) c->alpha = 0.0;
+    return;
+  }
+  ctrl_load_head(c, sctrl);  // consumed only by the last CTA, after grid_sum's barriers
   const double pq = c->pq, rr = c->rr;
   const bool ok = (pq > 0.0) && isfinite(pq);
   const double alpha = rr / pq;
   double acc = 0.0;
   if (ok) {
-    // 16-byte accesses (pairs of elements), 2 pairs in flight per thread; the element
+    // 16-byte accesses (pairs of elements), 4 pairs in flight per thread; the element
     // order of each thread (and so its reduction order) is fixed by the grid
     const int64_t n2 = n >> 1;
-    const double2* __restrict__ p2 = reinterpret_cast<const double2*>(p);
     const double2* __restrict__ q2 = reinterpret_cast<const double2*>(q);
-    double2* __restrict__ x2 = reinterpret_cast<double2*>(x);
     double2* __restrict__ r2 = reinterpret_cast<double2*>(r);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += 2 * stride) {
-      double2 xv[2], pv[2], rv[2], qv[2];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += 4 * stride) {
+      double2 rv[4], qv[4];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
+      for (int k = 0; k < 4; ++k) {
         const int64_t j = i + k * stride;
         if (j < n2) {
-          xv[k] = x2[j];
-          pv[k] = p2[j];
           rv[k] = r2[j];
           qv[k] = q2[j];
         }
       }
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
+      for (int k = 0; k < 4; ++k) {
         const int64_t j = i + k * stride;
         if (j < n2) {
-          double2 xo, ro;
-          xo.x = __dadd_rn(xv[k].x, __dmul_rn(alpha, pv[k].x));
-          xo.y = __dadd_rn(xv[k].y, __dmul_rn(alpha, pv[k].y));
+          double2 ro;
           ro.x = __dsub_rn(rv[k].x, __dmul_rn(alpha, qv[k].x));
           ro.y = __dsub_rn(rv[k].y, __dmul_rn(alpha, qv[k].y));
-          x2[j] = xo;
           r2[j] = ro;
           acc = __dadd_rn(acc, __dmul_rn(ro.x, ro.x));
           acc = __dadd_rn(acc, __dmul_rn(ro.y, ro.y));
@@ -288,7 +313,6 @@ __global__ void __launch_bounds__(256) k_cg_update(SolveCtrl* __restrict__ c, do
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd tail element
       const int64_t j = n - 1;
-      x[j] = __dadd_rn(x[j], __dmul_rn(alpha, p[j]));
       const double ri = __dsub_rn(r[j], __dmul_rn(alpha, q[j]));
       r[j] = ri;
       acc = __dadd_rn(acc, __dmul_rn(ri, ri));
@@ -296,17 +320,22 @@ __global__ void __launch_bounds__(256) k_cg_update(SolveCtrl* __restrict__ c, do
   }
   double tot;
   if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0) {
+    SolveCtrl* sc = reinterpret_cast<SolveCtrl*>(sctrl);
+    sc->alpha = ok ? alpha : 0.0;
     if (defer) {  // distributed: r.r is this rank's partial; k_cg_events runs after the allreduce
-      c->rr_part = tot;
-      c->upd_ok = ok ? 1 : 0;
+      sc->rr_part = tot;
+      sc->upd_ok = ok ? 1 : 0;
     } else {
-      cg_events(c, ring, tot, ok, handle, in_graph);
+      cg_events(sc, ring, tot, ok, handle, in_graph);
     }
+    ctrl_store_head(c, sctrl);
   }
 }
 
 // distributed CG: the event logic on the allreduced r.r (all ranks decide identically)
 __global__ void k_cg_events(SolveCtrl* __restrict__ c, double* ring) {
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x != 0 || blockIdx.x != 0 || c->event != EV_NONE) return;
   cg_events(c, ring, c->rr_part, c->upd_ok != 0, 0, 0);
 }
@@ -377,47 +406,67 @@ __global__ void __launch_bounds__(256, 4) k_cg_fused(SolveCtrl* __restrict__ c, 
   }
 }
 
-// p = r + beta p (skipped when an event is pending: the host restarts / stops)
-__global__ void __launch_bounds__(256) k_cg_xpay(const SolveCtrl* __restrict__ c,
-                                                 double* __restrict__ p,
+// x += alpha p (the update deferred by k_cg_update) ; p = r + beta p (skipped when an event
+// is pending: the host restarts / stops).  Both read the old p.
+__global__ void __launch_bounds__(256, 4) k_cg_xpay(const SolveCtrl* __restrict__ c,
+                                                 double* __restrict__ x, double* __restrict__ p,
                                                  const double* __restrict__ r, int64_t n) {
-  if (c->event != EV_NONE) return;
-  const double beta = c->beta;
+  pdl_wait();
+  pdl_trigger();
+  const double alpha = c->alpha, beta = c->beta;
+  const bool do_x = alpha != 0.0, do_p = c->event == EV_NONE;
+  if (!do_x && !do_p) return;
   const int64_t n2 = n >> 1;
+  double2* __restrict__ x2 = reinterpret_cast<double2*>(x);
   double2* __restrict__ p2 = reinterpret_cast<double2*>(p);
   const double2* __restrict__ r2 = reinterpret_cast<const double2*>(r);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += 2 * stride) {
-    double2 pv[2], rv[2];
+    double2 pv[2], rv[2], xv[2];
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const int64_t j = i + k * stride;
       if (j < n2) {
         pv[k] = p2[j];
-        rv[k] = r2[j];
+        if (do_p) rv[k] = r2[j];
+        if (do_x) xv[k] = x2[j];
       }
     }
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const int64_t j = i + k * stride;
       if (j < n2) {
-        double2 o;
-        o.x = __dadd_rn(rv[k].x, __dmul_rn(beta, pv[k].x));
-        o.y = __dadd_rn(rv[k].y, __dmul_rn(beta, pv[k].y));
-        p2[j] = o;
+        if (do_x) {
+          double2 o;
+          o.x = __dadd_rn(xv[k].x, __dmul_rn(alpha, pv[k].x));
+          o.y = __dadd_rn(xv[k].y, __dmul_rn(alpha, pv[k].y));
+          x2[j] = o;
+        }
+        if (do_p) {
+          double2 o;
+          o.x = __dadd_rn(rv[k].x, __dmul_rn(beta, pv[k].x));
+          o.y = __dadd_rn(rv[k].y, __dmul_rn(beta, pv[k].y));
+          p2[j] = o;
+        }
       }
     }
   }
-  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0)
-    p[n - 1] = __dadd_rn(r[n - 1], __dmul_rn(beta, p[n - 1]));
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t j = n - 1;
+    const double pv = p[j];
+    if (do_x) x[j] = __dadd_rn(x[j], __dmul_rn(alpha, pv));
+    if (do_p) p[j] = __dadd_rn(r[j], __dmul_rn(beta, pv));
+  }
 }
 
 // ---------------------------------------------------------------- GMRES kernels
 // prologue: w = b - A x ; beta = ||w|| ; explicit convergence / budget checks
-__global__ void __launch_bounds__(256) k_gm_restart(SolveCtrl* __restrict__ c,
+__global__ void __launch_bounds__(256, 4) k_gm_restart(SolveCtrl* __restrict__ c,
                                                     const double* __restrict__ b,
                                                     double* __restrict__ w, int64_t n,
                                                     double* partials, unsigned* ticket) {
+  pdl_wait();
+  pdl_trigger();
   double acc = 0.0;
   GRID_LOOP(i, n) {
     const double v = __dsub_rn(b[i], w[i]);
@@ -450,19 +499,23 @@ __global__ void __launch_bounds__(256) k_gm_restart(SolveCtrl* __restrict__ c,
 }
 
 // dst = src / *den   (skipped when stopped)
-__global__ void __launch_bounds__(256) k_gm_scale(const SolveCtrl* __restrict__ c,
+__global__ void __launch_bounds__(256, 4) k_gm_scale(const SolveCtrl* __restrict__ c,
                                                   const double* __restrict__ src,
                                                   double* __restrict__ dst, int64_t n,
                                                   int use_hn) {
+  pdl_wait();
+  pdl_trigger();
   if (c->stop) return;
   const double den = use_hn ? c->hn : c->beta;
   GRID_LOOP(i, n) dst[i] = src[i] / den;
 }
 
 // MGS step i of inner iteration j: (i > 0) w -= H[i-1][j] v_{i-1}; H[i][j] = w . v_i
-__global__ void __launch_bounds__(256) k_gm_mgs(SolveCtrl* __restrict__ c, double* __restrict__ w,
+__global__ void __launch_bounds__(256, 4) k_gm_mgs(SolveCtrl* __restrict__ c, double* __restrict__ w,
                                                 const double* __restrict__ V, int64_t n, int i,
                                                 int j, double* partials, unsigned* ticket) {
+  pdl_wait();
+  pdl_trigger();
   if (c->stop) return;
   const int m = c->restart;
   const double* vi = V + (size_t)i * n;
@@ -517,10 +570,12 @@ __global__ void __launch_bounds__(256) k_gm_mgs(SolveCtrl* __restrict__ c, doubl
 }
 
 // last MGS step: w -= H[j][j] v_j ; hn = ||w|| ; Givens (R18) ; estimate ; monitor
-__global__ void __launch_bounds__(256) k_gm_last(SolveCtrl* __restrict__ c, double* ring,
+__global__ void __launch_bounds__(256, 4) k_gm_last(SolveCtrl* __restrict__ c, double* ring,
                                                  double* __restrict__ w,
                                                  const double* __restrict__ V, int64_t n, int j,
                                                  double* partials, unsigned* ticket) {
+  pdl_wait();
+  pdl_trigger();
   if (c->stop) return;
   const int m = c->restart;
   const double h = c->H[j * m + j];
@@ -617,6 +672,8 @@ __global__ void __launch_bounds__(256) k_gm_last(SolveCtrl* __restrict__ c, doub
 
 // back substitution H[0:k,0:k] y = g[0:k] (one thread; k <= restart)
 __global__ void k_gm_backsolve(SolveCtrl* __restrict__ c) {
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (c->event == EV_ABORT) {
     c->k = 0;
@@ -631,9 +688,11 @@ __global__ void k_gm_backsolve(SolveCtrl* __restrict__ c) {
 }
 
 // x += sum_i y_i v_i (same per-element operation order as the oracle)
-__global__ void __launch_bounds__(256) k_gm_xupdate(const SolveCtrl* __restrict__ c,
+__global__ void __launch_bounds__(256, 4) k_gm_xupdate(const SolveCtrl* __restrict__ c,
                                                     double* __restrict__ x,
                                                     const double* __restrict__ V, int64_t n) {
+  pdl_wait();
+  pdl_trigger();
   const int k = c->k;
   if (k == 0) return;
   GRID_LOOP(q, n) {
@@ -686,7 +745,7 @@ static gse_status ensure_ws(Matrix& M, int64_t ring_t, int gm_restart, cudaStrea
   if (!ws) {
     ws = new SolverWs();
     ws->n = n;
-    ws->vgrid = num_sms(M.device) * 8;
+    ws->vgrid = num_sms(M.device) * 4;  // one wave: every vector kernel fits 4 CTAs of 256 per SM
     const size_t nn = (size_t)(n > 0 ? n : 1);
     ws->x = dev_alloc_n<double>(nn, s);
     ws->r = dev_alloc_n<double>(nn, s);
@@ -845,9 +904,9 @@ static gse_status build_cg_graph(Matrix& M, int level) {
       return cuda_status(le, "cooperative k_cg_fused");
     }
   } else {
-    k_cg_update<<<ws->vgrid, 256, 0, cs>>>(ws->ctrl, ws->ring, ws->x, ws->r, ws->p, ws->q, n,
-                                           ws->partials, ws->ticket, h, 1, 0);
-    k_cg_xpay<<<ws->vgrid, 256, 0, cs>>>(ws->ctrl, ws->p, ws->r, n);
+    launch_k(k_cg_update, ws->vgrid, 256, 0, cs, ws->ctrl, ws->ring, ws->r, ws->q, n, ws->partials,
+                                           ws->ticket, h, 1, 0);
+    launch_k(k_cg_xpay, ws->vgrid, 256, 0, cs, ws->ctrl, ws->x, ws->p, ws->r, n);
   }
   cudaGraph_t captured;
   cudaError_t e = cudaStreamEndCapture(cs, &captured);
@@ -905,7 +964,7 @@ static gse_status residual(Matrix& M, int level, const double* x, double* r, dou
   gse_status rc = spmv_local(M, level, x, ws->q, nullptr, s);
   if (rc != GSE_OK) return rc;
   rep.spmv_count[level - 1]++;
-  k_residual<<<ws->vgrid, 256, 0, s>>>(ws->b, ws->q, r, p, M.rows, ws->partials, ws->ticket,
+  launch_k(k_residual, ws->vgrid, 256, 0, s, ws->b, ws->q, r, p, M.rows, ws->partials, ws->ticket,
                                        out);
   GSE_CUDA_TRY(cudaGetLastError());
   return dist_allreduce_sum(M, out, 1, s);
@@ -936,7 +995,7 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
   GSE_CUDA_TRY(cudaMemcpyAsync(ws->b, b, n * 8, cudaMemcpyDeviceToDevice, s));
   GSE_CUDA_TRY(cudaMemcpyAsync(ws->x, x, n * 8, cudaMemcpyDeviceToDevice, s));
   // ||b||, r0 = b - A_L x0, p0 = r0, rr
-  k_dot<<<ws->vgrid, 256, 0, s>>>(ws->b, ws->b, n, ws->partials, ws->ticket, &ws->ctrl->dot);
+  launch_k(k_dot, ws->vgrid, 256, 0, s, ws->b, ws->b, n, ws->partials, ws->ticket, &ws->ctrl->dot);
   GSE_CUDA_TRY(cudaGetLastError());
   rc = dist_allreduce_sum(M, &ws->ctrl->dot, 1, s);
   if (rc != GSE_OK) return rc;
@@ -1009,12 +1068,12 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
           if (rc != GSE_OK) return rc;
           rc = dist_allreduce_sum(M, &ws->ctrl->pq, 1, s);
           if (rc != GSE_OK) return rc;
-          k_cg_update<<<ws->vgrid, 256, 0, s>>>(ws->ctrl, ws->ring, ws->x, ws->r, ws->p, ws->q,
-                                                n, ws->partials, ws->ticket, 0, 0, 1);
+          launch_k(k_cg_update, ws->vgrid, 256, 0, s, ws->ctrl, ws->ring, ws->r, ws->q, n,
+                                                ws->partials, ws->ticket, 0, 0, 1);
           rc = dist_allreduce_sum(M, &ws->ctrl->rr_part, 1, s);
           if (rc != GSE_OK) return rc;
-          k_cg_events<<<1, 32, 0, s>>>(ws->ctrl, ws->ring);
-          k_cg_xpay<<<ws->vgrid, 256, 0, s>>>(ws->ctrl, ws->p, ws->r, n);
+          launch_k(k_cg_events, 1, 32, 0, s, ws->ctrl, ws->ring);
+          launch_k(k_cg_xpay, ws->vgrid, 256, 0, s, ws->ctrl, ws->x, ws->p, ws->r, n);
         }
         GSE_CUDA_TRY(cudaGetLastError());
         rc = read_ctrl(ws, s);
@@ -1027,9 +1086,9 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
         for (int bt = 0; bt < 16; ++bt) {
           rc = launch_spmv(M, level, ws->p, ws->q, &d, s, &ws->ctrl->event);
           if (rc != GSE_OK) return rc;
-          k_cg_update<<<ws->vgrid, 256, 0, s>>>(ws->ctrl, ws->ring, ws->x, ws->r, ws->p, ws->q,
-                                                n, ws->partials, ws->ticket, 0, 0, 0);
-          k_cg_xpay<<<ws->vgrid, 256, 0, s>>>(ws->ctrl, ws->p, ws->r, n);
+          launch_k(k_cg_update, ws->vgrid, 256, 0, s, ws->ctrl, ws->ring, ws->r, ws->q, n,
+                                                ws->partials, ws->ticket, 0, 0, 0);
+          launch_k(k_cg_xpay, ws->vgrid, 256, 0, s, ws->ctrl, ws->x, ws->p, ws->r, n);
         }
         GSE_CUDA_TRY(cudaGetLastError());
         rc = read_ctrl(ws, s);
@@ -1124,18 +1183,18 @@ static gse_status build_gm_graph(Matrix& M, int level, int restart) {
   double* w = ws->tmp;
   GSE_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
   gse_status rc = launch_spmv(M, level, ws->x, w, nullptr, cs);
-  k_gm_restart<<<ws->vgrid, 256, 0, cs>>>(c, ws->b, w, n, ws->partials, ws->ticket);
-  k_gm_scale<<<ws->vgrid, 256, 0, cs>>>(c, w, ws->V, n, 0);
+  launch_pdl(k_gm_restart, ws->vgrid, 256, 0, cs, c, ws->b, w, n, ws->partials, ws->ticket);
+  launch_pdl(k_gm_scale, ws->vgrid, 256, 0, cs, c, w, ws->V, n, 0);
   for (int j = 0; j < restart && rc == GSE_OK; ++j) {
     rc = launch_spmv_guarded(M, level, ws->V + (size_t)j * n, w, &c->stop, cs);
     for (int i = 0; i <= j; ++i)
-      k_gm_mgs<<<ws->vgrid, 256, 0, cs>>>(c, w, ws->V, n, i, j, ws->partials, ws->ticket);
-    k_gm_last<<<ws->vgrid, 256, 0, cs>>>(c, ws->ring, w, ws->V, n, j, ws->partials, ws->ticket);
+      launch_pdl(k_gm_mgs, ws->vgrid, 256, 0, cs, c, w, ws->V, n, i, j, ws->partials, ws->ticket);
+    launch_pdl(k_gm_last, ws->vgrid, 256, 0, cs, c, ws->ring, w, ws->V, n, j, ws->partials, ws->ticket);
     if (j + 1 < restart)
-      k_gm_scale<<<ws->vgrid, 256, 0, cs>>>(c, w, ws->V + (size_t)(j + 1) * n, n, 1);
+      launch_pdl(k_gm_scale, ws->vgrid, 256, 0, cs, c, w, ws->V + (size_t)(j + 1) * n, n, 1);
   }
-  k_gm_backsolve<<<1, 32, 0, cs>>>(c);
-  k_gm_xupdate<<<ws->vgrid, 256, 0, cs>>>(c, ws->x, ws->V, n);
+  launch_pdl(k_gm_backsolve, 1, 32, 0, cs, c);
+  launch_pdl(k_gm_xupdate, ws->vgrid, 256, 0, cs, c, ws->x, ws->V, n);
   cudaGraph_t g;
   cudaError_t e = cudaStreamEndCapture(cs, &g);
   if (rc != GSE_OK) return rc;
@@ -1157,7 +1216,7 @@ gse_status solve_gmres(Matrix& M, const double* b, double* x, double tol, int re
   GSE_CUDA_TRY(cudaEventRecord(ws->ev0, s));
   GSE_CUDA_TRY(cudaMemcpyAsync(ws->b, b, n * 8, cudaMemcpyDeviceToDevice, s));
   GSE_CUDA_TRY(cudaMemcpyAsync(ws->x, x, n * 8, cudaMemcpyDeviceToDevice, s));
-  k_dot<<<ws->vgrid, 256, 0, s>>>(ws->b, ws->b, n, ws->partials, ws->ticket, &ws->ctrl->dot);
+  launch_k(k_dot, ws->vgrid, 256, 0, s, ws->b, ws->b, n, ws->partials, ws->ticket, &ws->ctrl->dot);
   GSE_CUDA_TRY(cudaGetLastError());
   rc = read_ctrl(ws, s);
   if (rc != GSE_OK) return rc;

@@ -192,7 +192,6 @@ __global__ void __launch_bounds__(SPMV_THREADS, 3) k_spmv_rw(const SpmvParams<T>
   __shared__ float sc32[64];
   __shared__ double ssc64[128];  // sign-folded scales: [2 EI + sign] = (sign ? -1 : 1) scale
   __shared__ float ssc32[128];
-  if (p.stop && *p.stop) return;
   if (threadIdx.x < 128) {
     const int t = threadIdx.x;
     if constexpr (sizeof(T) == 8)
@@ -233,9 +232,17 @@ __global__ void __launch_bounds__(SPMV_THREADS, 3) k_spmv_rw(const SpmvParams<T>
     }
     return B;
   };
+  // prologue on constant data (tables, row pointers, the first tile of planes) overlaps
+  // the previous kernel's drain under programmatic dependent launch
   Bounds cur_b = bounds(g), nxt_b = bounds(g + W);
   if (g < ng && lane == 0)
     issue_stage<L>(p, Stage<L>(wbase, N), &bars[warp][0], cur_b.a, cur_b.c);
+  pdl_wait();
+  if (p.stop && *p.stop) {  // drain the issued copy before the CTA exits
+    if (g < ng) mbar_wait(&bars[warp][0], 0);
+    return;
+  }
+  pdl_trigger();
   uint32_t it = 0;
   for (; g < ng; g += W, ++it) {
     const uint32_t cur = it & 1u;
@@ -282,7 +289,7 @@ static void go(const Matrix& M, const SpmvParams<T>& p, cudaStream_t s) {
   const int64_t want = (M.n_groups + SPMV_WARPS - 1) / SPMV_WARPS;
   int g = (int)(want < cache[dev] ? want : cache[dev]);
   if (g < 1) g = 1;
-  kern<<<g, SPMV_THREADS, smem, s>>>(p);
+  launch_k(kern, g, SPMV_THREADS, smem, s, p);
 }
 
 template <int L, bool DOT, class T>

@@ -69,8 +69,10 @@ __global__ void __launch_bounds__(SPMV_THREADS, 3) k_spmv_sp(const SpmvParams<T>
   __shared__ int sd32[64];
   __shared__ double sc64[64];
   __shared__ float sc32[64];
+  stage_tables<L>(p, sd64, sd32, sc64, sc32);  // constant data: before the PDL wait
+  pdl_wait();
   if (p.stop && *p.stop) return;
-  stage_tables<L>(p, sd64, sd32, sc64, sc32);
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   T* wp = wprod[warp];
   double dacc = 0.0;
@@ -140,7 +142,7 @@ template <int L, bool SIDE, bool DOT, bool FAST, class T>
 static void go(const Matrix& M, const SpmvParams<T>& p, cudaStream_t s) {
   static int cache[64] = {0};
   const int g = persistent_grid(k_spmv_sp<L, SIDE, DOT, FAST, T>, M.device, M.n_blocks, cache);
-  k_spmv_sp<L, SIDE, DOT, FAST, T><<<g, SPMV_THREADS, 0, s>>>(p);
+  launch_k(k_spmv_sp<L, SIDE, DOT, FAST, T>, g, SPMV_THREADS, 0, s, p);
 }
 
 template <int L, bool DOT, class T>
