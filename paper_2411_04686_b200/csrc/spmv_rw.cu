@@ -99,6 +99,9 @@ __device__ __forceinline__ void issue_stage(const SpmvParams<T>& p, const Stage<
   if constexpr (L == 3) bulk_g2s(st.tail2, p.tail2 + base, 4 * n, bar);
 }
 
+// index of the zero entry of the sign-folded scale tables: masked slots decode to exact 0
+constexpr uint32_t SSC_ZERO = 128;
+
 // sum of one row, elements [j0, j1) of the stage, in storage order
 template <int L, bool FAST, class T>
 __device__ __forceinline__ T walk_row(const SpmvParams<T>& p, const Stage<L>& st, uint32_t j0,
@@ -107,16 +110,15 @@ __device__ __forceinline__ T walk_row(const SpmvParams<T>& p, const Stage<L>& st
                                       const double* sc64, const float* sc32) {
   T sum = 0;
   for (uint32_t j = j0; j < j1; j += 8) {
+    const uint32_t nrem = j1 - j;  // slots q >= nrem lie past the row end
     uint32_t c[8], h[8], t1[8], t2[8];
     double v0[8];
-    bool ok[8];
     T xv[8];
     // 8 slots read unconditionally at immediate offsets: the stage holds >= 8 over-copied
     // stored entries past every row (issue_stage), so the columns are valid; slots past
     // the row end are masked to exact zeros below
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      ok[q] = j + q < j1;
       c[q] = st.col[j + q];
       if constexpr (L == 0) v0[q] = st.val[j + q];
       if constexpr (L >= 1) h[q] = st.head[j + q];
@@ -139,27 +141,29 @@ __device__ __forceinline__ T walk_row(const SpmvParams<T>& p, const Stage<L>& st
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
+      const bool ok = (uint32_t)q < nrem;
       T prod;
       if constexpr (L == 0) {
-        prod = (T)__dmul_rn(ok[q] ? v0[q] : 0.0, (double)xv[q]);
+        prod = (T)__dmul_rn(ok ? v0[q] : 0.0, (double)xv[q]);
       } else if constexpr (FAST) {
-        const uint32_t idx = (__funnelshift_rc(c[q], 0u, p.ei_shift) << 1) | (h[q] >> 15);
+        // scale index = EI | sign << ei_bits in one funnel shift (col's top bits are EI);
+        // a masked slot selects the zero entry
+        uint32_t idx = __funnelshift_rc(c[q], h[q] >> 15, p.ei_shift);
+        idx = ok ? idx : SSC_ZERO;
         if constexpr (L == 1) {
-          const uint32_t D = ok[q] ? (h[q] & 0x7FFFu) : 0u;
+          const uint32_t D = h[q] & 0x7FFFu;
           if constexpr (sizeof(T) == 8)
             prod = __dmul_rn(__dmul_rn((double)D, ssc64[idx]), xv[q]);
           else
             prod = __fmul_rn(__fmul_rn((float)D, ssc32[idx]), xv[q]);
         } else if constexpr (L == 2) {
-          const uint32_t D = ok[q] ? (((h[q] & 0x7FFFu) << 16) | t1[q]) : 0u;
+          const uint32_t D = ((h[q] & 0x7FFFu) << 16) | t1[q];
           if constexpr (sizeof(T) == 8)
             prod = __dmul_rn(__dmul_rn((double)D, ssc64[idx]), xv[q]);
           else
             prod = __fmul_rn(__fmul_rn(__uint2float_rz(D), ssc32[idx]), xv[q]);
         } else {
-          const uint64_t D =
-              ok[q] ? (((uint64_t)(h[q] & 0x7FFFu) << 48) | ((uint64_t)t1[q] << 32) | t2[q])
-                    : 0ull;
+          const uint64_t D = ((uint64_t)(h[q] & 0x7FFFu) << 48) | ((uint64_t)t1[q] << 32) | t2[q];
           if constexpr (sizeof(T) == 8)
             prod = __dmul_rn(__dmul_rn(__ull2double_rz(D), ssc64[idx]), xv[q]);
           else
@@ -170,10 +174,10 @@ __device__ __forceinline__ T walk_row(const SpmvParams<T>& p, const Stage<L>& st
         const uint32_t tt1 = L >= 2 ? t1[q] : 0u, tt2 = L == 3 ? t2[q] : 0u;
         if constexpr (sizeof(T) == 8) {
           const double a = dec64<L, false>(h[q], tt1, tt2, sd64, sc64, ei);
-          prod = __dmul_rn(ok[q] ? a : 0.0, xv[q]);
+          prod = __dmul_rn(ok ? a : 0.0, xv[q]);
         } else {
           const float a = dec32<L, false>(h[q], tt1, tt2, sd32, sc32, ei);
-          prod = __fmul_rn(ok[q] ? a : 0.0f, xv[q]);
+          prod = __fmul_rn(ok ? a : 0.0f, xv[q]);
         }
       }
       sum += prod;
@@ -190,14 +194,17 @@ __global__ void __launch_bounds__(SPMV_THREADS, 3) k_spmv_rw(const SpmvParams<T>
   __shared__ int sd32[64];
   __shared__ double sc64[64];
   __shared__ float sc32[64];
-  __shared__ double ssc64[128];  // sign-folded scales: [2 EI + sign] = (sign ? -1 : 1) scale
-  __shared__ float ssc32[128];
-  if (threadIdx.x < 128) {
-    const int t = threadIdx.x;
+  // sign-folded scales: [EI | sign << ei_bits] = (sign ? -1 : 1) scale; [SSC_ZERO] = 0
+  __shared__ double ssc64[SSC_ZERO + 1];
+  __shared__ float ssc32[SSC_ZERO + 1];
+  if (threadIdx.x <= SSC_ZERO) {
+    const uint32_t t = threadIdx.x, eb = 32u - (uint32_t)p.ei_shift;
+    const uint32_t sign = t >> eb, ei = t & ((1u << eb) - 1u);
+    const bool live = t < SSC_ZERO && sign <= 1u;
     if constexpr (sizeof(T) == 8)
-      ssc64[t] = (t & 1) ? -p.sc64[t >> 1] : p.sc64[t >> 1];
+      ssc64[t] = live ? (sign ? -p.sc64[ei] : p.sc64[ei]) : 0.0;
     else
-      ssc32[t] = (t & 1) ? -p.sc32[t >> 1] : p.sc32[t >> 1];
+      ssc32[t] = live ? (sign ? -p.sc32[ei] : p.sc32[ei]) : 0.0f;
   }
   stage_tables<L>(p, sd64, sd32, sc64, sc32);
   __syncthreads();
