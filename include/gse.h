@@ -91,6 +91,7 @@ typedef struct {
   int64_t n_zero_values; /* zero / subnormal inputs encoded as signed zero (R2)              */
   int device;
   size_t plane_bytes[5]; /* col_ei, head, tail1, tail2, side_ei (kind GSE); col, val (FP64) */
+  int spmv_mode;      /* SpMV kernel chosen at encode: 0 = warp blocks, 1 = row walk */
 } gse_matrix_info;
 
 /* ---------------------------------------------------------------------------------------

@@ -70,7 +70,8 @@ class MatrixInfo(C.Structure):
                 ("ei_in_column", C.c_int), ("table_len", C.c_int), ("table", C.c_uint16 * 64),
                 ("rows", C.c_int64), ("cols", C.c_int64), ("nnz", C.c_int64),
                 ("n_blocks", C.c_int64), ("n_zero_values", C.c_int64), ("device", C.c_int),
-                ("plane_bytes", C.c_size_t * 5)]
+                ("plane_bytes", C.c_size_t * 5),
+                ("spmv_mode", C.c_int)]
 
 
 class StepSchedule(C.Structure):
@@ -264,6 +265,7 @@ def gse_matrix_get_info(A: Matrix) -> dict:
         "cols": info.cols, "nnz": info.nnz, "n_blocks": info.n_blocks,
         "n_zero_values": info.n_zero_values, "device": info.device,
         "plane_bytes": [info.plane_bytes[i] for i in range(5)],
+        "spmv_mode": info.spmv_mode,
     }
 
 

@@ -360,6 +360,7 @@ gse_status gse_matrix_get_info(gse_matrix A, gse_matrix_info* info) {
   info->n_blocks = M.n_blocks;
   info->n_zero_values = M.n_zero;
   info->device = M.device;
+  info->spmv_mode = M.spmv_mode;
   if (M.kind == GSE_KIND_GSE) {
     info->plane_bytes[0] = (size_t)M.nnz * 4;
     info->plane_bytes[1] = (size_t)M.nnz * 2;

@@ -256,28 +256,55 @@ static int grid_for(int64_t n, int threads, int dev) {
   return (int)(g < 1 ? 1 : g);
 }
 
-// per 32-row group: non-zeros and longest row -> mode statistics
+// per 32-row group (one warp, lane = row): longest row, staged spans of the group and of
+// the 64-row group it starts -> mode statistics.  acc = {heavy groups, sum 32 * max len,
+// max len, max span (32 rows), max span (64 rows)}
 __global__ void k_group_stats(const uint32_t* __restrict__ rp, int64_t rows,
                               unsigned long long* __restrict__ acc) {
+  __shared__ unsigned long long red[5][8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t ng = (rows + RW_ROWS - 1) / RW_ROWS;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  unsigned long long heavy = 0, wsum = 0, mx = 0, span = 0;
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += stride) {
-    const int64_t r0 = g * RW_ROWS;
-    const int64_t r1 = r0 + RW_ROWS < rows ? r0 + RW_ROWS : rows;
-    uint32_t m = 0;
-    for (int64_t r = r0; r < r1; ++r) m = max(m, rp[r + 1] - rp[r]);
-    // staged span of the group: [rp[r0] & ~7, rp[r1]) rounded up to 8-element units
-    const uint32_t sp = ((rp[r1] - (rp[r0] & ~7u)) + 7u) & ~7u;
-    span = max(span, (unsigned long long)sp);
-    heavy += (sp > (uint32_t)RW_TILE) ? 1 : 0;
-    wsum += (unsigned long long)RW_ROWS * m;
-    mx = max(mx, (unsigned long long)m);
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  unsigned long long heavy = 0, wsum = 0, mx = 0, span = 0, span2 = 0;
+  for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; g < ng; g += nw) {
+    const int64_t r0 = g * RW_ROWS, r = r0 + lane;
+    const uint32_t len = r < rows ? rp[r + 1] - rp[r] : 0u;
+    const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, len);
+    if (lane == 0) {
+      const int64_t r1 = r0 + RW_ROWS < rows ? r0 + RW_ROWS : rows;
+      const int64_t r2 = r0 + 2 * RW_ROWS < rows ? r0 + 2 * RW_ROWS : rows;
+      // staged span: [rp[r0] & ~7, rp[r1]) rounded up to 8-element units
+      const uint32_t a0 = rp[r0] & ~7u;
+      const uint32_t sp = ((rp[r1] - a0) + 7u) & ~7u;
+      span = max(span, (unsigned long long)sp);
+      if ((g & 1) == 0) span2 = max(span2, (unsigned long long)(((rp[r2] - a0) + 7u) & ~7u));
+      heavy += (sp > (uint32_t)RW_TILE) ? 1 : 0;
+      wsum += (unsigned long long)RW_ROWS * m;
+      mx = max(mx, (unsigned long long)m);
+    }
   }
-  if (heavy) atomicAdd(&acc[0], heavy);
-  if (wsum) atomicAdd(&acc[1], wsum);
-  if (mx) atomicMax(&acc[2], mx);
-  if (span) atomicMax(&acc[3], span);
+  if (lane == 0) {
+    red[0][warp] = heavy;
+    red[1][warp] = wsum;
+    red[2][warp] = mx;
+    red[3][warp] = span;
+    red[4][warp] = span2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      heavy += red[0][w];
+      wsum += red[1][w];
+      mx = max(mx, red[2][w]);
+      span = max(span, red[3][w]);
+      span2 = max(span2, red[4][w]);
+    }
+    if (heavy) atomicAdd(&acc[0], heavy);
+    if (wsum) atomicAdd(&acc[1], wsum);
+    if (mx) atomicMax(&acc[2], mx);
+    if (span) atomicMax(&acc[3], span);
+    if (span2) atomicMax(&acc[4], span2);
+  }
 }
 
 static void choose_mode(Matrix& M) {
@@ -295,18 +322,20 @@ gse_status build_partition(Matrix& M, cudaStream_t s) {
   M.n_blocks = 0;
   M.n_groups = (M.rows + RW_ROWS - 1) / RW_ROWS;
   if (M.rows > 0) {
-    unsigned long long* acc = dev_alloc_n<unsigned long long>(4, s);
+    unsigned long long* acc = dev_alloc_n<unsigned long long>(5, s);
     if (!acc) return GSE_ERR_OOM;
-    GSE_CUDA_TRY(cudaMemsetAsync(acc, 0, 32, s));
-    k_group_stats<<<grid_for(M.n_groups, 256, M.device), 256, 0, s>>>(M.row_ptr, M.rows, acc);
-    unsigned long long h[4];
-    GSE_CUDA_TRY(cudaMemcpyAsync(h, acc, 32, cudaMemcpyDeviceToHost, s));
+    GSE_CUDA_TRY(cudaMemsetAsync(acc, 0, 40, s));
+    k_group_stats<<<grid_for(M.n_groups * 32, 256, M.device), 256, 0, s>>>(M.row_ptr, M.rows,
+                                                                           acc);
+    unsigned long long h[5];
+    GSE_CUDA_TRY(cudaMemcpyAsync(h, acc, 40, cudaMemcpyDeviceToHost, s));
     GSE_CUDA_TRY(cudaStreamSynchronize(s));
     dev_free(acc, s);
     M.heavy_groups = (int64_t)h[0];
     M.rw_efficiency = h[1] ? (double)M.nnz / (double)h[1] : 0.0;
     M.max_row_len = (int64_t)h[2];
     M.rw_span = (int64_t)h[3];
+    M.rw_span2 = (int64_t)h[4];
   }
   choose_mode(M);
   if (M.rows == 0) {

@@ -76,6 +76,7 @@ struct Matrix {
   int64_t heavy_groups = 0;     // groups with > RW_TILE non-zeros
   int64_t max_row_len = 0;
   int64_t rw_span = 0;          // max staged span of a group (sizes the RW smem stages)
+  int64_t rw_span2 = 0;         // the same for 64-row groups (two rows per lane)
   double rw_efficiency = 0.0;   // sum(len) / sum over groups of 32 * max(len)
   DecodeTable* dtab = nullptr;  // device copy
   DecodeTable htab;             // host copy

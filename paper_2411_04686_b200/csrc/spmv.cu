@@ -25,6 +25,7 @@ static SpmvParams<T> make_params(const Matrix& M, int level, const T* x, T* y,
   p.rows = (uint32_t)M.rows;
   p.n_groups = (uint32_t)M.n_groups;
   p.rw_stage = (uint32_t)((M.rw_span + 15) / 16 * 16 + 16);  // + over-copy (spmv_rw.cu)
+  p.rw_stage2 = (uint32_t)((M.rw_span2 + 15) / 16 * 16 + 16);
   p.ei_shift = 32 - M.ei_bits;
   p.col_mask = (M.kind == GSE_KIND_GSE && M.ei_in_column && M.ei_bits)
                    ? ((1u << (32 - M.ei_bits)) - 1u)

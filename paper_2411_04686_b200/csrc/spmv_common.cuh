@@ -73,6 +73,7 @@ struct SpmvParams {
   uint32_t rows;
   uint32_t n_groups;  // RW 32-row groups
   uint32_t rw_stage;  // RW: elements per staging buffer (>= max group span, multiple of 16)
+  uint32_t rw_stage2;  // the same for 64-row groups
   int ei_shift;       // 32 - ei_bits
   uint32_t col_mask;  // (1 << (32 - ei_bits)) - 1, or ~0u
   const T* __restrict__ x;

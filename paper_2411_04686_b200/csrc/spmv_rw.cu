@@ -18,6 +18,8 @@
 //    are close (Matrix::rw_efficiency >= 0.6); otherwise spmv_sp.cu runs.
 #include "spmv_common.cuh"
 
+#include <cstdlib>
+
 namespace gse {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -186,7 +188,10 @@ __device__ __forceinline__ T walk_row(const SpmvParams<T>& p, const Stage<L>& st
   return sum;
 }
 
-template <int L, bool DOT, bool FAST, class T>
+// RPL = rows per lane: a group is 32 * RPL consecutive rows staged by one set of bulk
+// copies and walked in RPL passes of lane = row (RPL = 2 halves the per-group overhead:
+// row bounds, copy issue, barrier wait)
+template <int L, int RPL, bool DOT, bool FAST, class T>
 __global__ void __launch_bounds__(SPMV_THREADS, 3) k_spmv_rw(const SpmvParams<T> p) {
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t bars[SPMV_WARPS][2];
@@ -209,7 +214,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, 3) k_spmv_rw(const SpmvParams<T>
   stage_tables<L>(p, sd64, sd32, sc64, sc32);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t N = p.rw_stage;
+  const uint32_t N = RPL == 1 ? p.rw_stage : p.rw_stage2;
   const uint32_t SB = N * rw_elem_bytes<L>();
   unsigned char* wbase = dsm + (size_t)warp * 2 * SB;
   if (lane == 0) {
@@ -221,21 +226,27 @@ __global__ void __launch_bounds__(SPMV_THREADS, 3) k_spmv_rw(const SpmvParams<T>
   }
   __syncwarp();
 
+  constexpr uint32_t GR = RW_ROWS * RPL;  // rows per group
   double dacc = 0.0;
-  const uint32_t ng = p.n_groups, rows = p.rows;
+  const uint32_t rows = p.rows, ng = (rows + GR - 1) / GR;
   const uint32_t W = gridDim.x * SPMV_WARPS;
   uint32_t g = blockIdx.x * SPMV_WARPS + warp;
-  // row bounds of a group of 32 rows: a = rp[r0 + lane], c = rp[r0 + 32] (indices clamped
-  // to rows: rows past the end are empty); a row's end is the next lane's start
+  // row bounds of a group: a[k] = rp[r0 + 32 k + lane], c = rp[r0 + GR] (indices clamped to
+  // rows: rows past the end are empty); a row's end is the next row's start
   struct Bounds {
-    uint32_t a, c;
+    uint32_t a[RPL];
+    uint32_t c;
   };
   auto bounds = [&](uint32_t grp) {
-    Bounds B{0, 0};
+    Bounds B;
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) B.a[k] = 0;
+    B.c = 0;
     if (grp < ng) {
-      const uint32_t r0 = grp * RW_ROWS;
-      B.a = p.row_ptr[min(r0 + lane, rows)];
-      B.c = p.row_ptr[min(r0 + RW_ROWS, rows)];
+      const uint32_t r0 = grp * GR;
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) B.a[k] = p.row_ptr[min(r0 + 32 * k + lane, rows)];
+      B.c = p.row_ptr[min(r0 + GR, rows)];
     }
     return B;
   };
@@ -243,7 +254,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, 3) k_spmv_rw(const SpmvParams<T>
   // the previous kernel's drain under programmatic dependent launch
   Bounds cur_b = bounds(g), nxt_b = bounds(g + W);
   if (g < ng && lane == 0)
-    issue_stage<L>(p, Stage<L>(wbase, N), &bars[warp][0], cur_b.a, cur_b.c);
+    issue_stage<L>(p, Stage<L>(wbase, N), &bars[warp][0], cur_b.a[0], cur_b.c);
   pdl_wait();
   if (p.stop && *p.stop) {  // drain the issued copy before the CTA exits
     if (g < ng) mbar_wait(&bars[warp][0], 0);
@@ -255,22 +266,32 @@ __global__ void __launch_bounds__(SPMV_THREADS, 3) k_spmv_rw(const SpmvParams<T>
     const uint32_t cur = it & 1u;
     const Bounds n2_b = bounds(g + 2 * W);  // two groups ahead
     if (g + W < ng) {                       // planes of the next group -> the other stage
-      const uint32_t s = __shfl_sync(0xFFFFFFFFu, nxt_b.a, 0);
+      const uint32_t s = __shfl_sync(0xFFFFFFFFu, nxt_b.a[0], 0);
       if (lane == 0)
         issue_stage<L>(p, Stage<L>(wbase + (cur ^ 1u) * SB, N), &bars[warp][cur ^ 1u], s,
                        nxt_b.c);
     }
-    const uint32_t r0 = g * RW_ROWS;
-    const uint32_t base = __shfl_sync(0xFFFFFFFFu, cur_b.a, 0) & ~7u;
-    uint32_t ea = __shfl_down_sync(0xFFFFFFFFu, cur_b.a, 1);
-    if (lane == 31) ea = cur_b.c;
+    const uint32_t r0 = g * GR;
+    const uint32_t base = __shfl_sync(0xFFFFFFFFu, cur_b.a[0], 0) & ~7u;
+    uint32_t ea[RPL];
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) {
+      ea[k] = __shfl_down_sync(0xFFFFFFFFu, cur_b.a[k], 1);
+      const uint32_t last = (k + 1 < RPL) ? __shfl_sync(0xFFFFFFFFu, cur_b.a[k + 1 < RPL ? k + 1 : k], 0)
+                                          : cur_b.c;
+      if (lane == 31) ea[k] = last;
+    }
     mbar_wait(&bars[warp][cur], (it >> 1) & 1u);
     const Stage<L> st(wbase + cur * SB, N);
-    const T sa = walk_row<L, FAST, T>(p, st, cur_b.a - base, ea - base, ssc64, ssc32, sd64, sd32,
-                                      sc64, sc32);
-    if (r0 + lane < rows) {
-      p.y[r0 + lane] = sa;
-      if (DOT) dacc += (double)p.x[r0 + lane] * (double)sa;
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) {
+      const T sa = walk_row<L, FAST, T>(p, st, cur_b.a[k] - base, ea[k] - base, ssc64, ssc32,
+                                        sd64, sd32, sc64, sc32);
+      const uint32_t row = r0 + 32 * k + lane;
+      if (row < rows) {
+        p.y[row] = sa;
+        if (DOT) dacc += (double)p.x[row] * (double)sa;
+      }
     }
     __syncwarp();
     cur_b = nxt_b;
@@ -279,13 +300,14 @@ __global__ void __launch_bounds__(SPMV_THREADS, 3) k_spmv_rw(const SpmvParams<T>
   if constexpr (DOT) finalize_dot(warp_sum(dacc), p.partials, p.ticket, p.dot_result);
 }
 
-template <int L, bool DOT, bool FAST, class T>
-static void go(const Matrix& M, const SpmvParams<T>& p, cudaStream_t s) {
+template <int L, int RPL, bool DOT, bool FAST, class T>
+static void go_rpl(const Matrix& M, const SpmvParams<T>& p, cudaStream_t s) {
   static int cache[64] = {0};
   static uint32_t cache_smem[64] = {0};
   const int dev = M.device < 64 ? M.device : 0;
-  const size_t smem = (size_t)SPMV_WARPS * 2 * p.rw_stage * rw_elem_bytes<L>();
-  auto kern = k_spmv_rw<L, DOT, FAST, T>;
+  const uint32_t N = RPL == 1 ? p.rw_stage : p.rw_stage2;
+  const size_t smem = (size_t)SPMV_WARPS * 2 * N * rw_elem_bytes<L>();
+  auto kern = k_spmv_rw<L, RPL, DOT, FAST, T>;
   if (cache_smem[dev] != smem) {  // occupancy depends on the stage size of this matrix
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int blocks = 0;
@@ -293,10 +315,35 @@ static void go(const Matrix& M, const SpmvParams<T>& p, cudaStream_t s) {
     cache[dev] = (blocks < 1 ? 1 : blocks) * num_sms(M.device);
     cache_smem[dev] = (uint32_t)smem;
   }
-  const int64_t want = (M.n_groups + SPMV_WARPS - 1) / SPMV_WARPS;
+  const int64_t ng = (M.rows + RW_ROWS * RPL - 1) / (RW_ROWS * RPL);
+  const int64_t want = (ng + SPMV_WARPS - 1) / SPMV_WARPS;
   int g = (int)(want < cache[dev] ? want : cache[dev]);
   if (g < 1) g = 1;
   launch_k(kern, g, SPMV_THREADS, smem, s, p);
+}
+
+// rows per lane (measured): 2 for level 1 (its per-group overhead
+// is the largest share of the walk) and, for the other levels, when every warp gets >= 32
+// groups (fewer: the +-1 group tail imbalance of the static schedule costs more than the
+// overhead saved); 1 when the doubled stages do not fit 3 CTAs per SM
+template <int L>
+static int rw_rpl(const Matrix& M, uint32_t rw_stage2) {
+  const char* e = getenv("GSE_RW_RPL");  // A/B and test override: 1 or 2 (read per launch)
+  const int forced = e ? atoi(e) : 0;
+  if (forced == 1 || forced == 2) return forced;
+  const size_t two = (size_t)SPMV_WARPS * 2 * rw_stage2 * rw_elem_bytes<L>();
+  if (two * 3 > 200 * 1024) return 1;
+  if (L == 1) return 2;
+  const int64_t warps = (int64_t)num_sms(M.device) * 3 * SPMV_WARPS;
+  return (M.rows + 2 * RW_ROWS - 1) / (2 * RW_ROWS) >= 32 * warps ? 2 : 1;
+}
+
+template <int L, bool DOT, bool FAST, class T>
+static void go(const Matrix& M, const SpmvParams<T>& p, cudaStream_t s) {
+  if (rw_rpl<L>(M, p.rw_stage2) == 2)
+    go_rpl<L, 2, DOT, FAST, T>(M, p, s);
+  else
+    go_rpl<L, 1, DOT, FAST, T>(M, p, s);
 }
 
 template <int L, bool DOT, class T>

@@ -165,6 +165,31 @@ def test_spmv_f32acc_parity(g, name):
         assert np.all(np.abs(y32.astype(np.float64) - yo) <= spmv_bound(R, x32.astype(np.float64), L, 1e-5))
 
 
+@pytest.mark.parametrize("rpl", ["1", "2"])
+@pytest.mark.parametrize("name", ["poisson3d_40", "poisson2d_varcoef", "convdiff_20"])
+def test_spmv_row_walk_rows_per_lane(g, name, rpl, monkeypatch):
+    """Both row-walk variants (32-row groups, lane = row; 64-row groups, two rows per lane)
+    at every level and both accumulations, forced with GSE_RW_RPL (read per launch)."""
+    A = MATS[name]()
+    M, R = enc_both(g, A)
+    assert M.info["spmv_mode"] == 1, "row-walk matrix expected"
+    monkeypatch.setenv("GSE_RW_RPL", rpl)
+    x = gi.uniform_vec(A.cols, seed=11)
+    for L in (1, 2, 3):
+        yg = g.gse_spmv(M, x, segments=L)
+        yo = O.spmv_gse(R, x, L)
+        assert np.all(np.abs(yg - yo) <= spmv_bound(R, x, L, 1e-12)), L
+        y32 = g.gse_spmv_f32acc(M, x.astype(np.float32), segments=L)
+        x64 = x.astype(np.float32).astype(np.float64)
+        assert np.all(np.abs(y32.astype(np.float64) - O.spmv_gse(R, x64, L))
+                      <= spmv_bound(R, x64, L, 1e-5)), L
+    F = g.gse_fp64_matrix(A.row_ptr, A.col, A.val, A.rows, A.cols)
+    yf = g.gse_spmv(F, x, segments=3)
+    Fo = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+    Fa = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, np.abs(A.val))
+    assert np.all(np.abs(yf - O.spmv_fp64(Fo, x)) <= 1e-12 * O.spmv_fp64(Fa, np.abs(x)))
+
+
 def test_spmv_head_exact_poisson_bitwise(g):
     """Constant Poisson is exact in the head: levels 1/2/3 and FP64 agree bitwise, and
     short rows are summed in storage order like the oracle."""
