@@ -80,12 +80,12 @@ struct SolverWs {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
-// The scalar head of SolveCtrl (everything before the GMRES arrays).  The single thread
+// The scalar head of SolveCtrl (everything before the GMRES arrays H, cs, sn, g, y).  The single thread
 // that runs the CG event logic works on a shared-memory snapshot loaded by warp 0 at
 // kernel start (overlapped with the vector pass) and writes it back: done directly on
 // global memory the logic is a chain of ~20 dependent L2 round trips (~7 us per iteration).
-constexpr int CTRL_HEAD_WORDS = (int)(offsetof(SolveCtrl, restart) / 8);
-static_assert(offsetof(SolveCtrl, restart) % 8 == 0, "SolveCtrl head must be 8-byte words");
+constexpr int CTRL_HEAD_WORDS = (int)(offsetof(SolveCtrl, H) / 8);
+static_assert(offsetof(SolveCtrl, H) % 8 == 0, "SolveCtrl head must be 8-byte words");
 
 __device__ __forceinline__ void ctrl_load_head(const SolveCtrl* c, unsigned long long* sm) {
   if (threadIdx.x < 32) {
@@ -569,6 +569,198 @@ __global__ void __launch_bounds__(256, 4) k_gm_mgs(SolveCtrl* __restrict__ c, do
   if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0) c->H[i * m + j] = tot;
 }
 
+// End of inner iteration j (one thread): h_{j+1,j} = hn, previous Givens rotations applied
+// to column j, new rotation (R18), residual estimate |g_{j+1}| / ||b||, monitor and events.
+// col[i * cstride] = H[i][j] (i <= j + 1); cs, sn, g and the scalars in *c may be the
+// control block itself or a shared-memory snapshot of it (written back by the caller).
+__device__ void gm_finish(SolveCtrl* c, double* ring, int j, double hn, double* col,
+                          int cstride, double* cs, double* sn, double* g) {
+  c->hn = hn;
+  col[(j + 1) * cstride] = hn;
+  for (int i = 0; i < j; ++i) {  // apply previous rotations to column j
+    const double h1 = col[i * cstride], h2 = col[(i + 1) * cstride];
+    const double a1 = __dmul_rn(cs[i], h1), a2 = __dmul_rn(sn[i], h2);
+    const double b1 = __dmul_rn(sn[i], h1), b2 = __dmul_rn(cs[i], h2);
+    col[i * cstride] = __dadd_rn(a1, a2);
+    col[(i + 1) * cstride] = __dsub_rn(b2, b1);
+  }
+  const double h1 = col[j * cstride], h2 = col[(j + 1) * cstride];
+  double cc, ss;
+  if (h2 == 0.0) {
+    cc = 1.0;
+    ss = 0.0;
+  } else if (fabs(h2) > fabs(h1)) {
+    const double tau = h1 / h2;
+    ss = 1.0 / sqrt(__dadd_rn(1.0, __dmul_rn(tau, tau)));
+    cc = __dmul_rn(ss, tau);
+  } else {
+    const double tau = h2 / h1;
+    cc = 1.0 / sqrt(__dadd_rn(1.0, __dmul_rn(tau, tau)));
+    ss = __dmul_rn(cc, tau);
+  }
+  cs[j] = cc;
+  sn[j] = ss;
+  col[j * cstride] = __dadd_rn(__dmul_rn(cc, h1), __dmul_rn(ss, h2));
+  col[(j + 1) * cstride] = 0.0;
+  g[j + 1] = -__dmul_rn(ss, g[j]);
+  g[j] = __dmul_rn(cc, g[j]);
+  const double resid = fabs(g[j + 1]) / c->bnorm;
+  c->resid = resid;
+  const long long jg = c->iter + 1;
+  c->iter = jg;
+  c->k = j + 1;
+  if (!isfinite(resid)) {
+    c->event = EV_ABORT;
+    c->stop = 1;
+  } else {
+    ring_push(c, ring, resid);
+    if (resid <= c->tol || hn == 0.0) {
+      c->event = EV_CONVERGED;
+      c->stop = 1;
+    } else if (monitor_check(c, ring, jg, resid)) {
+      c->event = EV_ESCALATE;
+      c->stop = 1;
+    } else if (jg >= c->max_iters) {
+      c->stop = 1;  // the next restart reports MAXITER after the explicit check
+    }
+  }
+}
+
+// Whole Arnoldi step j after the SpMV w = A v_j, in ONE cooperative launch (the per-step
+// kernels below are the fallback for vectors too long for the shared-memory slice):
+//   for i = 0..j: w -= h_{i-1,j} v_{i-1} (i > 0); h_{i,j} = w . v_i     (MGS, oracle order)
+//   w -= h_{j,j} v_j ; hn = ||w|| ; v_{j+1} = w / hn ; gm_finish
+// Each thread owns elements e0 + k T (T = grid threads, k < E) of w, kept in shared memory
+// across the j + 2 grid-wide reductions, so a step reads only v_{i-1} and v_i from memory
+// (the per-step kernels also read and write w).  Each reduction: CTA partial -> grid
+// barrier -> every CTA sums all partials in the same fixed order (identical totals
+// everywhere; partials double-buffered across consecutive reductions).
+constexpr int GM_THREADS = 1024;  // one CTA per SM: 148 barrier arrivals and partials
+
+__device__ __forceinline__ double gm_grid_total(double part, double* partials, int buf,
+                                                double* red, double* s_tot) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  part = warp_sum_d(part);
+  if (lane == 0) red[warp] = part;
+  __syncthreads();
+  const unsigned G = gridDim.x;
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < GM_THREADS / 32; ++w) s += red[w];
+    partials[(size_t)buf * G + blockIdx.x] = s;
+  }
+  cooperative_groups::this_grid().sync();
+  if (warp == 0) {
+    double s = 0.0;
+    for (unsigned q = lane; q < G; q += 32) s += __ldcg(partials + (size_t)buf * G + q);
+    s = warp_sum_d(s);
+    if (lane == 0) *s_tot = s;
+  }
+  __syncthreads();
+  return *s_tot;
+}
+
+__global__ void __launch_bounds__(GM_THREADS, 1) k_gm_arnoldi(SolveCtrl* __restrict__ c,
+                                                             double* ring,
+                                                             const double* __restrict__ w_in,
+                                                             double* __restrict__ V, int64_t n,
+                                                             int j, int E, double* partials) {
+  extern __shared__ double wsm[];  // E * GM_THREADS: this thread's slice of w at [k * GM_THREADS + t]
+  __shared__ unsigned long long sctrl[CTRL_HEAD_WORDS];
+  __shared__ double s_col[MAX_RESTART + 1], s_cs[MAX_RESTART], s_sn[MAX_RESTART];
+  __shared__ double s_g[MAX_RESTART + 1];
+  __shared__ double red[GM_THREADS / 32];
+  __shared__ double s_tot;
+  if (c->stop) return;  // uniform: written only before this launch
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // snapshots for the end-of-step logic (consumed by CTA 0 after the barriers)
+  if (blockIdx.x == 0) {
+    if (warp == 0) ctrl_load_head(c, sctrl);
+    if (warp == 1)
+      for (int i = lane; i < j; i += 32) {
+        s_cs[i] = c->cs[i];
+        s_sn[i] = c->sn[i];
+      }
+    if (warp == 2)
+      for (int i = lane; i <= j + 1; i += 32) s_g[i] = c->g[i];
+  }
+  const int64_t T = (int64_t)gridDim.x * GM_THREADS;
+  const int64_t e0 = (int64_t)blockIdx.x * GM_THREADS + tid;
+  for (int k = 0; k < E; ++k) {
+    const int64_t e = e0 + k * T;
+    wsm[k * GM_THREADS + tid] = e < n ? w_in[e] : 0.0;
+  }
+  double h_prev = 0.0;
+  for (int i = 0; i <= j; ++i) {
+    const double* vi = V + (size_t)i * n;
+    const double* vp = V + (size_t)(i > 0 ? i - 1 : 0) * n;
+    double acc = 0.0;
+    // batches of 4 slice elements: all 8 loads issued before the dependent arithmetic
+    for (int k0 = 0; k0 < E; k0 += 4) {
+      double a[4], bp[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t e = e0 + (int64_t)(k0 + q) * T;
+        const bool in = k0 + q < E && e < n;
+        a[q] = in ? __ldg(vi + e) : 0.0;
+        bp[q] = (in && i > 0) ? __ldg(vp + e) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t e = e0 + (int64_t)(k0 + q) * T;
+        if (k0 + q < E && e < n) {
+          double wv = wsm[(k0 + q) * GM_THREADS + tid];
+          if (i > 0) {
+            wv = __dsub_rn(wv, __dmul_rn(h_prev, bp[q]));
+            wsm[(k0 + q) * GM_THREADS + tid] = wv;
+          }
+          acc = __dadd_rn(acc, __dmul_rn(wv, a[q]));
+        }
+      }
+    }
+    h_prev = gm_grid_total(acc, partials, i & 1, red, &s_tot);
+    if (blockIdx.x == 0 && tid == 0) s_col[i] = h_prev;
+  }
+  {  // w -= h_{j,j} v_j ; ||w||
+    const double* vj = V + (size_t)j * n;
+    double acc = 0.0;
+    for (int k0 = 0; k0 < E; k0 += 4) {
+      double a[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t e = e0 + (int64_t)(k0 + q) * T;
+        a[q] = (k0 + q < E && e < n) ? __ldg(vj + e) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t e = e0 + (int64_t)(k0 + q) * T;
+        if (k0 + q < E && e < n) {
+          const double wv = __dsub_rn(wsm[(k0 + q) * GM_THREADS + tid], __dmul_rn(h_prev, a[q]));
+          wsm[(k0 + q) * GM_THREADS + tid] = wv;
+          acc = __dadd_rn(acc, __dmul_rn(wv, wv));
+        }
+      }
+    }
+    const double hn = sqrt(gm_grid_total(acc, partials, (j + 1) & 1, red, &s_tot));
+    double* vn = V + (size_t)(j + 1) * n;  // V holds restart + 1 vectors
+    for (int k = 0; k < E; ++k) {
+      const int64_t e = e0 + k * T;
+      if (e < n) vn[e] = wsm[k * GM_THREADS + tid] / hn;
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+      SolveCtrl* sc = reinterpret_cast<SolveCtrl*>(sctrl);
+      gm_finish(sc, ring, j, hn, s_col, 1, s_cs, s_sn, s_g);
+      const int m = sc->restart;
+      for (int i = 0; i <= j + 1; ++i) c->H[i * m + j] = s_col[i];
+      c->cs[j] = s_cs[j];
+      c->sn[j] = s_sn[j];
+      c->g[j] = s_g[j];
+      c->g[j + 1] = s_g[j + 1];
+      ctrl_store_head(c, sctrl);
+    }
+  }
+}
+
 // last MGS step: w -= H[j][j] v_j ; hn = ||w|| ; Givens (R18) ; estimate ; monitor
 __global__ void __launch_bounds__(256, 4) k_gm_last(SolveCtrl* __restrict__ c, double* ring,
                                                  double* __restrict__ w,
@@ -615,59 +807,8 @@ __global__ void __launch_bounds__(256, 4) k_gm_last(SolveCtrl* __restrict__ c, d
     }
   }
   double tot;
-  if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0) {
-    const double hn = sqrt(tot);
-    c->hn = hn;
-    double* H = c->H;
-    H[(j + 1) * m + j] = hn;
-    for (int i = 0; i < j; ++i) {  // apply previous rotations to column j
-      const double h1 = H[i * m + j], h2 = H[(i + 1) * m + j];
-      const double a1 = __dmul_rn(c->cs[i], h1), a2 = __dmul_rn(c->sn[i], h2);
-      const double b1 = __dmul_rn(c->sn[i], h1), b2 = __dmul_rn(c->cs[i], h2);
-      H[i * m + j] = __dadd_rn(a1, a2);
-      H[(i + 1) * m + j] = __dsub_rn(b2, b1);
-    }
-    const double h1 = H[j * m + j], h2 = H[(j + 1) * m + j];
-    double cc, ss;
-    if (h2 == 0.0) {
-      cc = 1.0;
-      ss = 0.0;
-    } else if (fabs(h2) > fabs(h1)) {
-      const double tau = h1 / h2;
-      ss = 1.0 / sqrt(__dadd_rn(1.0, __dmul_rn(tau, tau)));
-      cc = __dmul_rn(ss, tau);
-    } else {
-      const double tau = h2 / h1;
-      cc = 1.0 / sqrt(__dadd_rn(1.0, __dmul_rn(tau, tau)));
-      ss = __dmul_rn(cc, tau);
-    }
-    c->cs[j] = cc;
-    c->sn[j] = ss;
-    H[j * m + j] = __dadd_rn(__dmul_rn(cc, h1), __dmul_rn(ss, h2));
-    H[(j + 1) * m + j] = 0.0;
-    c->g[j + 1] = -__dmul_rn(ss, c->g[j]);
-    c->g[j] = __dmul_rn(cc, c->g[j]);
-    const double resid = fabs(c->g[j + 1]) / c->bnorm;
-    c->resid = resid;
-    const long long jg = c->iter + 1;
-    c->iter = jg;
-    c->k = j + 1;
-    if (!isfinite(resid)) {
-      c->event = EV_ABORT;
-      c->stop = 1;
-    } else {
-      ring_push(c, ring, resid);
-      if (resid <= c->tol || hn == 0.0) {
-        c->event = EV_CONVERGED;
-        c->stop = 1;
-      } else if (monitor_check(c, ring, jg, resid)) {
-        c->event = EV_ESCALATE;
-        c->stop = 1;
-      } else if (jg >= c->max_iters) {
-        c->stop = 1;  // the next restart reports MAXITER after the explicit check
-      }
-    }
-  }
+  if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0)
+    gm_finish(c, ring, j, sqrt(tot), c->H + j, m, c->cs, c->sn, c->g);
 }
 
 // back substitution H[0:k,0:k] y = g[0:k] (one thread; k <= restart)
@@ -754,7 +895,7 @@ static gse_status ensure_ws(Matrix& M, int64_t ring_t, int gm_restart, cudaStrea
     ws->q = dev_alloc_n<double>(nn, s);
     ws->b = dev_alloc_n<double>(nn, s);
     ws->tmp = dev_alloc_n<double>(nn, s);
-    const int64_t np = (M.n_blocks > ws->vgrid ? M.n_blocks : ws->vgrid) + 1;
+    const int64_t np = (M.n_blocks > 2 * ws->vgrid ? M.n_blocks : 2 * ws->vgrid) + 1;
     ws->partials = dev_alloc_n<double>((size_t)np, s);
     ws->ticket = dev_alloc_n<unsigned>(4, s);
     ws->ctrl = dev_alloc_n<SolveCtrl>(1, s);
@@ -1165,6 +1306,37 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
 }
 
 // ---------------------------------------------------------------- GMRES
+// Launch shape of k_gm_arnoldi: one CTA of GM_THREADS per SM, E elements of w per thread
+// in shared memory.  False (per-step kernels) when the slice does not fit or GSE_GM_COOP=0.
+static bool gm_coop_config(const Matrix& M, int64_t n, int* grid, int* E, size_t* smem) {
+  const char* env = getenv("GSE_GM_COOP");
+  if ((env && env[0] == '0') || n <= 0) return false;
+  const int sms = num_sms(M.device);
+  for (int per = 1; per >= 1; --per) {
+    int64_t G = (int64_t)sms * per;
+    const int64_t need = (n + GM_THREADS - 1) / GM_THREADS;
+    if (G > need) G = need;
+    const int64_t e = (n + G * GM_THREADS - 1) / (G * GM_THREADS);
+    const size_t sm = (size_t)e * GM_THREADS * sizeof(double);
+    if (sm > 200 * 1024) continue;
+    if (cudaFuncSetAttribute(k_gm_arnoldi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+        cudaSuccess)
+      continue;
+    int blocks = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_gm_arnoldi, GM_THREADS, sm) !=
+        cudaSuccess)
+      continue;
+    if ((int64_t)blocks * sms >= G) {
+      *grid = (int)G;
+      *E = (int)e;
+      *smem = sm;
+      return true;
+    }
+  }
+  cudaGetLastError();
+  return false;
+}
+
 static gse_status build_gm_graph(Matrix& M, int level, int restart) {
   SolverWs* ws = M.ws;
   if (ws->gm_restart != restart) {
@@ -1185,8 +1357,30 @@ static gse_status build_gm_graph(Matrix& M, int level, int restart) {
   gse_status rc = launch_spmv(M, level, ws->x, w, nullptr, cs);
   launch_pdl(k_gm_restart, ws->vgrid, 256, 0, cs, c, ws->b, w, n, ws->partials, ws->ticket);
   launch_pdl(k_gm_scale, ws->vgrid, 256, 0, cs, c, w, ws->V, n, 0);
+  int cg_grid = 0, cg_e = 0;
+  size_t cg_smem = 0;
+  const bool coop = gm_coop_config(M, n, &cg_grid, &cg_e, &cg_smem);
   for (int j = 0; j < restart && rc == GSE_OK; ++j) {
     rc = launch_spmv_guarded(M, level, ws->V + (size_t)j * n, w, &c->stop, cs);
+    if (coop) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(cg_grid);
+      cfg.blockDim = dim3(GM_THREADS);
+      cfg.dynamicSmemBytes = cg_smem;
+      cfg.stream = cs;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      const cudaError_t le = cudaLaunchKernelEx(&cfg, k_gm_arnoldi, c, ws->ring, (const double*)w,
+                                                ws->V, n, j, cg_e, ws->partials);
+      if (le != cudaSuccess) {
+        cudaStreamEndCapture(cs, nullptr);
+        return cuda_status(le, "cooperative k_gm_arnoldi");
+      }
+      continue;
+    }
     for (int i = 0; i <= j; ++i)
       launch_pdl(k_gm_mgs, ws->vgrid, 256, 0, cs, c, w, ws->V, n, i, j, ws->partials, ws->ticket);
     launch_pdl(k_gm_last, ws->vgrid, 256, 0, cs, c, ws->ring, w, ws->V, n, j, ws->partials, ws->ticket);
