@@ -166,7 +166,8 @@ def _config(args, n, nnz, world):
             "n": int(n), "nnz": int(nnz), "k_max": 8, "tol": 1e-10,
             "schedule": "paper default CG (l=3000,t=250,m=500) + verify_at_full",
             "step": "gse_encode + gse_solve_cg (inputs resident in HBM)",
-            "l2": "flushed (256 MiB write) before every timed step; per-step CUDA events",
+            "l2": "flushed before every timed step (256 MiB write, then a read pass over it so no "
+                  "dirty lines are written back inside the timed region); per-step CUDA events",
             "parallelism": (f"row-partitioned x{world} (NCCL halo + allreduce)" if world > 1
                             else "single GPU")}
 
@@ -283,7 +284,7 @@ def run_gse(args, world, rank, local, pg):
         torch.cuda.synchronize()
         barrier(pg)
         for i in range(args.steps):
-            flush.fill_(float(i))
+            l2_flush(flush, i)
             ev[i][0].record(stream)
             reps.append(step())
             ev[i][1].record(stream)
@@ -348,8 +349,10 @@ def estimate_launches(rep, world):
 
 
 def _profiled_traffic():
-    p = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
-    if os.path.exists(p):
+    import glob
+    found = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_summary_r*.json")))
+    p = found[-1] if found else ""
+    if p and os.path.exists(p):
         try:
             return json.load(open(p)).get("k_spmv_L1", {}).get("dram_bytes_per_launch")
         except Exception:
@@ -357,12 +360,19 @@ def _profiled_traffic():
     return None
 
 
+def l2_flush(buf, i):
+    """Evict L2: write a 256 MiB buffer (2x the 126 MB L2), then read it back once, so the
+    write-backs of the dirty lines happen here and not inside the next timed region."""
+    buf.fill_(float(i))
+    buf.sum()
+
+
 def time_cuda(fn, reps, stream, flush):
     import torch
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(reps)]
     for i in range(reps):
-        flush.fill_(float(i))
+        l2_flush(flush, i)
         evs[i][0].record(stream)
         fn()
         evs[i][1].record(stream)

@@ -15,7 +15,7 @@ def timeit(fn, reps=30):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
     fn()
     for i in range(reps):
-        flush.fill_(i)
+        flush.fill_(i); flush.sum()  # write + read back: no dirty write-backs in the timing
         evs[i][0].record(); fn(); evs[i][1].record()
     torch.cuda.synchronize()
     return statistics.median(s.elapsed_time(e) for s, e in evs) * 1e-3
