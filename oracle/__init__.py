@@ -63,6 +63,7 @@ class OrcMatrix(C.Structure):
         ("ei_bits", C.c_int), ("ei_in_column", C.c_int),
         ("head", _p(C.c_uint16)), ("tail1", _p(C.c_uint16)), ("tail2", _p(C.c_uint32)),
         ("table", _p(C.c_uint16)), ("table_len", C.c_int),
+        ("half_kind", C.c_int), ("half", _p(C.c_uint16)),
     ]
 
 
@@ -116,6 +117,15 @@ def _declare(L):
     L.orc_gmres.argtypes = [_p(OrcMatrix), _p(dbl), _p(dbl), dbl, i32, i64, _p(OrcSchedule),
                             _p(OrcReport)]
     L.orc_set_threads.argtypes = [i32]
+    L.orc_round_half.argtypes = [dbl, i32]
+    L.orc_round_half.restype = C.c_uint16
+    L.orc_half_value.argtypes = [C.c_uint16, i32]
+    L.orc_half_value.restype = dbl
+    L.orc_round_half_array.argtypes = [i64, _p(dbl), _p(C.c_uint16), i32]
+    L.orc_round_half_array.restype = None
+    L.orc_half_value_array.argtypes = [i64, _p(C.c_uint16), _p(dbl), i32]
+    L.orc_half_value_array.restype = None
+    L.orc_spmv_half.argtypes = [_p(OrcMatrix), _p(dbl), _p(dbl)]
 
 
 def _ptr(a: np.ndarray, ct):
@@ -255,6 +265,69 @@ def _csr_arrays(row_ptr, col, val):
     return (np.ascontiguousarray(row_ptr, dtype=np.int64),
             np.ascontiguousarray(col, dtype=np.int32),
             np.ascontiguousarray(val, dtype=np.float64))
+
+
+FP16, BF16 = 1, 2  # orc_round_half kinds (P:406 baselines)
+
+
+def _half_kind(kind) -> int:
+    return {"fp16": FP16, "bf16": BF16, FP16: FP16, BF16: BF16}[kind]
+
+
+def round_half(values, kind) -> np.ndarray:
+    """FP64 -> FP16 / BF16 bit patterns, round-to-nearest-even (R26), overflow -> +-Inf."""
+    v = np.ascontiguousarray(values, dtype=np.float64).ravel()
+    out = np.zeros(max(v.size, 1), np.uint16)
+    lib().orc_round_half_array(v.size, _ptr(v, C.c_double), _ptr(out, C.c_uint16),
+                               _half_kind(kind))
+    return out[:v.size]
+
+
+def half_values(bits, kind) -> np.ndarray:
+    """FP16 / BF16 bit patterns -> their exact FP64 values."""
+    h = np.ascontiguousarray(bits, dtype=np.uint16).ravel()
+    out = np.zeros(max(h.size, 1), np.float64)
+    lib().orc_half_value_array(h.size, _ptr(h, C.c_uint16), _ptr(out, C.c_double),
+                               _half_kind(kind))
+    return out[:h.size]
+
+
+@dataclass
+class HalfCsr:
+    """The FP16 / BF16 storage baseline: CSR with 16-bit stored values."""
+    rows: int
+    cols: int
+    row_ptr: np.ndarray
+    col: np.ndarray
+    half: np.ndarray  # uint16 bit patterns
+    kind: int
+
+    def orc(self) -> OrcMatrix:
+        m = OrcMatrix()
+        m.rows, m.cols = self.rows, self.cols
+        m.row_ptr = _ptr(self.row_ptr, C.c_int64)
+        m.col = _ptr(self.col, C.c_int32)
+        m.half_kind = self.kind
+        m.half = _ptr(self.half, C.c_uint16)
+        return m
+
+
+def half_csr(rows, cols, row_ptr, col, val, kind) -> HalfCsr:
+    rp, c, v = _csr_arrays(row_ptr, col, val)
+    h = round_half(v, kind)
+    if h.size == 0:
+        h = np.zeros(1, np.uint16)
+    return HalfCsr(rows, cols, rp, c, np.ascontiguousarray(h), _half_kind(kind))
+
+
+def spmv_half(A: HalfCsr, x) -> np.ndarray:
+    xx = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.zeros(A.rows, np.float64)
+    m = A.orc()
+    st = lib().orc_spmv_half(C.byref(m), _ptr(xx, C.c_double), _ptr(y, C.c_double))
+    if st != OK:
+        raise OracleError(st, "spmv_half")
+    return y
 
 
 def fp64_csr(rows, cols, row_ptr, col, val) -> Fp64Csr:

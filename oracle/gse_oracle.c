@@ -324,7 +324,95 @@ int orc_spmv_gse(const orc_matrix* A, int level, const double* x, double* y) {
   return bad ? ORC_ERR_INVALID_EXP_INDEX : ORC_OK;
 }
 
+/* ------------------------------------------------------------------------------------
+ * FP16 / BF16 storage baselines.  P:406 [4.3]: "all non-zero elements are stored and
+ * loaded in FP16 or BF16 format, then converted to FP64 and multiplied by the
+ * double-precision vector. All intermediate results are accumulated in double-precision".
+ * The FP64 -> 16-bit conversion is round-to-nearest-even, directly from the double (R26;
+ * the paper does not state it).  Formats (IEEE 754 binary16 / bfloat16):
+ *   FP16: 1 sign, 5 exponent bits (bias 15), 10 fraction bits; min normal 2^-14,
+ *         subnormal spacing 2^-24, max finite 65504;
+ *   BF16: 1 sign, 8 exponent bits (bias 127), 7 fraction bits; min normal 2^-126,
+ *         subnormal spacing 2^-133, max finite (2 - 2^-7) 2^127.
+ * Rounding, written out: with a = |v| = 1.f * 2^E, the representable numbers near a are
+ * the integer multiples of the quantum 2^q, q = E - fraction_bits (or the subnormal
+ * spacing below the normal range); n = a / 2^q is exact (power-of-two scaling) and
+ * nearbyint() rounds it to the nearest integer, ties to even (the default rounding
+ * mode).  A result above the largest finite value is an overflow (+-Inf).
+ * ------------------------------------------------------------------------------------ */
+uint16_t orc_round_half(double v, int kind) {
+  const int fb = (kind == ORC_FP16) ? 10 : 7;          /* fraction bits */
+  const int bias = (kind == ORC_FP16) ? 15 : 127;
+  const int emin = 1 - bias;                           /* exponent of the min normal */
+  const uint16_t inf_bits = (kind == ORC_FP16) ? 0x7C00 : 0x7F80;
+  const uint16_t nan_bits = (kind == ORC_FP16) ? 0x7E00 : 0x7FC0;
+  const double max_finite = ldexp(2.0 - ldexp(1.0, -fb), bias);
+  const uint16_t sign = (bits_of(v) >> 63) ? 0x8000 : 0;
+  if (isnan(v)) return (uint16_t)(sign | nan_bits);
+  const double a = fabs(v);
+  if (isinf(a)) return (uint16_t)(sign | inf_bits);
+  if (a == 0.0) return sign;
+  int e2;
+  frexp(a, &e2);       /* a = f 2^e2, f in [0.5, 1) */
+  const int E = e2 - 1; /* a = 1.f 2^E */
+  const int q = (E < emin) ? emin - fb : E - fb;       /* quantum exponent */
+  const double n = nearbyint(ldexp(a, -q));            /* RNE to an integer multiple */
+  const double r = ldexp(n, q);
+  if (r > max_finite) return (uint16_t)(sign | inf_bits);
+  if (r < ldexp(1.0, emin)) return (uint16_t)(sign | (uint16_t)n); /* subnormal (or 0) */
+  int er;
+  frexp(r, &er);
+  const int Er = er - 1;
+  const double frac = ldexp(r, -Er) - 1.0;             /* in [0, 1), exact */
+  const uint16_t m = (uint16_t)ldexp(frac, fb);
+  return (uint16_t)(sign | (uint16_t)((Er + bias) << fb) | m);
+}
+
+double orc_half_value(uint16_t h, int kind) {
+  const int fb = (kind == ORC_FP16) ? 10 : 7;
+  const int eb = (kind == ORC_FP16) ? 5 : 8;
+  const int bias = (kind == ORC_FP16) ? 15 : 127;
+  const int emax_field = (1 << eb) - 1;
+  const int s = (h >> 15) & 1;
+  const int e = (h >> fb) & emax_field;
+  const int m = h & ((1 << fb) - 1);
+  double a;
+  if (e == 0)
+    a = ldexp((double)m, 1 - bias - fb);               /* subnormal: m 2^(emin - fb) */
+  else if (e == emax_field)
+    a = m ? NAN : INFINITY;
+  else
+    a = ldexp((double)((1 << fb) + m), e - bias - fb); /* (1.m) 2^(e - bias) */
+  return s ? -a : a;
+}
+
+void orc_round_half_array(int64_t n, const double* v, uint16_t* out, int kind) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) out[i] = orc_round_half(v[i], kind);
+}
+
+void orc_half_value_array(int64_t n, const uint16_t* h, double* out, int kind) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) out[i] = orc_half_value(h[i], kind);
+}
+
+int orc_spmv_half(const orc_matrix* A, const double* x, double* y) {
+  if (A->half_kind != ORC_FP16 && A->half_kind != ORC_BF16) return ORC_ERR_INVALID_ARG;
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < A->rows; ++i) {
+    double sum = 0.0;
+    for (int64_t j = A->row_ptr[i]; j < A->row_ptr[i + 1]; ++j) {
+      double v = orc_half_value(A->half[j], A->half_kind);
+      double prod = v * x[A->col[j]];
+      sum = sum + prod;
+    }
+    y[i] = sum;
+  }
+  return ORC_OK;
+}
+
 int orc_apply(const orc_matrix* A, int level, const double* x, double* y) {
+  if (A->half_kind) return orc_spmv_half(A, x, y);
   if (A->val) return orc_spmv_fp64(A->rows, A->row_ptr, A->col, A->val, x, y);
   return orc_spmv_gse(A, level, x, y);
 }

@@ -53,6 +53,8 @@ typedef struct {
   const uint32_t* tail2;
   const uint16_t* table;
   int table_len;
+  int half_kind;        /* 0: not a 16-bit baseline; ORC_FP16 / ORC_BF16: values in half[] */
+  const uint16_t* half; /* with col[]: the FP16 / BF16 storage baseline       */
 } orc_matrix;
 
 /* ---- SpMV (Alg. 2) ---- */
@@ -60,6 +62,17 @@ int orc_spmv_fp64(int64_t rows, const int64_t* row_ptr, const int32_t* col, cons
                   const double* x, double* y);
 int orc_spmv_gse(const orc_matrix* A, int level, const double* x, double* y);
 int orc_apply(const orc_matrix* A, int level, const double* x, double* y);
+
+/* ---- FP16 / BF16 storage baselines (P:406 [4.3]; R26) ----
+ * values rounded FP64 -> 16 bit with round-to-nearest-even (overflow -> +-Inf), stored,
+ * converted back to FP64 exactly and multiplied by the FP64 vector, FP64 accumulation. */
+#define ORC_FP16 1
+#define ORC_BF16 2
+uint16_t orc_round_half(double v, int kind);
+double orc_half_value(uint16_t h, int kind);
+int orc_spmv_half(const orc_matrix* A, const double* x, double* y);
+void orc_round_half_array(int64_t n, const double* v, uint16_t* out, int kind);
+void orc_half_value_array(int64_t n, const uint16_t* h, double* out, int kind);
 
 /* ---- residual monitor (Eqs. 3-6) ---- */
 double orc_rsd(const double* w, int64_t t);
