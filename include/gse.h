@@ -80,7 +80,12 @@ typedef struct {
   uint64_t seed;             /* reserved for sampling                                      */
 } gse_encode_opts;
 
-typedef enum { GSE_KIND_GSE = 0, GSE_KIND_FP64 = 1 } gse_matrix_kind;
+typedef enum {
+  GSE_KIND_GSE = 0,  /* GSE-SEM planes (gse_encode)                                      */
+  GSE_KIND_FP64 = 1, /* plain FP64 CSR (gse_fp64_matrix)                                 */
+  GSE_KIND_FP16 = 2, /* FP16 storage baseline (gse_half_matrix)                   */
+  GSE_KIND_BF16 = 3  /* BF16 storage baseline (gse_half_matrix)                   */
+} gse_matrix_kind;
 
 typedef struct {
   int kind;          /* gse_matrix_kind                                                     */
@@ -90,7 +95,8 @@ typedef struct {
   int64_t n_blocks;   /* SpMV row blocks                           */
   int64_t n_zero_values; /* zero / subnormal inputs encoded as signed zero (R2)              */
   int device;
-  size_t plane_bytes[5]; /* col_ei, head, tail1, tail2, side_ei (kind GSE); col, val (FP64) */
+  size_t plane_bytes[5]; /* col_ei, head, tail1, tail2, side_ei (kind GSE); col, val (FP64);
+                          col, 16-bit codes (FP16 / BF16)                                 */
   int spmv_mode;      /* SpMV kernel chosen at encode: 0 = warp blocks, 1 = row walk */
 } gse_matrix_info;
 
@@ -116,11 +122,28 @@ gse_status gse_encode(const gse_csr_f64* A, const gse_encode_opts* opts, gse_mat
  * solvers with a disabled schedule (fixed FP64). */
 gse_status gse_fp64_matrix(const gse_csr_f64* A, int device, gse_matrix* out, void* stream);
 
+/* The FP16 / BF16 storage baselines of the paper's evaluation (P:406 [4.3]: "FP16-SpMV" /
+ * "BF16-SpMV" -- values stored in 16 bits, products and sums in FP64; Tables IV-V,
+ * P:449-505, for the solvers).  kind = GSE_KIND_FP16 (IEEE binary16) or GSE_KIND_BF16
+ * (bfloat16).  Each FP64 value is rounded to nearest, ties to even, directly from the double
+ * (R26: the paper does not state the conversion); beyond the largest finite value -> +-Inf
+ * (FP16 overflows above 65504: the "/" entries of Tables IV-V), below the smallest
+ * subnormal -> signed zero.  The 16-bit codes are stored in the `head` plane (readable with
+ * gse_matrix_copy_planes; bit-identical to the oracle), columns in `col_ei` (no EI).  The
+ * matrix is read at full precision only (gse_spmv with segments = 3: each code is converted
+ * exactly to FP64, multiplied and summed in FP64) and the solvers run it at that one
+ * precision (a schedule is accepted but never steps).  Errors as gse_fp64_matrix;
+ * NaN inputs are kept as NaN codes (no error: the baseline reproduces the paper's overflow
+ * behaviour instead of rejecting it). */
+gse_status gse_half_matrix(const gse_csr_f64* A, int kind, int device, gse_matrix* out,
+                           void* stream);
+
 gse_status gse_matrix_get_info(gse_matrix A, gse_matrix_info* info);
 
 /* Copy the encoded planes out (any pointer may be NULL to skip): col_ei[nnz] uint32,
  * side_ei[nnz] uint8 (only when !ei_in_column), head[nnz] / tail1[nnz] uint16,
- * tail2[nnz] uint32, table[table_len] uint16.  Host or device destinations. */
+ * tail2[nnz] uint32, table[table_len] uint16.  Host or device destinations.  FP16 / BF16
+ * matrices: col_ei (plain columns) and head (the 16-bit codes) only; FP64: col_ei only. */
 gse_status gse_matrix_copy_planes(gse_matrix A, uint32_t* col_ei, uint8_t* side_ei,
                                   uint16_t* head, uint16_t* tail1, uint32_t* tail2,
                                   uint16_t* table, void* stream);

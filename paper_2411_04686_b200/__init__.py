@@ -6,7 +6,7 @@ arrays -> raw pointers, the current CUDA stream) and raises on error statuses; e
 the method runs in the library's kernels.  There is no CPU fallback: if the library cannot
 be loaded, importing this package fails.
 
-Function names follow the C-ABI: gse_encode, gse_fp64_matrix, gse_spmv, gse_spmv_f32acc,
+Function names follow the C-ABI: gse_encode, gse_fp64_matrix, gse_half_matrix, gse_spmv, gse_spmv_f32acc,
 gse_decode, gse_matrix_copy_planes, gse_matrix_get_info, gse_solve_cg, gse_solve_gmres,
 gse_default_schedule, gse_matrix_free.
 """
@@ -28,10 +28,10 @@ GSE_OK, GSE_NOT_CONVERGED, GSE_NUMERICAL_ABORT = 0, 2, 3
 GSE_ERR_INVALID_ARG, GSE_ERR_DIM_MISMATCH, GSE_ERR_NONFINITE, GSE_ERR_NO_VALUES = 10, 11, 12, 13
 GSE_ERR_UNREPRESENTABLE, GSE_ERR_INVALID_EXP_INDEX, GSE_ERR_FP32_RANGE = 14, 15, 16
 GSE_ERR_WRONG_FORMAT, GSE_ERR_CUDA, GSE_ERR_NCCL, GSE_ERR_OOM = 17, 20, 21, 22
-GSE_KIND_GSE, GSE_KIND_FP64 = 0, 1
+GSE_KIND_GSE, GSE_KIND_FP64, GSE_KIND_FP16, GSE_KIND_BF16 = 0, 1, 2, 3
 
 ABI_SYMBOLS = (
-    "gse_encode", "gse_fp64_matrix", "gse_matrix_get_info", "gse_matrix_copy_planes",
+    "gse_encode", "gse_fp64_matrix", "gse_half_matrix", "gse_matrix_get_info", "gse_matrix_copy_planes",
     "gse_decode", "gse_spmv", "gse_spmv_f32acc", "gse_default_schedule", "gse_solve_cg",
     "gse_solve_gmres", "gse_matrix_free", "gse_status_string", "gse_last_error_detail",
     "gse_set_allocator", "gse_nccl_unique_id", "gse_dist_create", "gse_encode_dist",
@@ -94,6 +94,7 @@ def _declare(L):
     vp, i32, i64, dbl = C.c_void_p, C.c_int, C.c_int64, C.c_double
     L.gse_encode.argtypes = [C.POINTER(CsrF64), C.POINTER(EncodeOpts), C.POINTER(vp), vp]
     L.gse_fp64_matrix.argtypes = [C.POINTER(CsrF64), i32, C.POINTER(vp), vp]
+    L.gse_half_matrix.argtypes = [C.POINTER(CsrF64), i32, i32, C.POINTER(vp), vp]
     L.gse_matrix_get_info.argtypes = [vp, C.POINTER(MatrixInfo)]
     L.gse_matrix_copy_planes.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp]
     L.gse_decode.argtypes = [vp, i32, vp, vp]
@@ -245,6 +246,22 @@ def gse_fp64_matrix(row_ptr, col_idx, values, rows: int, cols: int, device: int 
     return Matrix(out.value)
 
 
+def gse_half_matrix(row_ptr, col_idx, values, rows: int, cols: int, kind: str = "fp16",
+                    device: int | None = None, stream=None) -> Matrix:
+    """The FP16 / BF16 storage baselines: values rounded to nearest-even 16-bit codes
+    on the device, read with FP64 products and sums (gse_spmv segments = 3)."""
+    k = {"fp16": GSE_KIND_FP16, "bf16": GSE_KIND_BF16}[kind]
+    A = _csr(rows, cols, row_ptr, col_idx, values)
+    dev = _device_of(values, col_idx, row_ptr) if device is None else device
+    if dev < 0:
+        dev = _current_device()
+    out = C.c_void_p()
+    _check(_lib.gse_half_matrix(C.byref(A), k, dev, C.byref(out),
+                                _stream(values, col_idx, row_ptr, stream=stream)),
+           "gse_half_matrix")
+    return Matrix(out.value)
+
+
 def _current_device() -> int:
     try:
         import torch
@@ -277,6 +294,11 @@ def gse_matrix_copy_planes(A: Matrix) -> dict:
            "tail1": np.zeros(max(n, 1), np.uint16), "tail2": np.zeros(max(n, 1), np.uint32),
            "table": np.zeros(64, np.uint16)}
     side = None if inf["ei_in_column"] else np.zeros(max(n, 1), np.uint8)
+    if inf["kind"] != GSE_KIND_GSE:  # FP64: columns; FP16 / BF16: columns + 16-bit codes
+        head = out["head"] if inf["kind"] in (GSE_KIND_FP16, GSE_KIND_BF16) else None
+        _check(_lib.gse_matrix_copy_planes(A.handle, _addr(out["col_ei"]), None, _addr(head),
+                                           None, None, None, None), "gse_matrix_copy_planes")
+        return {"col": out["col_ei"][:n], "half": None if head is None else head[:n]}
     _check(_lib.gse_matrix_copy_planes(A.handle, _addr(out["col_ei"]), _addr(side),
                                        _addr(out["head"]), _addr(out["tail1"]),
                                        _addr(out["tail2"]), _addr(out["table"]), None),

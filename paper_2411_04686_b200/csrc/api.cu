@@ -237,7 +237,7 @@ gse_status create_from_csr(const gse_csr_f64* A, int kind, int k_max, int device
   if (kind == GSE_KIND_GSE)
     rc = encode_matrix(M, *A, rp, A->row_ptr_64, col, val, s, comm);
   else
-    rc = fp64_matrix(M, rp, A->row_ptr_64, col, val, s);
+    rc = fp64_matrix(M, rp, A->row_ptr_64, col, val, s, kind);
   if (rc == GSE_OK) rc = st.finish();
   if (rc != GSE_OK) {
     destroy_matrix(M);
@@ -341,6 +341,15 @@ gse_status gse_fp64_matrix(const gse_csr_f64* A, int device, gse_matrix* out, vo
                          nullptr);
 }
 
+gse_status gse_half_matrix(const gse_csr_f64* A, int kind, int device, gse_matrix* out,
+                           void* stream) {
+  if (kind != GSE_KIND_FP16 && kind != GSE_KIND_BF16) {
+    set_error("kind must be GSE_KIND_FP16 or GSE_KIND_BF16");
+    return GSE_ERR_INVALID_ARG;
+  }
+  return create_from_csr(A, kind, 1, device, out, (cudaStream_t)stream, nullptr, nullptr, nullptr);
+}
+
 gse_status gse_matrix_get_info(gse_matrix A, gse_matrix_info* info) {
   if (!A || !info) {
     set_error("NULL argument");
@@ -369,7 +378,7 @@ gse_status gse_matrix_get_info(gse_matrix A, gse_matrix_info* info) {
     info->plane_bytes[4] = M.ei_in_column ? 0 : (size_t)M.nnz;
   } else {
     info->plane_bytes[0] = (size_t)M.nnz * 4;
-    info->plane_bytes[1] = (size_t)M.nnz * 8;
+    info->plane_bytes[1] = (size_t)M.nnz * (M.kind == GSE_KIND_FP64 ? 8 : 2);
   }
   return GSE_OK;
 }
@@ -382,8 +391,12 @@ gse_status gse_matrix_copy_planes(gse_matrix A, uint32_t* col_ei, uint8_t* side_
     return GSE_ERR_INVALID_ARG;
   }
   const Matrix& M = A->m;
-  if (M.kind != GSE_KIND_GSE && (side_ei || head || tail1 || tail2 || table)) {
-    set_error("FP64 matrices have no GSE planes");
+  if (M.kind != GSE_KIND_GSE && (side_ei || tail1 || tail2 || table)) {
+    set_error("FP64 / FP16 / BF16 matrices have no GSE planes");
+    return GSE_ERR_WRONG_FORMAT;
+  }
+  if (M.kind == GSE_KIND_FP64 && head) {
+    set_error("FP64 matrices have no 16-bit plane");
     return GSE_ERR_WRONG_FORMAT;
   }
   DeviceGuard g(M.device);
@@ -429,8 +442,8 @@ gse_status gse_spmv(gse_matrix A, const double* x, double* y, int segments, void
     return GSE_ERR_INVALID_ARG;
   }
   const Matrix& M = A->m;
-  if (M.kind == GSE_KIND_FP64 && segments != 3) {
-    set_error("an FP64-CSR matrix is read at full precision only (segments = 3)");
+  if (M.kind != GSE_KIND_GSE && segments != 3) {
+    set_error("an FP64 / FP16 / BF16 CSR matrix is read at full precision only (segments = 3)");
     return GSE_ERR_WRONG_FORMAT;
   }
   const int64_t xlen = M.dist ? dist_n_local(M) : M.cols;  // dist: x is the rank's slice

@@ -577,7 +577,61 @@ gse_status encode_matrix(Matrix& M, const gse_csr_f64& A, const void* d_row_ptr,
   return GSE_OK;
 }
 
-// ------------------------------------------------------------------ FP64 comparator
+// ------------------------------------------------------------------ FP16 / BF16 baselines
+// P:406 [4.3]: the paper's FP16-SpMV / BF16-SpMV baselines store every value in 16 bits.
+// Conversion (R26): round to nearest, ties to even, straight from the double's bits.  With
+// FB fraction bits and bias BIAS, a = m53 * 2^(E-52) (m53 the 53-bit significand) is a
+// multiple of the quantum 2^q, q = max(E, 1-BIAS) - FB, after rounding n = m53 >> sh,
+// sh = q - (E - 52) >= 52 - FB, on the dropped bits (above half -> up; exactly half -> to
+// the even n).  The code is ((E + BIAS) << FB) + n - 2^FB for normal E (a carry out of
+// the fraction lands in the exponent field) and n itself in the subnormal range (n = 2^FB
+// there is the smallest normal code); a code reaching the all-ones exponent is +-Inf.
+template <int FB, int EB>
+__device__ __forceinline__ uint16_t round_to_half(double v) {
+  constexpr int BIAS = (1 << (EB - 1)) - 1;
+  constexpr uint32_t INF = ((1u << EB) - 1u) << FB;
+  const uint64_t bits = (uint64_t)__double_as_longlong(v);
+  const uint32_t sign = (uint32_t)(bits >> 48) & 0x8000u;
+  const int e64 = (int)((bits >> 52) & 0x7FF);
+  const uint64_t frac = bits & ((1ull << 52) - 1);
+  if (e64 == 0x7FF) return (uint16_t)(sign | INF | (frac ? (1u << (FB - 1)) : 0u));  // Inf/NaN
+  if (e64 == 0) return (uint16_t)sign;  // zero / FP64 subnormal (< 2^-1022): rounds to 0
+  const int E = e64 - 1023;
+  if (E > BIAS) return (uint16_t)(sign | INF);  // >= 2^(emax+1): overflow
+  const uint64_t m53 = (1ull << 52) | frac;
+  const int q = (E < 1 - BIAS ? 1 - BIAS : E) - FB;
+  const int sh = q - (E - 52);
+  uint64_t n;
+  if (sh >= 64) {
+    n = 0;
+  } else {
+    n = m53 >> sh;
+    const uint64_t rem = m53 & ((1ull << sh) - 1), halfw = 1ull << (sh - 1);
+    if (rem > halfw || (rem == halfw && (n & 1))) ++n;
+  }
+  uint32_t code = (E < 1 - BIAS) ? (uint32_t)n
+                                 : ((uint32_t)(E + BIAS) << FB) + (uint32_t)n - (1u << FB);
+  if (code >= INF) code = INF;
+  return (uint16_t)(sign | code);
+}
+
+template <int KIND>
+__global__ void k_copy_half(const double* __restrict__ val, const int32_t* __restrict__ col,
+                            int64_t nnz, int64_t cols, uint16_t* __restrict__ hout,
+                            uint32_t* __restrict__ cout, unsigned long long* __restrict__ bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long b = ~0ull;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += stride) {
+    const int32_t c = col[i];
+    if (c < 0 || (int64_t)c >= cols) b = min(b, (unsigned long long)i);
+    hout[i] = KIND == GSE_KIND_FP16 ? round_to_half<10, 5>(val[i]) : round_to_half<7, 8>(val[i]);
+    cout[i] = (uint32_t)c;
+  }
+  if (b != ~0ull) atomicMin(bad, b);
+}
+
+// ------------------------------------------------------------------ FP64 comparator (and the
+// FP16 / BF16 baselines below, which share its structure checks and partition)
 __global__ void k_copy_fp64(const double* __restrict__ val, const int32_t* __restrict__ col,
                             int64_t nnz, int64_t cols, double* __restrict__ vout,
                             uint32_t* __restrict__ cout, unsigned long long* __restrict__ bad) {
@@ -593,8 +647,8 @@ __global__ void k_copy_fp64(const double* __restrict__ val, const int32_t* __res
 }
 
 gse_status fp64_matrix(Matrix& M, const void* d_row_ptr, int rp64, const int32_t* d_col,
-                       const double* d_val, cudaStream_t s) {
-  M.kind = GSE_KIND_FP64;
+                       const double* d_val, cudaStream_t s, int kind) {
+  M.kind = kind;
   M.ei_bits = 0;
   M.ei_in_column = 1;
   M.table_len = 0;
@@ -606,14 +660,24 @@ gse_status fp64_matrix(Matrix& M, const void* d_row_ptr, int rp64, const int32_t
   gse_status rc = convert_row_ptr(M, d_row_ptr, rp64, s, d_flags);
   if (rc != GSE_OK) return rc;
   const size_t np = padded(M.nnz);
-  M.val = dev_alloc_n<double>(np, s);
   M.col_ei = dev_alloc_n<uint32_t>(np, s);
-  if (!M.val || !M.col_ei) return GSE_ERR_OOM;
-  GSE_CUDA_TRY(cudaMemsetAsync(M.val + M.nnz, 0, (np - M.nnz) * 8, s));
+  if (kind == GSE_KIND_FP64)
+    M.val = dev_alloc_n<double>(np, s);
+  else
+    M.head = dev_alloc_n<uint16_t>(np, s);
+  if ((!M.val && !M.head) || !M.col_ei) return GSE_ERR_OOM;
+  if (M.val) GSE_CUDA_TRY(cudaMemsetAsync(M.val + M.nnz, 0, (np - M.nnz) * 8, s));
+  if (M.head) GSE_CUDA_TRY(cudaMemsetAsync(M.head + M.nnz, 0, (np - M.nnz) * 2, s));
   GSE_CUDA_TRY(cudaMemsetAsync(M.col_ei + M.nnz, 0, (np - M.nnz) * 4, s));
   if (M.nnz > 0) {
-    k_copy_fp64<<<grid_for(M.nnz, 256, M.device), 256, 0, s>>>(
-        d_val, d_col, M.nnz, M.cols, M.val, M.col_ei, (unsigned long long*)(d_flags + 2));
+    unsigned long long* bad = (unsigned long long*)(d_flags + 2);
+    const int g = grid_for(M.nnz, 256, M.device);
+    if (kind == GSE_KIND_FP64)
+      k_copy_fp64<<<g, 256, 0, s>>>(d_val, d_col, M.nnz, M.cols, M.val, M.col_ei, bad);
+    else if (kind == GSE_KIND_FP16)
+      k_copy_half<GSE_KIND_FP16><<<g, 256, 0, s>>>(d_val, d_col, M.nnz, M.cols, M.head, M.col_ei, bad);
+    else
+      k_copy_half<GSE_KIND_BF16><<<g, 256, 0, s>>>(d_val, d_col, M.nnz, M.cols, M.head, M.col_ei, bad);
     GSE_CUDA_TRY(cudaGetLastError());
   }
   rc = build_partition(M, s);

@@ -65,7 +65,7 @@ struct Matrix {
   uint32_t* row_ptr = nullptr;  // [rows + 1]
   uint32_t* col_ei = nullptr;   // [nnz_pad] column | EI << (32 - ei_bits)  (or plain column)
   uint8_t* side_ei = nullptr;   // [nnz_pad] when !ei_in_column
-  uint16_t* head = nullptr;     // [nnz_pad]
+  uint16_t* head = nullptr;     // [nnz_pad] (FP16 / BF16 kinds: the 16-bit codes)
   uint16_t* tail1 = nullptr;    // [nnz_pad]
   uint32_t* tail2 = nullptr;    // [nnz_pad]
   double* val = nullptr;        // [nnz_pad] FP64 kind
@@ -160,8 +160,9 @@ gse_status build_partition(Matrix& M, cudaStream_t s);
 gse_status encode_matrix(Matrix& M, const gse_csr_f64& A, const void* d_row_ptr, int rp64,
                          const int32_t* d_col, const double* d_val, cudaStream_t s,
                          Comm* comm = nullptr);
+// kind: GSE_KIND_FP64 (values copied) or GSE_KIND_FP16 / GSE_KIND_BF16 (RNE to 16 bits, R26)
 gse_status fp64_matrix(Matrix& M, const void* d_row_ptr, int rp64, const int32_t* d_col,
-                       const double* d_val, cudaStream_t s);
+                       const double* d_val, cudaStream_t s, int kind = GSE_KIND_FP64);
 void build_decode_table(Matrix& M);
 gse_status decode_all(const Matrix& M, int level, double* out, cudaStream_t s);
 

@@ -1127,7 +1127,7 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
                     const gse_step_schedule& sched, gse_solve_report& rep, cudaStream_t s) {
   const int64_t n = M.rows;  // local rows (distributed: this rank's slice)
   const int stepped = sched.enabled && M.kind == GSE_KIND_GSE;
-  int level = (M.kind == GSE_KIND_FP64) ? 3 : sched.start_level;
+  int level = (M.kind != GSE_KIND_GSE) ? 3 : sched.start_level;  // FP64/FP16/BF16: one precision
   const bool dist = M.dist != nullptr;
   gse_status rc = ensure_ws(M, stepped ? sched.t : 0, 0, s);
   if (rc != GSE_OK) return rc;
@@ -1403,7 +1403,7 @@ gse_status solve_gmres(Matrix& M, const double* b, double* x, double tol, int re
                        cudaStream_t s) {
   const int64_t n = M.rows;
   const int stepped = sched.enabled && M.kind == GSE_KIND_GSE;
-  int level = (M.kind == GSE_KIND_FP64) ? 3 : sched.start_level;
+  int level = (M.kind != GSE_KIND_GSE) ? 3 : sched.start_level;  // FP64/FP16/BF16: one precision
   gse_status rc = ensure_ws(M, stepped ? sched.t : 0, restart, s);
   if (rc != GSE_OK) return rc;
   SolverWs* ws = M.ws;

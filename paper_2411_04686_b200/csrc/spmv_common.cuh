@@ -1,6 +1,8 @@
 // spmv_common.cuh -- shared pieces of the two SpMV kernels (spmv_sp.cu: strided products
 // for irregular rows; spmv_rw.cu: row walk over staged planes for regular rows).
 #pragma once
+#include <cuda_fp16.h>
+
 #include <cstdint>
 
 #include "decode.cuh"
@@ -57,6 +59,28 @@ __device__ __forceinline__ uint2 ld_nc_v2(const void* p) {
       : "=r"(r.x), "=r"(r.y)
       : "l"(p), "l"(l2_evict_first()));
   return r;
+}
+
+// Kernel "levels": 0 = FP64 CSR (a6), 1..3 = GSE segments (a5), and the 16-bit storage
+// baselines of P:406 (FP16 / BF16 codes in the head plane, converted exactly to FP64).
+constexpr int L_FP16 = 4, L_BF16 = 5;
+template <int L>
+__host__ __device__ constexpr bool has_head() { return L >= 1; }
+template <int L>
+__host__ __device__ constexpr bool has_t1() { return L == 2 || L == 3; }
+template <int L>
+__host__ __device__ constexpr bool has_t2() { return L == 3; }
+template <int L>
+__host__ __device__ constexpr bool is_half() { return L == L_FP16 || L == L_BF16; }
+
+// exact FP64 value of a 16-bit code (binary16: via FP32, which holds every binary16 value;
+// bfloat16: the top half of an FP32)
+template <int L>
+__device__ __forceinline__ double half_value(uint32_t h) {
+  if constexpr (L == L_FP16)
+    return (double)__half2float(__ushort_as_half((unsigned short)h));
+  else
+    return (double)__uint_as_float(h << 16);
 }
 
 template <class T>

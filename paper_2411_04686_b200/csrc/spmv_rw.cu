@@ -56,7 +56,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // bytes per staged element at level L (col_ei + requested planes; L = 0: FP64 values)
 template <int L>
 __host__ __device__ constexpr uint32_t rw_elem_bytes() {
-  return 4u + (L == 0 ? 8u : 0u) + (L >= 1 ? 2u : 0u) + (L >= 2 ? 2u : 0u) + (L == 3 ? 4u : 0u);
+  return 4u + (L == 0 ? 8u : 0u) + (has_head<L>() ? 2u : 0u) + (has_t1<L>() ? 2u : 0u) +
+         (has_t2<L>() ? 4u : 0u);
 }
 
 // views of one staging buffer (rebuilt from the dynamic shared array each time, so the
@@ -76,9 +77,9 @@ struct Stage {
     val = reinterpret_cast<double*>(q);
     if (L == 0) q += 8 * N;
     head = reinterpret_cast<uint16_t*>(q);
-    if (L >= 1) q += 2 * N;
+    if (has_head<L>()) q += 2 * N;
     tail1 = reinterpret_cast<uint16_t*>(q);
-    if (L >= 2) q += 2 * N;
+    if (has_t1<L>()) q += 2 * N;
     tail2 = reinterpret_cast<uint32_t*>(q);
   }
 };
@@ -96,9 +97,9 @@ __device__ __forceinline__ void issue_stage(const SpmvParams<T>& p, const Stage<
   if (n == 0) return;
   bulk_g2s(st.col, p.col_ei + base, 4 * n, bar);
   if constexpr (L == 0) bulk_g2s(st.val, p.val + base, 8 * n, bar);
-  if constexpr (L >= 1) bulk_g2s(st.head, p.head + base, 2 * n, bar);
-  if constexpr (L >= 2) bulk_g2s(st.tail1, p.tail1 + base, 2 * n, bar);
-  if constexpr (L == 3) bulk_g2s(st.tail2, p.tail2 + base, 4 * n, bar);
+  if constexpr (has_head<L>()) bulk_g2s(st.head, p.head + base, 2 * n, bar);
+  if constexpr (has_t1<L>()) bulk_g2s(st.tail1, p.tail1 + base, 2 * n, bar);
+  if constexpr (has_t2<L>()) bulk_g2s(st.tail2, p.tail2 + base, 4 * n, bar);
 }
 
 // index of the zero entry of the sign-folded scale tables: masked slots decode to exact 0
@@ -123,9 +124,9 @@ __device__ __forceinline__ T walk_row(const SpmvParams<T>& p, const Stage<L>& st
     for (int q = 0; q < 8; ++q) {
       c[q] = st.col[j + q];
       if constexpr (L == 0) v0[q] = st.val[j + q];
-      if constexpr (L >= 1) h[q] = st.head[j + q];
-      if constexpr (L >= 2) t1[q] = st.tail1[j + q];
-      if constexpr (L == 3) t2[q] = st.tail2[j + q];
+      if constexpr (has_head<L>()) h[q] = st.head[j + q];
+      if constexpr (has_t1<L>()) t1[q] = st.tail1[j + q];
+      if constexpr (has_t2<L>()) t2[q] = st.tail2[j + q];
     }
     // all 8 gathers issued before any product (ld.global.nc, volatile asm keeps the order)
 #pragma unroll
@@ -147,6 +148,8 @@ __device__ __forceinline__ T walk_row(const SpmvParams<T>& p, const Stage<L>& st
       T prod;
       if constexpr (L == 0) {
         prod = (T)__dmul_rn(ok ? v0[q] : 0.0, (double)xv[q]);
+      } else if constexpr (is_half<L>()) {  // P:406 baselines: exact code value x x in FP64
+        prod = (T)__dmul_rn(ok ? half_value<L>(h[q]) : 0.0, (double)xv[q]);
       } else if constexpr (FAST) {
         // scale index = EI | sign << ei_bits in one funnel shift (col's top bits are EI);
         // a masked slot selects the zero entry
@@ -359,6 +362,13 @@ static void go_dot(const Matrix& M, int level, bool fast, const SpmvParams<T>& p
                    cudaStream_t s) {
   if (M.kind == GSE_KIND_FP64) {
     go<0, DOT, false, T>(M, p, s);
+  } else if (M.kind == GSE_KIND_FP16 || M.kind == GSE_KIND_BF16) {
+    if constexpr (sizeof(T) == 8) {  // FP64 accumulation only
+      if (M.kind == GSE_KIND_FP16)
+        go<L_FP16, DOT, false, T>(M, p, s);
+      else
+        go<L_BF16, DOT, false, T>(M, p, s);
+    }
   } else if (level == 1) {
     go_l<1, DOT, T>(M, fast, p, s);
   } else if (level == 2) {

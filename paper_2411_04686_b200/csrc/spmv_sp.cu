@@ -29,10 +29,10 @@ __device__ __forceinline__ void products(const SpmvParams<T>& p, const long long
     const bool ok = i < e;
     c[k] = ok ? ld_nc_u32(p.col_ei + i) : 0u;
     if constexpr (L == 0) v64[k] = ok ? ld_nc_f64(p.val + i) : 0.0;
-    if constexpr (L >= 1) h[k] = ok ? ld_nc_u16(p.head + i) : 0u;
-    if constexpr (L >= 2) t1[k] = ok ? ld_nc_u16(p.tail1 + i) : 0u;
-    if constexpr (L == 3) t2[k] = ok ? ld_nc_u32(p.tail2 + i) : 0u;
-    if constexpr (SIDE && L >= 1) ei[k] = ok ? (ld_nc_u8(p.side + i) & 63u) : 0u;
+    if constexpr (has_head<L>()) h[k] = ok ? ld_nc_u16(p.head + i) : 0u;
+    if constexpr (has_t1<L>()) t1[k] = ok ? ld_nc_u16(p.tail1 + i) : 0u;
+    if constexpr (has_t2<L>()) t2[k] = ok ? ld_nc_u32(p.tail2 + i) : 0u;
+    if constexpr (SIDE && L >= 1 && !is_half<L>()) ei[k] = ok ? (ld_nc_u8(p.side + i) & 63u) : 0u;
   }
   // all EPL gathers issued back to back (masked slots gather x[0], always valid) before any
   // product: volatile asm keeps them together, the register budget of the launch bounds
@@ -52,6 +52,8 @@ __device__ __forceinline__ void products(const SpmvParams<T>& p, const long long
   for (int k = 0; k < EPL; ++k) {
     if constexpr (L == 0) {
       out[k] = (T)(v64[k] * (double)xv[k]);
+    } else if constexpr (is_half<L>()) {  // P:406 baselines: exact code value x x in FP64
+      out[k] = (T)(half_value<L>(h[k]) * (double)xv[k]);
     } else {
       if constexpr (!SIDE) ei[k] = __funnelshift_rc(c[k], 0u, p.ei_shift);
       if constexpr (sizeof(T) == 8)
@@ -161,6 +163,13 @@ template <bool DOT, class T>
 static void go_dot(const Matrix& M, int level, bool fast, const SpmvParams<T>& p, cudaStream_t s) {
   if (M.kind == GSE_KIND_FP64) {
     go<0, false, DOT, false, T>(M, p, s);
+  } else if (M.kind == GSE_KIND_FP16 || M.kind == GSE_KIND_BF16) {
+    if constexpr (sizeof(T) == 8) {  // FP64 accumulation only
+      if (M.kind == GSE_KIND_FP16)
+        go<L_FP16, false, DOT, false, T>(M, p, s);
+      else
+        go<L_BF16, false, DOT, false, T>(M, p, s);
+    }
   } else if (level == 1) {
     go_l<1, DOT, T>(M, fast, p, s);
   } else if (level == 2) {
