@@ -327,15 +327,18 @@ def run_gse(args, world, rank, local, pg):
             "stepped_gse_solve_only": extra["cg_gse_ms"], "encode": extra["encode_ms"],
             "fp64_csr_cg": extra["cg_fp64_ms"],
             "speedup_vs_fp64_csr": extra["cg_fp64_ms"] / extra["cg_gse_ms"]}
+        line["time_to_1e-10_ms"]["half_storage_cg"] = extra["cg_half"]
         line["solve"]["fp64_iterations"] = extra["cg_fp64_iters"]
         line["spmv_sweep"] = extra["spmv"]
+        line["spmv_sweep_steady"] = extra["spmv_steady"]
         line["roofline"] = {
             "bound": "hbm", "kernel": "k_spmv_rw<L=1> (level-1 GSE SpMV, row walk; the CG inner kernel)",
             "achieved": dom["GBps"], "peak": hbm_peak, "unit": "GB/s",
             "frac": dom["GBps"] / hbm_peak, "peak_source": peak_src,
             "traffic": _profiled_traffic(), "algorithmic_bytes_per_launch": dom["bytes"],
             "avg_launch_us": dom["us"],
-            "timing": "CUDA events per launch on the launching stream, L2 flushed before each"}
+            "timing": "CUDA events per launch on the launching stream, L2 flushed before each "
+                      "(cold; spmv_sweep_steady has back-to-back launches as in the CG loop)"}
     print(json.dumps(line), flush=True)
 
 
@@ -406,6 +409,26 @@ def spmv_and_cg_sweep(args, A, rp, col, val, b, dev, stream, flush, hbm_peak):
         rec(f"L{L}_f32acc", lambda: g.gse_spmv_f32acc(M, x32, y32, segments=L),
             nnz * (4 + s_l) + rows_bytes + 8 * n)
     rec("fp64_csr", lambda: g.gse_spmv(F, x, y, segments=3), nnz * 12 + rows_bytes + 16 * n)
+    # the paper's 16-bit storage baselines: FP16 / BF16 values, FP64 products and sums
+    H = {k: g.gse_half_matrix(rp, col, val, A.rows, A.cols, kind=k) for k in ("fp16", "bf16")}
+    for k, Hm in H.items():
+        rec(k, lambda: g.gse_spmv(Hm, x, y, segments=3), nnz * 6 + rows_bytes + 16 * n)
+    # steady state, as inside the CG loop: back-to-back launches, no flush in between
+    steady = {}
+    for L in (1, 2, 3):
+        fn = lambda: g.gse_spmv(M, x, y, segments=L)
+        fn()
+        l2_flush(flush, 0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 4 * args.spmv_reps
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) * 1e-3 / reps
+        byt = out[f"L{L}"]["bytes"]
+        steady[f"L{L}"] = {"us": t * 1e6, "GBps": byt / t / 1e9, "frac_hbm": byt / t / 1e9 / hbm_peak}
     # CG solve only (no encode), stepped GSE vs FP64-CSR
     xs = torch.zeros(n, dtype=torch.float64, device=dev)
     sched = g.gse_default_schedule("cg")
@@ -423,6 +446,16 @@ def spmv_and_cg_sweep(args, A, rp, col, val, b, dev, stream, flush, hbm_peak):
     t_gse = statistics.median(time_cuda(cg_gse, 3, stream, flush))
     t_f64 = statistics.median(time_cuda(cg_f64, 3, stream, flush))
     rf = cg_f64()
+    half_cg = {}
+    for k, Hm in H.items():
+        def cg_h(Hm=Hm):
+            xs.zero_()
+            return g.gse_solve_cg(Hm, b, xs, tol=1e-10)[1]
+        rh = cg_h()
+        half_cg[k] = {"ms": statistics.median(time_cuda(cg_h, 3, stream, flush)),
+                      "iterations": rh["iterations"], "status": rh["status"],
+                      "rel_residual_true_vs_rounded_matrix": rh["rel_residual_true"]}
+        Hm.close()
 
     def enc():
         m = g.gse_encode(rp, col, val, A.rows, A.cols)
@@ -431,8 +464,8 @@ def spmv_and_cg_sweep(args, A, rp, col, val, b, dev, stream, flush, hbm_peak):
     t_enc = statistics.median(time_cuda(enc, 3, stream, flush))
     M.close()
     F.close()
-    return {"spmv": out, "cg_gse_ms": t_gse, "cg_fp64_ms": t_f64,
-            "cg_fp64_iters": rf["iterations"], "encode_ms": t_enc}
+    return {"spmv": out, "spmv_steady": steady, "cg_gse_ms": t_gse, "cg_fp64_ms": t_f64,
+            "cg_fp64_iters": rf["iterations"], "encode_ms": t_enc, "cg_half": half_cg}
 
 
 def e2e_measure(args, A, b_h, dev, stream, encode, r0, n_glob):

@@ -252,8 +252,10 @@ gse_status gse_dist_create_thread(void* group, int rank, int device, gse_dist* o
  * The exponent histogram is summed over ranks before the table is chosen, so all ranks
  * share one table (R21); columns are renumbered locally (owned first, then the halo in
  * global order).  gse_spmv on the result takes / returns the rank's slices (x: local_rows
- * entries); gse_solve_cg runs the distributed CG (halo exchange + allreduces); GMRES and
- * FP32 accumulation are single-GPU only (GSE_ERR_WRONG_FORMAT). */
+ * entries); gse_solve_cg runs the distributed CG (halo exchange + two allreduces per
+ * iteration); gse_solve_gmres the distributed GMRES(m) (halo exchange per SpMV, one
+ * allreduce per MGS dot and per norm: j + 2 per inner step, MGS order kept).  FP32
+ * accumulation is single-GPU only (GSE_ERR_WRONG_FORMAT). */
 gse_status gse_encode_dist(gse_dist D, const gse_csr_f64* local_rows, int64_t row_begin,
                            int64_t global_rows, const gse_encode_opts* opts, gse_matrix* out,
                            void* stream);

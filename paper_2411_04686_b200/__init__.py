@@ -21,7 +21,8 @@ import numpy as np
 from . import build as _build
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = _build.LIB
+# GSE_LIB_PATH: developer A/B override (a prebuilt variant of the same library)
+LIB_PATH = os.environ.get("GSE_LIB_PATH") or _build.LIB
 
 # ---------------------------------------------------------------------------- status codes
 GSE_OK, GSE_NOT_CONVERGED, GSE_NUMERICAL_ABORT = 0, 2, 3
@@ -41,7 +42,7 @@ ABI_SYMBOLS = (
 
 
 def _load():
-    if _build.stale():
+    if LIB_PATH == _build.LIB and _build.stale():
         if shutil.which(_build.NVCC) or os.path.exists(_build.NVCC):
             _build.build()
         elif not os.path.exists(LIB_PATH):

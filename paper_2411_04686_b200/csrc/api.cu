@@ -518,10 +518,6 @@ static gse_status solve_common(gse_matrix A, const double* b, double* x, double 
     set_error("solvers need a square matrix");
     return GSE_ERR_DIM_MISMATCH;
   }
-  if (M.dist && gmres) {
-    set_error("distributed GMRES is not implemented (distributed CG is)");
-    return GSE_ERR_WRONG_FORMAT;
-  }
   if (!(tol > 0.0) || max_iters < 0 || (M.rows > 0 && (!b || !x))) {
     set_error("invalid tol (must be > 0), max_iters or NULL b/x");
     return GSE_ERR_INVALID_ARG;

@@ -461,20 +461,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_xpay(const SolveCtrl* __restrict_
 
 // ---------------------------------------------------------------- GMRES kernels
 // prologue: w = b - A x ; beta = ||w|| ; explicit convergence / budget checks
-__global__ void __launch_bounds__(256, 4) k_gm_restart(SolveCtrl* __restrict__ c,
-                                                    const double* __restrict__ b,
-                                                    double* __restrict__ w, int64_t n,
-                                                    double* partials, unsigned* ticket) {
-  pdl_wait();
-  pdl_trigger();
-  double acc = 0.0;
-  GRID_LOOP(i, n) {
-    const double v = __dsub_rn(b[i], w[i]);
-    w[i] = v;
-    acc = __dadd_rn(acc, __dmul_rn(v, v));
-  }
-  double tot;
-  if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0) {
+__device__ void gm_restart_logic(SolveCtrl* c, double tot) {
     const double beta = sqrt(tot);
     const double resid = beta / c->bnorm;
     c->resid = resid;
@@ -495,7 +482,34 @@ __global__ void __launch_bounds__(256, 4) k_gm_restart(SolveCtrl* __restrict__ c
       for (int i = 0; i <= c->restart; ++i) c->g[i] = 0.0;
       c->g[0] = beta;
     }
+}
+
+// defer (distributed): only this rank's ||w||^2 partial -> c->dot; the host allreduces it
+// and k_gm_restart_fin applies the logic on the global sum (identically on every rank)
+__global__ void __launch_bounds__(256, 4) k_gm_restart(SolveCtrl* __restrict__ c,
+                                                    const double* __restrict__ b,
+                                                    double* __restrict__ w, int64_t n,
+                                                    double* partials, unsigned* ticket,
+                                                    int defer) {
+  pdl_wait();
+  pdl_trigger();
+  double acc = 0.0;
+  GRID_LOOP(i, n) {
+    const double v = __dsub_rn(b[i], w[i]);
+    w[i] = v;
+    acc = __dadd_rn(acc, __dmul_rn(v, v));
   }
+  double tot;
+  if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0) {
+    if (defer)
+      c->dot = tot;
+    else
+      gm_restart_logic(c, tot);
+  }
+}
+
+__global__ void k_gm_restart_fin(SolveCtrl* __restrict__ c) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) gm_restart_logic(c, c->dot);
 }
 
 // dst = src / *den   (skipped when stopped)
@@ -765,7 +779,8 @@ __global__ void __launch_bounds__(GM_THREADS, 1) k_gm_arnoldi(SolveCtrl* __restr
 __global__ void __launch_bounds__(256, 4) k_gm_last(SolveCtrl* __restrict__ c, double* ring,
                                                  double* __restrict__ w,
                                                  const double* __restrict__ V, int64_t n, int j,
-                                                 double* partials, unsigned* ticket) {
+                                                 double* partials, unsigned* ticket,
+                                                 int defer) {
   pdl_wait();
   pdl_trigger();
   if (c->stop) return;
@@ -807,8 +822,17 @@ __global__ void __launch_bounds__(256, 4) k_gm_last(SolveCtrl* __restrict__ c, d
     }
   }
   double tot;
-  if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0)
-    gm_finish(c, ring, j, sqrt(tot), c->H + j, m, c->cs, c->sn, c->g);
+  if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0) {
+    if (defer)  // distributed: ||w||^2 partial, finished by k_gm_last_fin after the allreduce
+      c->dot = tot;
+    else
+      gm_finish(c, ring, j, sqrt(tot), c->H + j, m, c->cs, c->sn, c->g);
+  }
+}
+
+__global__ void k_gm_last_fin(SolveCtrl* __restrict__ c, double* ring, int j) {
+  if (threadIdx.x != 0 || blockIdx.x != 0 || c->stop) return;
+  gm_finish(c, ring, j, sqrt(c->dot), c->H + j, c->restart, c->cs, c->sn, c->g);
 }
 
 // back substitution H[0:k,0:k] y = g[0:k] (one thread; k <= restart)
@@ -1355,7 +1379,7 @@ static gse_status build_gm_graph(Matrix& M, int level, int restart) {
   double* w = ws->tmp;
   GSE_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
   gse_status rc = launch_spmv(M, level, ws->x, w, nullptr, cs);
-  launch_pdl(k_gm_restart, ws->vgrid, 256, 0, cs, c, ws->b, w, n, ws->partials, ws->ticket);
+  launch_pdl(k_gm_restart, ws->vgrid, 256, 0, cs, c, ws->b, w, n, ws->partials, ws->ticket, 0);
   launch_pdl(k_gm_scale, ws->vgrid, 256, 0, cs, c, w, ws->V, n, 0);
   int cg_grid = 0, cg_e = 0;
   size_t cg_smem = 0;
@@ -1383,7 +1407,7 @@ static gse_status build_gm_graph(Matrix& M, int level, int restart) {
     }
     for (int i = 0; i <= j; ++i)
       launch_pdl(k_gm_mgs, ws->vgrid, 256, 0, cs, c, w, ws->V, n, i, j, ws->partials, ws->ticket);
-    launch_pdl(k_gm_last, ws->vgrid, 256, 0, cs, c, ws->ring, w, ws->V, n, j, ws->partials, ws->ticket);
+    launch_pdl(k_gm_last, ws->vgrid, 256, 0, cs, c, ws->ring, w, ws->V, n, j, ws->partials, ws->ticket, 0);
     if (j + 1 < restart)
       launch_pdl(k_gm_scale, ws->vgrid, 256, 0, cs, c, w, ws->V + (size_t)(j + 1) * n, n, 1);
   }
@@ -1395,6 +1419,43 @@ static gse_status build_gm_graph(Matrix& M, int level, int restart) {
   GSE_CUDA_TRY(e);
   GSE_CUDA_TRY(cudaGraphInstantiate(&ws->gm_exec[level - 1], g, 0));
   ws->gm_graph[level - 1] = g;
+  return GSE_OK;
+}
+
+// One restart cycle enqueued directly (no graph) for a row-partitioned matrix: every rank
+// enqueues the same kernels and collectives (halo exchange before each SpMV, one 8-byte
+// allreduce per MGS dot, per ||w||^2 and per restart norm -- j + 2 per inner step, MGS
+// order kept); kernels after a stop return early, so the collectives of the
+// skipped steps sum values nobody reads.  All ranks see bit-identical scalars (allreduce),
+// hence identical H, Givens rotations, monitor decisions and events.
+static gse_status gm_cycle_dist(Matrix& M, int level, int restart, cudaStream_t s) {
+  SolverWs* ws = M.ws;
+  const int64_t n = M.rows;
+  SolveCtrl* c = ws->ctrl;
+  double* w = ws->tmp;
+  gse_status rc = spmv_local(M, level, ws->x, w, nullptr, s);
+  if (rc != GSE_OK) return rc;
+  launch_k(k_gm_restart, ws->vgrid, 256, 0, s, c, ws->b, w, n, ws->partials, ws->ticket, 1);
+  if ((rc = dist_allreduce_sum(M, &c->dot, 1, s)) != GSE_OK) return rc;
+  launch_k(k_gm_restart_fin, 1, 32, 0, s, c);
+  launch_k(k_gm_scale, ws->vgrid, 256, 0, s, c, w, ws->V, n, 0);
+  for (int j = 0; j < restart; ++j) {
+    rc = spmv_local(M, level, ws->V + (size_t)j * n, w, nullptr, s, &c->stop);
+    if (rc != GSE_OK) return rc;
+    for (int i = 0; i <= j; ++i) {
+      launch_k(k_gm_mgs, ws->vgrid, 256, 0, s, c, w, ws->V, n, i, j, ws->partials, ws->ticket);
+      if ((rc = dist_allreduce_sum(M, &c->H[i * restart + j], 1, s)) != GSE_OK) return rc;
+    }
+    launch_k(k_gm_last, ws->vgrid, 256, 0, s, c, ws->ring, w, ws->V, n, j, ws->partials,
+             ws->ticket, 1);
+    if ((rc = dist_allreduce_sum(M, &c->dot, 1, s)) != GSE_OK) return rc;
+    launch_k(k_gm_last_fin, 1, 32, 0, s, c, ws->ring, j);
+    if (j + 1 < restart)
+      launch_k(k_gm_scale, ws->vgrid, 256, 0, s, c, w, ws->V + (size_t)(j + 1) * n, n, 1);
+  }
+  launch_k(k_gm_backsolve, 1, 32, 0, s, c);
+  launch_k(k_gm_xupdate, ws->vgrid, 256, 0, s, c, ws->x, ws->V, n);
+  GSE_CUDA_TRY(cudaGetLastError());
   return GSE_OK;
 }
 
@@ -1412,6 +1473,8 @@ gse_status solve_gmres(Matrix& M, const double* b, double* x, double tol, int re
   GSE_CUDA_TRY(cudaMemcpyAsync(ws->x, x, n * 8, cudaMemcpyDeviceToDevice, s));
   launch_k(k_dot, ws->vgrid, 256, 0, s, ws->b, ws->b, n, ws->partials, ws->ticket, &ws->ctrl->dot);
   GSE_CUDA_TRY(cudaGetLastError());
+  rc = dist_allreduce_sum(M, &ws->ctrl->dot, 1, s);
+  if (rc != GSE_OK) return rc;
   rc = read_ctrl(ws, s);
   if (rc != GSE_OK) return rc;
   SolveCtrl* hc = ws->hctrl;
@@ -1436,9 +1499,14 @@ gse_status solve_gmres(Matrix& M, const double* b, double* x, double tol, int re
   gse_status status = GSE_NOT_CONVERGED;
   int64_t last_iter = 0, iter = 0;
   for (;;) {
-    rc = build_gm_graph(M, level, restart);
-    if (rc != GSE_OK) return rc;
-    GSE_CUDA_TRY(cudaGraphLaunch(ws->gm_exec[level - 1], s));
+    if (M.dist) {
+      rc = gm_cycle_dist(M, level, restart, s);
+      if (rc != GSE_OK) return rc;
+    } else {
+      rc = build_gm_graph(M, level, restart);
+      if (rc != GSE_OK) return rc;
+      GSE_CUDA_TRY(cudaGraphLaunch(ws->gm_exec[level - 1], s));
+    }
     rc = read_ctrl(ws, s);
     if (rc != GSE_OK) return rc;
     iter = hc->iter;

@@ -194,8 +194,16 @@ __device__ __forceinline__ T walk_row(const SpmvParams<T>& p, const Stage<L>& st
 // RPL = rows per lane: a group is 32 * RPL consecutive rows staged by one set of bulk
 // copies and walked in RPL passes of lane = row (RPL = 2 halves the per-group overhead:
 // row bounds, copy issue, barrier wait)
+// register budget: 3 resident CTAs per SM (measured: capping at 64 registers for 4 CTAs
+// gains 6 % on the plain level-1 SpMV at 256^3 but loses 6 % on the 128^3 CG's fused-dot
+// variant and 1-7 % at levels 2/3); GSE_RW_MINB overrides (A/B builds)
+#ifdef GSE_RW_MINB
+#define RW_MINB(L) GSE_RW_MINB
+#else
+#define RW_MINB(L) 3
+#endif
 template <int L, int RPL, bool DOT, bool FAST, class T>
-__global__ void __launch_bounds__(SPMV_THREADS, 3) k_spmv_rw(const SpmvParams<T> p) {
+__global__ void __launch_bounds__(SPMV_THREADS, RW_MINB(L)) k_spmv_rw(const SpmvParams<T> p) {
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t bars[SPMV_WARPS][2];
   __shared__ long long sd64[64];

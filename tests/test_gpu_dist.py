@@ -134,3 +134,53 @@ def test_dist_cg(g, P, variant):
     F = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
     res = np.linalg.norm(b - O.spmv_fp64(F, x)) / np.linalg.norm(b)
     assert res <= 1e-10 * 1.01
+
+
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("mode", ["fp64", "stepped_scaled"])
+def test_dist_gmres(g, P, mode):
+    """row-partitioned GMRES(30) (halo per SpMV, one allreduce per MGS dot and norm): every
+    rank takes the same decisions; iterations within 2 of the single-GPU solve and of the
+    oracle; true residual <= tol"""
+    A = gi.convdiff3d(12)
+    b = gi.ones_rhs(A)
+    if mode == "fp64":
+        enc1 = lambda: g.gse_fp64_matrix(A.row_ptr, A.col, A.val, A.rows, A.cols)
+        sched, so = (lambda: None), None
+        Ro = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+    else:
+        enc1 = lambda: g.gse_encode(A.row_ptr, A.col, A.val, A.rows, A.cols)
+        sched = lambda: g.gse_default_schedule("gmres", l=30, t=10, m=10)
+        so = O.schedule("gmres", l=30, t=10, m=10)
+        Ro = O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+    _, r1 = g.gse_solve_gmres(enc1(), b, tol=1e-10, sched=sched())
+    _, ro = O.gmres(Ro, b, tol=1e-10, sched=so)
+    rr = partition(A.rows, P)
+
+    def fn(r, D, st):
+        a, bb = rr[r], rr[r + 1]
+        rp, col, val = slab(A, a, bb)
+        dev = lambda v: torch.from_numpy(v).cuda()
+        M = g.gse_encode_dist(D, dev(rp), dev(col), dev(val), a, A.rows, stream=st.cuda_stream)
+        s = sched()
+        if s is None:  # fixed full precision on the GSE planes (the FP64 result, d <= 11)
+            s = g.fixed_schedule(3)
+        x, rep = g.gse_solve_gmres(M, dev(b[a:bb].copy()), tol=1e-10, sched=s,
+                                   stream=st.cuda_stream)
+        torch.cuda.synchronize()
+        M.close()
+        return x.cpu().numpy(), rep
+
+    outs = run_ranks(P, fn)
+    reps = [rep for _, rep in outs]
+    x = np.concatenate([xx for xx, _ in outs])
+    for rep in reps:
+        assert rep["iterations"] == reps[0]["iterations"]
+        assert rep["switch_iter"] == reps[0]["switch_iter"]
+    rep = reps[0]
+    assert rep["converged"], rep
+    assert abs(rep["iterations"] - r1["iterations"]) <= 2, (rep, r1)
+    assert abs(rep["iterations"] - ro.iterations) <= 2, (rep, ro)
+    F = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+    res = np.linalg.norm(b - O.spmv_fp64(F, x)) / np.linalg.norm(b)
+    assert res <= 1e-10 * 1.01

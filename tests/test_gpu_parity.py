@@ -141,6 +141,62 @@ def test_spmv_levels_parity(g, name):
         assert np.all(yg[bound == 0] == 0.0)
 
 
+@pytest.mark.parametrize("k", [1, 2, 8, 16, 64])
+def test_spmv_k_sweep_parity(g, k):
+    """strided-products kernel: register scale table (k <= 8, exponent span < 256) and the
+    shared-memory table (k = 16, 64) at all levels, FP64 and FP32 accumulation"""
+    A = gi.powerlaw_spd(20000, seed=11 + k)
+    M, R = enc_both(g, A, k)
+    assert M.info["spmv_mode"] == 0
+    x = gi.uniform_vec(A.cols, seed=5)
+    for L in (1, 2, 3):
+        yg = g.gse_spmv(M, x, segments=L)
+        yo = O.spmv_gse(R, x, L)
+        assert np.all(np.abs(yg - yo) <= spmv_bound(R, x, L, 1e-12)), L
+        yf = g.gse_spmv_f32acc(M, x.astype(np.float32), segments=L).astype(np.float64)
+        yo32 = O.spmv_gse(R, x.astype(np.float32).astype(np.float64), L)
+        bound = spmv_bound(R, x.astype(np.float32).astype(np.float64), L, 1e-5)
+        assert np.all(np.abs(yf - yo32) <= bound), L
+
+
+def short_rows_matrix():
+    """blocks of > 32 rows (rows of 0-3 entries) next to ordinary ones: the strided kernel's
+    lane-per-row fallback and the segmented path in one matrix"""
+    rng = np.random.default_rng(21)
+    lens = np.concatenate([rng.integers(0, 4, 3000), rng.integers(5, 40, 2000),
+                           rng.integers(1, 3, 2000), rng.integers(20, 64, 500)])
+    rows = lens.size
+    cols = 5000
+    rp = np.zeros(rows + 1, np.int64)
+    np.cumsum(lens, out=rp[1:])
+    col = np.concatenate([np.sort(rng.choice(cols, L, replace=False)) for L in lens]).astype(np.int32)
+    val = rng.uniform(-2, 2, rp[-1]) * np.ldexp(1.0, rng.integers(-6, 6, rp[-1]))
+    return gi.Csr(rows, cols, rp, col, val, "short_rows")
+
+
+@pytest.mark.parametrize("mode", ["sp", "auto"])
+def test_spmv_short_rows_and_sp_cg(g, mode, monkeypatch):
+    A = short_rows_matrix()
+    M, R = enc_both(g, A)
+    x = gi.uniform_vec(A.cols, seed=2)
+    for L in (1, 2, 3):
+        yg = g.gse_spmv(M, x, segments=L)
+        yo = O.spmv_gse(R, x, L)
+        bound = spmv_bound(R, x, L, 1e-12)
+        assert np.all(np.abs(yg - yo) <= bound), L
+        assert np.all(yg[bound == 0] == 0.0)
+    # CG through the strided kernel's fused dot (DOT variant) on an SPD stencil
+    if mode == "sp":
+        monkeypatch.setenv("GSE_SPMV_MODE", "sp")
+    B = gi.poisson3d(20, "varcoef")
+    Mb, Rb = enc_both(g, B)
+    assert (Mb.info["spmv_mode"] == 0) == (mode == "sp")
+    b = gi.ones_rhs(B)
+    _, rg = g.gse_solve_cg(Mb, b, tol=1e-10, sched=g.gse_default_schedule("cg", l=30, t=10, m=10))
+    _, ro = O.cg(Rb, b, tol=1e-10, sched=O.schedule("cg", l=30, t=10, m=10))
+    _cmp_reports(rg, ro)
+
+
 @pytest.mark.parametrize("name", ["poisson3d_40", "powerlaw_30k", "long_rows", "random_mixed"])
 def test_spmv_fp64_comparator_parity(g, name):
     A = MATS[name]()
