@@ -101,6 +101,16 @@ def _declare(L):
                                  _p(C.c_uint16), _p(i32), _p(i32), _p(i32), _p(C.c_uint32),
                                  _p(C.c_uint8), _p(C.c_uint16), _p(C.c_uint16),
                                  _p(C.c_uint32), _p(i64)]
+    L.orc_encode_csr_sampled.argtypes = [i64, i64, i64, _p(i64), _p(C.c_int32), _p(dbl), i32,
+                                         i64, C.c_uint64, _p(C.c_uint16), _p(i32), _p(i32),
+                                         _p(i32), _p(C.c_uint32), _p(C.c_uint8),
+                                         _p(C.c_uint16), _p(C.c_uint16), _p(C.c_uint32), _p(i64)]
+    L.orc_build_table_emax.argtypes = [_p(C.c_uint64), i32, i32, _p(C.c_uint16), _p(i32)]
+    L.orc_sample_z.argtypes = [C.c_uint64, i64]
+    L.orc_sample_z.restype = C.c_uint64
+    L.orc_sample_row.argtypes = [i64, i64, C.c_uint64, i64]
+    L.orc_sample_row.restype = i64
+    L.orc_sampled_histogram.argtypes = [i64, _p(i64), _p(dbl), i64, C.c_uint64, _p(C.c_uint64)]
     L.orc_spmv_fp64.argtypes = [i64, _p(i64), _p(C.c_int32), _p(dbl), _p(dbl), _p(dbl)]
     L.orc_spmv_gse.argtypes = [_p(OrcMatrix), i32, _p(dbl), _p(dbl)]
     L.orc_rsd.argtypes = [_p(dbl), i64]
@@ -168,6 +178,37 @@ def build_table(hist, k_max: int = 8):
     st = lib().orc_build_table(_ptr(h, C.c_uint64), k_max, _ptr(table, C.c_uint16), C.byref(n))
     if st != OK:
         raise OracleError(st, "build_table")
+    return table[: n.value].copy()
+
+
+def sample_row(rows: int, block_rows: int, seed: int, b: int) -> int:
+    """NEXT-3 (R27): the random row of row block b."""
+    return lib().orc_sample_row(rows, block_rows, seed, b)
+
+
+def sample_z(seed: int, b: int) -> int:
+    return lib().orc_sample_z(seed, b)
+
+
+def sampled_histogram(rows, row_ptr, val, block_rows: int, seed: int):
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    v = np.ascontiguousarray(val, dtype=np.float64)
+    hist = np.zeros(2048, dtype=np.uint64)
+    st = lib().orc_sampled_histogram(rows, _ptr(rp, C.c_int64), _ptr(v, C.c_double), block_rows,
+                                     seed, _ptr(hist, C.c_uint64))
+    if st != OK:
+        raise OracleError(st, "sampled_histogram")
+    return hist
+
+
+def build_table_emax(hist, k_max: int, e_max_true: int):
+    h = np.ascontiguousarray(hist, dtype=np.uint64)
+    table = np.zeros(64, dtype=np.uint16)
+    n = C.c_int()
+    st = lib().orc_build_table_emax(_ptr(h, C.c_uint64), k_max, e_max_true,
+                                    _ptr(table, C.c_uint16), C.byref(n))
+    if st != OK:
+        raise OracleError(st, "build_table_emax")
     return table[: n.value].copy()
 
 
@@ -335,7 +376,8 @@ def fp64_csr(rows, cols, row_ptr, col, val) -> Fp64Csr:
     return Fp64Csr(rows, cols, rp, c, v)
 
 
-def encode_csr(rows: int, cols: int, row_ptr, col, val, k_max: int = 8) -> GseCsr:
+def encode_csr(rows: int, cols: int, row_ptr, col, val, k_max: int = 8,
+               sample_block_rows: int = 0, seed: int = 0) -> GseCsr:
     rp, c, v = _csr_arrays(row_ptr, col, val)
     nnz = v.size
     table = np.zeros(64, dtype=np.uint16)
@@ -346,8 +388,9 @@ def encode_csr(rows: int, cols: int, row_ptr, col, val, k_max: int = 8) -> GseCs
     t1 = np.zeros(max(nnz, 1), np.uint16)
     t2 = np.zeros(max(nnz, 1), np.uint32)
     bad = C.c_int64()
-    st = lib().orc_encode_csr(rows, cols, nnz, _ptr(rp, C.c_int64), _ptr(c, C.c_int32),
-                              _ptr(v, C.c_double), k_max, _ptr(table, C.c_uint16),
+    st = lib().orc_encode_csr_sampled(rows, cols, nnz, _ptr(rp, C.c_int64), _ptr(c, C.c_int32),
+                              _ptr(v, C.c_double), k_max, sample_block_rows, seed,
+                              _ptr(table, C.c_uint16),
                               C.byref(tl), C.byref(eb), C.byref(inc), _ptr(col_ei, C.c_uint32),
                               _ptr(side, C.c_uint8), _ptr(head, C.c_uint16),
                               _ptr(t1, C.c_uint16), _ptr(t2, C.c_uint32), C.byref(bad))

@@ -77,7 +77,10 @@ static int cmp_count_desc_e_desc(const void* a, const void* b) {
   return ea > eb ? -1 : (ea < eb ? 1 : 0);
 }
 
-int orc_build_table(const uint64_t* hist, int k_max, uint16_t* table, int* table_len) {
+/* e_max_true >= 1: the exponent the max-exponent rule must cover (the TRUE maximum of all
+ * values when hist is a sample); 0: the largest exponent in hist. */
+int orc_build_table_emax(const uint64_t* hist, int k_max, int e_max_true, uint16_t* table,
+                         int* table_len) {
   int es[2048];
   int n = 0, e_max = 0;
   if (k_max < 1 || k_max > 64 || (k_max & (k_max - 1)) != 0) return ORC_ERR_INVALID_ARG;
@@ -87,7 +90,13 @@ int orc_build_table(const uint64_t* hist, int k_max, uint16_t* table, int* table
       e_max = e;
     }
   }
-  if (n == 0) return ORC_ERR_NO_VALUES; /* S:58 "no representable values" */
+  if (e_max_true > 0) e_max = e_max_true;
+  if (n == 0 && e_max == 0) return ORC_ERR_NO_VALUES; /* S:58 "no representable values" */
+  if (n == 0) { /* a sample without normal values: the forced entry alone */
+    table[0] = (uint16_t)(e_max + 1);
+    *table_len = 1;
+    return ORC_OK;
+  }
   g_sort_hist = hist;
   qsort(es, (size_t)n, sizeof(int), cmp_count_desc_e_desc);
   int take = n < k_max ? n : k_max;
@@ -96,6 +105,53 @@ int orc_build_table(const uint64_t* hist, int k_max, uint16_t* table, int* table
   if (!have_max) es[take - 1] = e_max;
   for (int i = 0; i < take; ++i) table[i] = (uint16_t)(es[i] + 1);
   *table_len = take;
+  return ORC_OK;
+}
+
+int orc_build_table(const uint64_t* hist, int k_max, uint16_t* table, int* table_len) {
+  return orc_build_table_emax(hist, k_max, 0, table, table_len);
+}
+
+/* ------------------------------------------------------------------------------------
+ * NEXT-3 -- sampled table extraction.  P:116 "the shared exponents can be calculated using
+ * sampling techniques. For instance, a sparse matrix is divided into several row blocks,
+ * and the exponents' distribution in a random row is calculated for each row block,
+ * serving as the exponents' distribution in that block"; one uniformly chosen
+ * row per contiguous block of block_rows rows, histogram fed to the table selection, the
+ * max-exponent rule on the TRUE global maximum (full scan), so every value stays
+ * representable.  The random row (R27; the paper names no generator): block b covers rows
+ * [b*B, min((b+1)*B, rows)) of length len_b, and its row is b*B + (z mod len_b) with z the
+ * SplitMix64 output for counter (b + 1) from the seed:
+ *   z = seed + (b + 1) * 0x9E3779B97F4A7C15;
+ *   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9;  z = (z ^ (z >> 27)) * 0x94D049BB133111EB;
+ *   z = z ^ (z >> 31)   (all mod 2^64).
+ * ------------------------------------------------------------------------------------ */
+uint64_t orc_sample_z(uint64_t seed, int64_t b) {
+  uint64_t z = seed + (uint64_t)(b + 1) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+int64_t orc_sample_row(int64_t rows, int64_t block_rows, uint64_t seed, int64_t b) {
+  int64_t r0 = b * block_rows;
+  int64_t len = rows - r0 < block_rows ? rows - r0 : block_rows;
+  return r0 + (int64_t)(orc_sample_z(seed, b) % (uint64_t)len);
+}
+
+/* histogram of the sampled rows' values (zero / subnormal / non-finite not counted) */
+int orc_sampled_histogram(int64_t rows, const int64_t* row_ptr, const double* val,
+                          int64_t block_rows, uint64_t seed, uint64_t* hist) {
+  if (block_rows < 1) return ORC_ERR_INVALID_ARG;
+  memset(hist, 0, 2048 * sizeof(uint64_t));
+  int64_t nblocks = (rows + block_rows - 1) / block_rows;
+  for (int64_t b = 0; b < nblocks; ++b) {
+    int64_t r = orc_sample_row(rows, block_rows, seed, b);
+    for (int64_t j = row_ptr[r]; j < row_ptr[r + 1]; ++j) {
+      unsigned e = (unsigned)((bits_of(val[j]) >> 52) & 0x7FF);
+      if (e >= 1 && e <= 2046) hist[e] += 1;
+    }
+  }
   return ORC_OK;
 }
 
@@ -231,6 +287,18 @@ int orc_encode_csr(int64_t rows, int64_t cols, int64_t nnz, const int64_t* row_p
                    int* table_len, int* ei_bits_out, int* ei_in_column, uint32_t* col_ei,
                    uint8_t* side_ei, uint16_t* head, uint16_t* tail1, uint32_t* tail2,
                    int64_t* bad_index) {
+  return orc_encode_csr_sampled(rows, cols, nnz, row_ptr, col, val, k_max, 0, 0, table,
+                                table_len, ei_bits_out, ei_in_column, col_ei, side_ei, head,
+                                tail1, tail2, bad_index);
+}
+
+/* sample_block_rows = 0: full histogram; >= 1: the sampled table of NEXT-3 (above) */
+int orc_encode_csr_sampled(int64_t rows, int64_t cols, int64_t nnz, const int64_t* row_ptr,
+                           const int32_t* col, const double* val, int k_max,
+                           int64_t sample_block_rows, uint64_t seed, uint16_t* table,
+                           int* table_len, int* ei_bits_out, int* ei_in_column,
+                           uint32_t* col_ei, uint8_t* side_ei, uint16_t* head,
+                           uint16_t* tail1, uint32_t* tail2, int64_t* bad_index) {
   *bad_index = -1;
   if (rows < 0 || cols < 0 || nnz < 0) return ORC_ERR_INVALID_ARG;
   if (row_ptr[0] != 0 || row_ptr[rows] != nnz) return ORC_ERR_INVALID_ARG;
@@ -249,7 +317,19 @@ int orc_encode_csr(int64_t rows, int64_t cols, int64_t nnz, const int64_t* row_p
     free(hist);
     return st;
   }
-  st = orc_build_table(hist, k_max, table, table_len);
+  if (sample_block_rows > 0 && rows > 0) {
+    int e_max_true = 0; /* true maximum from the full histogram */
+    for (int e = 1; e <= 2046; ++e)
+      if (hist[e] > 0) e_max_true = e;
+    if (e_max_true == 0) {
+      free(hist);
+      return ORC_ERR_NO_VALUES;
+    }
+    orc_sampled_histogram(rows, row_ptr, val, sample_block_rows, seed, hist);
+    st = orc_build_table_emax(hist, k_max, e_max_true, table, table_len);
+  } else {
+    st = orc_build_table(hist, k_max, table, table_len);
+  }
   free(hist);
   if (st != ORC_OK) return st;
   int eb = 0;

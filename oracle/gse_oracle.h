@@ -25,6 +25,12 @@
 int orc_exponent_histogram(int64_t nnz, const double* val, uint64_t* hist2048,
                            int64_t* n_zero, int64_t* first_nonfinite);
 int orc_build_table(const uint64_t* hist2048, int k_max, uint16_t* table, int* table_len);
+int orc_build_table_emax(const uint64_t* hist2048, int k_max, int e_max_true, uint16_t* table,
+                         int* table_len);
+uint64_t orc_sample_z(uint64_t seed, int64_t b);
+int64_t orc_sample_row(int64_t rows, int64_t block_rows, uint64_t seed, int64_t b);
+int orc_sampled_histogram(int64_t rows, const int64_t* row_ptr, const double* val,
+                          int64_t block_rows, uint64_t seed, uint64_t* hist2048);
 int orc_encode_value(double x, const uint16_t* table, int table_len, uint64_t* word, int* ei);
 void orc_segment(uint64_t word, uint16_t* head, uint16_t* tail1, uint32_t* tail2);
 uint64_t orc_assemble(uint16_t head, uint16_t tail1, uint32_t tail2, int level);
@@ -38,6 +44,12 @@ int orc_encode_csr(int64_t rows, int64_t cols, int64_t nnz, const int64_t* row_p
                    uint16_t* table /* k_max */, int* table_len, int* ei_bits, int* ei_in_column,
                    uint32_t* col_ei, uint8_t* side_ei, uint16_t* head, uint16_t* tail1,
                    uint32_t* tail2, int64_t* bad_index);
+int orc_encode_csr_sampled(int64_t rows, int64_t cols, int64_t nnz, const int64_t* row_ptr,
+                           const int32_t* col, const double* val, int k_max,
+                           int64_t sample_block_rows, uint64_t seed, uint16_t* table,
+                           int* table_len, int* ei_bits_out, int* ei_in_column,
+                           uint32_t* col_ei, uint8_t* side_ei, uint16_t* head,
+                           uint16_t* tail1, uint32_t* tail2, int64_t* bad_index);
 
 /* matrix as seen by the oracle solvers: either plain FP64 CSR (val != NULL) or GSE */
 typedef struct {
