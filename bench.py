@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-c3", action="store_true",
+                    help="skip the configs[2] power-law SpMV segment sweep")
     ap.add_argument("--cpu-iters", type=int, default=40,
                     help="oracle CG iterations in the bounded CPU sample")
     a = ap.parse_args()
@@ -331,14 +333,20 @@ def run_gse(args, world, rank, local, pg):
         line["solve"]["fp64_iterations"] = extra["cg_fp64_iters"]
         line["spmv_sweep"] = extra["spmv"]
         line["spmv_sweep_steady"] = extra["spmv_steady"]
+        st = extra["spmv_steady"]["L1"]
         line["roofline"] = {
             "bound": "hbm", "kernel": "k_spmv_rw<L=1> (level-1 GSE SpMV, row walk; the CG inner kernel)",
-            "achieved": dom["GBps"], "peak": hbm_peak, "unit": "GB/s",
-            "frac": dom["GBps"] / hbm_peak, "peak_source": peak_src,
+            "achieved": st["GBps"], "peak": hbm_peak, "unit": "GB/s",
+            "frac": st["GBps"] / hbm_peak, "peak_source": peak_src,
             "traffic": _profiled_traffic(), "algorithmic_bytes_per_launch": dom["bytes"],
-            "avg_launch_us": dom["us"],
-            "timing": "CUDA events per launch on the launching stream, L2 flushed before each "
-                      "(cold; spmv_sweep_steady has back-to-back launches as in the CG loop)"}
+            "avg_launch_us": st["us"],
+            "timing": "CUDA events on the launching stream around back-to-back launches (as in "
+                      "the CG loop: no flush between SpMVs), average per launch",
+            "cold": {"achieved": dom["GBps"], "frac": dom["GBps"] / hbm_peak,
+                     "avg_launch_us": dom["us"],
+                     "timing": "one launch between CUDA events, L2 flushed before it"}}
+    if rank == 0 and world == 1 and not args.no_c3 and not args.no_sweep:
+        line["spmv_sweep_c3"] = c3_sweep(args, dev, stream, flush, hbm_peak)
     print(json.dumps(line), flush=True)
 
 
@@ -466,6 +474,52 @@ def spmv_and_cg_sweep(args, A, rp, col, val, b, dev, stream, flush, hbm_peak):
     F.close()
     return {"spmv": out, "spmv_steady": steady, "cg_gse_ms": t_gse, "cg_fp64_ms": t_f64,
             "cg_fp64_iters": rf["iterations"], "encode_ms": t_enc, "cg_half": half_cg}
+
+
+def c3_sweep(args, dev, stream, flush, hbm_peak):
+    """configs[2]: the power-law SPD (10M rows, ~200M nnz; recipe in DESIGN.md) SpMV segment
+    sweep -- the strided-products kernel -- per level and accumulation, the FP64-CSR
+    comparator and the FP16 / BF16 baselines.  Cold launches (L2 flushed before each)."""
+    import torch
+    import gse_inputs as gi
+    import paper_2411_04686_b200 as g
+    t0 = time.time()
+    A = gi.powerlaw_spd(10_000_000, seed=42)
+    gen_s = time.time() - t0
+    n, nnz = A.rows, A.nnz
+    rp = torch.from_numpy(A.row_ptr.astype(np.int32)).to(dev)
+    col = torch.from_numpy(A.col).to(dev)
+    val = torch.from_numpy(A.val).to(dev)
+    del A
+    x = torch.from_numpy(gi.uniform_vec(n, seed=7)).to(dev)
+    y = torch.empty(n, dtype=torch.float64, device=dev)
+    x32, y32 = x.float(), torch.empty(n, dtype=torch.float32, device=dev)
+    out = {"n": n, "nnz": int(nnz), "generate_s": round(gen_s, 1)}
+
+    def rec(key, fn, byt):
+        fn()
+        t = statistics.mean(time_cuda(fn, 10, stream, flush)) * 1e-3
+        out[key] = {"us": round(t * 1e6, 1), "GBps": round(byt / t / 1e9, 1),
+                    "GFLOPs": round(2 * nnz / t / 1e9, 1), "frac_hbm": round(byt / t / 1e9 / hbm_peak, 3)}
+
+    M = g.gse_encode(rp, col, val, n, n)
+    rows_b = 4 * (n + 1)
+    for L, s_l in ((1, 2), (2, 4), (3, 8)):
+        rec(f"L{L}", lambda: g.gse_spmv(M, x, y, segments=L), nnz * (4 + s_l) + rows_b + 16 * n)
+        rec(f"L{L}_f32acc", lambda: g.gse_spmv_f32acc(M, x32, y32, segments=L),
+            nnz * (4 + s_l) + rows_b + 8 * n)
+    out["spmv_mode"] = "strided products" if M.info["spmv_mode"] == 0 else "row walk"
+    M.close()
+    F = g.gse_fp64_matrix(rp, col, val, n, n)
+    rec("fp64_csr", lambda: g.gse_spmv(F, x, y, segments=3), nnz * 12 + rows_b + 16 * n)
+    F.close()
+    for k in ("fp16", "bf16"):
+        H = g.gse_half_matrix(rp, col, val, n, n, kind=k)
+        rec(k, lambda: g.gse_spmv(H, x, y, segments=3), nnz * 6 + rows_b + 16 * n)
+        H.close()
+    del rp, col, val
+    torch.cuda.empty_cache()
+    return out
 
 
 def e2e_measure(args, A, b_h, dev, stream, encode, r0, n_glob):

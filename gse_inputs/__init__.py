@@ -193,7 +193,8 @@ def powerlaw_spd(n: int, seed: int = 42, xm: float = 4.3, max_half: int = 20000,
     dst = src + delta
     keep = dst < n
     src, dst = src[keep], dst[keep]
-    key = np.unique(src * n + dst)
+    key = np.sort(src * n + dst)  # sorted unique (np.unique's hash path is ~6x slower here)
+    key = key[np.concatenate(([True], key[1:] != key[:-1]))]
     src, dst = key // n, key % n
     del key
     m = src.size

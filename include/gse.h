@@ -76,8 +76,13 @@ typedef struct {
 typedef struct {
   int k_max;      /* number of shared exponents k: power of two in [1, 64]; default 8 */
   int device;     /* CUDA device ordinal for the matrix; -1 = infer from device pointers, else 0 */
-  int64_t sample_block_rows; /* reserved (sampling extraction P:116, NEXT-3); must be 0      */
-  uint64_t seed;             /* reserved for sampling                                      */
+  int64_t sample_block_rows; /* 0: table from the full exponent histogram; B >= 1: from one
+                              * random row per block of B rows ("calculated using
+                              * sampling techniques"; NEXT-3), the max-exponent rule
+                              * still on the true maximum of all values (so every value stays
+                              * representable).  Single-GPU gse_encode only.                */
+  uint64_t seed;             /* sampling: row of block b = b*B + splitmix64(seed, b+1) mod
+                              * len_b (R27: SplitMix64 output for counter b+1)              */
 } gse_encode_opts;
 
 typedef enum {

@@ -220,13 +220,15 @@ def _csr(rows, cols, row_ptr, col_idx, values):
 
 
 def gse_encode(row_ptr, col_idx, values, rows: int, cols: int, k_max: int = 8,
-               device: int | None = None, stream=None) -> Matrix:
-    """a1-a3: build the GSE-SEM matrix (host or device CSR input; see include/gse.h)."""
+               device: int | None = None, stream=None, sample_block_rows: int = 0,
+               seed: int = 0) -> Matrix:
+    """a1-a3: build the GSE-SEM matrix (host or device CSR input; see include/gse.h).
+    sample_block_rows > 0: table from one random row per row block (NEXT-3)."""
     A = _csr(rows, cols, row_ptr, col_idx, values)
     dev = _device_of(values, col_idx, row_ptr) if device is None else device
     if dev < 0:
         dev = _current_device()
-    opts = EncodeOpts(k_max, dev, 0, 0)
+    opts = EncodeOpts(k_max, dev, sample_block_rows, seed)
     out = C.c_void_p()
     _check(_lib.gse_encode(C.byref(A), C.byref(opts), C.byref(out),
                            _stream(values, col_idx, row_ptr, stream=stream)), "gse_encode")

@@ -205,7 +205,8 @@ static void destroy_matrix(Matrix& M) {
 
 gse_status create_from_csr(const gse_csr_f64* A, int kind, int k_max, int device,
                            gse_matrix* out, cudaStream_t s, Matrix** mout, Comm* comm,
-                           const int32_t* local_col_host) {
+                           const int32_t* local_col_host, int64_t sample_block_rows,
+                           uint64_t sample_seed) {
   gse_status rc = check_csr(A);
   if (rc != GSE_OK) return rc;
   if (!out) {
@@ -235,7 +236,8 @@ gse_status create_from_csr(const gse_csr_f64* A, int kind, int k_max, int device
   M.nnz = A->nnz;
   M.k_max = k_max;
   if (kind == GSE_KIND_GSE)
-    rc = encode_matrix(M, *A, rp, A->row_ptr_64, col, val, s, comm);
+    rc = encode_matrix(M, *A, rp, A->row_ptr_64, col, val, s, comm, sample_block_rows,
+                       sample_seed);
   else
     rc = fp64_matrix(M, rp, A->row_ptr_64, col, val, s, kind);
   if (rc == GSE_OK) rc = st.finish();
@@ -328,12 +330,12 @@ gse_status gse_encode(const gse_csr_f64* A, const gse_encode_opts* opts, gse_mat
     set_error("k_max must be a power of two in [1, 64]");
     return GSE_ERR_INVALID_ARG;
   }
-  if (o.sample_block_rows != 0) {
-    set_error("sampled table extraction is not implemented (sample_block_rows must be 0)");
+  if (o.sample_block_rows < 0) {
+    set_error("sample_block_rows must be >= 0 (0 = full histogram)");
     return GSE_ERR_INVALID_ARG;
   }
   return create_from_csr(A, GSE_KIND_GSE, o.k_max, o.device, out, (cudaStream_t)stream, nullptr,
-                         nullptr, nullptr);
+                         nullptr, nullptr, o.sample_block_rows, o.seed);
 }
 
 gse_status gse_fp64_matrix(const gse_csr_f64* A, int device, gse_matrix* out, void* stream) {

@@ -536,6 +536,10 @@ gse_status gse_dist_plan(int64_t nnz, const int32_t* col, int64_t row_begin, int
 gse_status gse_encode_dist(gse_dist Dh, const gse_csr_f64* A, int64_t row_begin,
                            int64_t global_rows, const gse_encode_opts* opts, gse_matrix* out,
                            void* stream) {
+  if (opts && opts->sample_block_rows != 0) {  // (checked before any collective)
+    set_error("sampled tables (sample_block_rows > 0) are single-GPU only");
+    return GSE_ERR_INVALID_ARG;
+  }
   if (!Dh || !A || !out) {
     set_error("NULL argument");
     return GSE_ERR_INVALID_ARG;

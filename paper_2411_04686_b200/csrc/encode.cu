@@ -32,6 +32,7 @@ struct EncodeStatus {
   int e_max;
   unsigned short table[64];
   unsigned int lut[2048];  // ei | d << 8 ; 0xFFFFFFFF = no entry above e
+  unsigned long long shist[2048];  // sampled histogram (NEXT-3), selection input if sampled
 };
 
 // ------------------------------------------------------------------ a1 histogram
@@ -77,6 +78,35 @@ __global__ void __launch_bounds__(512) k_hist(const double* __restrict__ val, in
   }
 }
 
+// ------------------------------------------------------------------ NEXT-3 sampled histogram
+// P:116 "a sparse matrix is divided into several row blocks, and the exponents'
+// distribution in a random row is calculated for each row block".  Block b =
+// rows [b B, min((b+1) B, rows)); its row = b B + z mod len, z = SplitMix64 output for
+// counter b + 1 from the seed (R27).  One thread per block; the max-exponent rule keeps
+// the TRUE e_max from the full histogram (k_select), so every value stays representable.
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long seed, long long b) {
+  unsigned long long z = seed + (unsigned long long)(b + 1) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_hist_sampled(const uint32_t* __restrict__ rp, const double* __restrict__ val,
+                               int64_t rows, int64_t nnz, int64_t B, unsigned long long seed,
+                               EncodeStatus* __restrict__ st) {
+  const int64_t nb = (rows + B - 1) / B;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += stride) {
+    const int64_t r0 = b * B, len = rows - r0 < B ? rows - r0 : B;
+    const int64_t r = r0 + (int64_t)(splitmix64(seed, b) % (unsigned long long)len);
+    const uint32_t j1 = (int64_t)rp[r + 1] < nnz ? rp[r + 1] : (uint32_t)nnz;  // (bad structure
+    for (uint32_t j = rp[r]; j < j1; ++j) {                                      //  is reported later)
+      const unsigned e = (unsigned)((unsigned long long)__double_as_longlong(val[j]) >> 52) & 0x7FFu;
+      if (e >= 1u && e <= 2046u) atomicAdd(&st->shist[e], 1ull);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ a2 table + LUT
 __device__ unsigned long long block_max_u64(unsigned long long v, unsigned long long* red) {
   for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
@@ -93,19 +123,21 @@ __device__ unsigned long long block_max_u64(unsigned long long v, unsigned long 
   return red[32];
 }
 
-__global__ void __launch_bounds__(1024) k_select(EncodeStatus* __restrict__ st, int k_max) {
+// sampled: the selection counts come from st->shist (NEXT-3); e_max always from the full
+// histogram st->hist
+__global__ void __launch_bounds__(1024) k_select(EncodeStatus* __restrict__ st, int k_max,
+                                                 int sampled) {
   __shared__ unsigned long long key[2048];
   __shared__ unsigned long long red[33];
   __shared__ int sel[64];
   unsigned long long mloc = 0, nd = 0;
   for (int e = threadIdx.x; e < 2048; e += blockDim.x) {
-    unsigned long long c = (e >= 1 && e <= 2046) ? st->hist[e] : 0ull;
+    const bool ok = e >= 1 && e <= 2046;
+    unsigned long long c = ok ? (sampled ? st->shist[e] : st->hist[e]) : 0ull;
     // key orders by count desc, then exponent desc (R4); unique because e is in the key
     key[e] = c ? ((c << 11) | (unsigned long long)e) : 0ull;
-    if (c) {
-      mloc = max(mloc, (unsigned long long)e);
-      ++nd;
-    }
+    if (c) ++nd;
+    if (ok && st->hist[e]) mloc = max(mloc, (unsigned long long)e);
   }
   const unsigned long long e_max = block_max_u64(mloc, red);
   // count distinct exponents (sum via max-reduction of per-thread prefix is overkill:
@@ -116,8 +148,13 @@ __global__ void __launch_bounds__(1024) k_select(EncodeStatus* __restrict__ st, 
   if (nd) atomicAdd(&s_nd, (unsigned)nd);
   __syncthreads();
   const int n_distinct = (int)s_nd;
-  const int take = n_distinct < k_max ? n_distinct : k_max;
-  for (int k = 0; k < take; ++k) {
+  int take = n_distinct < k_max ? n_distinct : k_max;
+  if (take == 0 && e_max > 0) {  // a sample without normal values: the forced entry alone
+    take = 1;
+    if (threadIdx.x == 0) sel[0] = (int)e_max;
+    __syncthreads();
+  }
+  for (int k = 0; k < (n_distinct < take ? n_distinct : take); ++k) {
     unsigned long long loc = 0;
     for (int e = threadIdx.x; e < 2048; e += blockDim.x) loc = max(loc, key[e]);
     unsigned long long best = block_max_u64(loc, red);
@@ -450,7 +487,8 @@ static std::string row_col_of(const void* d_row_ptr, int rp64, const int32_t* d_
 }
 
 gse_status encode_matrix(Matrix& M, const gse_csr_f64& A, const void* d_row_ptr, int rp64,
-                         const int32_t* d_col, const double* d_val, cudaStream_t s, Comm* comm) {
+                         const int32_t* d_col, const double* d_val, cudaStream_t s, Comm* comm,
+                         int64_t sample_block_rows, uint64_t sample_seed) {
   M.kind = GSE_KIND_GSE;
   int eb = 0;
   while ((1 << eb) < M.k_max) ++eb;
@@ -479,7 +517,15 @@ gse_status encode_matrix(Matrix& M, const gse_csr_f64& A, const void* d_row_ptr,
     rc = comm_allreduce_u64(comm, st->hist, 2048 + 1, s);
     if (rc != GSE_OK) return rc;
   }
-  k_select<<<1, 1024, 0, s>>>(st, M.k_max);
+  const int sampled = (sample_block_rows > 0 && M.rows > 0) ? 1 : 0;
+  if (sampled) {
+    const int64_t nb = (M.rows + sample_block_rows - 1) / sample_block_rows;
+    k_hist_sampled<<<grid_for(nb, 256, M.device), 256, 0, s>>>(M.row_ptr, d_val, M.rows,
+                                                               M.nnz, sample_block_rows,
+                                                               sample_seed, st);
+    GSE_CUDA_TRY(cudaGetLastError());
+  }
+  k_select<<<1, 1024, 0, s>>>(st, M.k_max, sampled);
   GSE_CUDA_TRY(cudaGetLastError());
 
   // read back the table / status (one sync, the table is needed on the host for the

@@ -157,9 +157,11 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 // ---------------------------------------------------------------- kernels (launchers)
 // encode.cu
 gse_status build_partition(Matrix& M, cudaStream_t s);
+// sample_block_rows > 0: table from one sampled row per row block (NEXT-3)
 gse_status encode_matrix(Matrix& M, const gse_csr_f64& A, const void* d_row_ptr, int rp64,
                          const int32_t* d_col, const double* d_val, cudaStream_t s,
-                         Comm* comm = nullptr);
+                         Comm* comm = nullptr, int64_t sample_block_rows = 0,
+                         uint64_t sample_seed = 0);
 // kind: GSE_KIND_FP64 (values copied) or GSE_KIND_FP16 / GSE_KIND_BF16 (RNE to 16 bits, R26)
 gse_status fp64_matrix(Matrix& M, const void* d_row_ptr, int rp64, const int32_t* d_col,
                        const double* d_val, cudaStream_t s, int kind = GSE_KIND_FP64);
@@ -198,7 +200,8 @@ int64_t dist_n_local(const Matrix& M);
 void free_dist(Matrix& M);
 gse_status create_from_csr(const gse_csr_f64* A, int kind, int k_max, int device,
                            gse_matrix* out, cudaStream_t s, Matrix** mout, Comm* comm,
-                           const int32_t* local_col_host);
+                           const int32_t* local_col_host, int64_t sample_block_rows = 0,
+                           uint64_t sample_seed = 0);
 
 }  // namespace gse
 

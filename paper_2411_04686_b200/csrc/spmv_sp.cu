@@ -64,8 +64,11 @@ __device__ __forceinline__ void products(const SpmvParams<T>& p, const long long
   }
 }
 
+#ifndef GSE_SP_MINB  // resident CTAs per SM the register budget is sized for (A/B knob)
+#define GSE_SP_MINB 4
+#endif
 template <int L, bool SIDE, bool DOT, bool FAST, class T>
-__global__ void __launch_bounds__(SPMV_THREADS, 3) k_spmv_sp(const SpmvParams<T> p) {
+__global__ void __launch_bounds__(SPMV_THREADS, GSE_SP_MINB) k_spmv_sp(const SpmvParams<T> p) {
   __shared__ __align__(16) T wprod[SPMV_WARPS][WTILE];
   __shared__ long long sd64[64];
   __shared__ int sd32[64];
@@ -109,6 +112,14 @@ __global__ void __launch_bounds__(SPMV_THREADS, 3) k_spmv_sp(const SpmvParams<T>
       }
     } else {
       T v[EPL];
+      // row bounds (and x of the rows, for the fused dot) of a block of < 32 rows loaded
+      // up front, one per lane, so they travel with the plane loads instead of costing a
+      // dependent round trip after the products (the kernel is gather-latency-bound)
+      const bool pre = nrows < 32;
+      uint32_t rpl = 0;
+      double xr = 0.0;
+      if (pre && (uint32_t)lane <= nrows) rpl = p.row_ptr[r0 + lane];
+      if (DOT && pre && (uint32_t)lane < nrows) xr = (double)p.x[r0 + lane];
       products<L, SIDE, FAST, T>(p, sd64, sd32, sc64, sc32, s + lane, e, v);
 #pragma unroll
       for (int k = 0; k < EPL; ++k) wp[lane + 32 * k] = v[k];
@@ -122,14 +133,25 @@ __global__ void __launch_bounds__(SPMV_THREADS, 3) k_spmv_sp(const SpmvParams<T>
       for (uint32_t base_r = 0; base_r < nrows; base_r += rpw) {
         const uint32_t rr = base_r + grp;
         T sum = 0;
+        uint32_t ra, rb;
+        double xrow = 0.0;
+        if (pre) {  // (uniform branch) bounds from the lanes that loaded them
+          ra = __shfl_sync(0xFFFFFFFFu, rpl, rr & 31u);
+          rb = __shfl_sync(0xFFFFFFFFu, rpl, (rr + 1u) & 31u);
+          if (DOT) xrow = __shfl_sync(0xFFFFFFFFu, xr, rr & 31u);
+        }
         if (rr < nrows) {
-          const uint32_t ra = p.row_ptr[r0 + rr], rb = p.row_ptr[r0 + rr + 1];
+          if (!pre) {
+            ra = p.row_ptr[r0 + rr];
+            rb = p.row_ptr[r0 + rr + 1];
+            if (DOT) xrow = (double)p.x[r0 + rr];
+          }
           for (uint32_t j = ra - s + sub; j < rb - s; j += lpr) sum += wp[j];
         }
         for (uint32_t o = lpr >> 1; o > 0; o >>= 1) sum += __shfl_down_sync(0xFFFFFFFFu, sum, o, lpr);
         if (rr < nrows && sub == 0) {
           p.y[r0 + rr] = sum;
-          if (DOT) dacc += (double)p.x[r0 + rr] * (double)sum;
+          if (DOT) dacc += xrow * (double)sum;
         }
       }
       __syncwarp();

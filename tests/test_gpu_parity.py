@@ -436,3 +436,41 @@ def test_solver_x0_and_host_device_paths(g):
     assert np.array_equal(xh, xd.cpu().numpy())  # deterministic reductions
     xo, ro = O.cg(R, b, x0=x0, tol=1e-10, sched=O.fixed_schedule(3))
     _cmp_reports(rh, ro)
+
+
+# ------------------------------------------------------------------ NEXT-3 sampled tables
+@pytest.mark.parametrize("B,seed,k", [(1, 0, 8), (16, 42, 8), (64, 7, 4), (1000, 3, 16),
+                                      (100000, 9, 8)])
+def test_encode_sampled_bit_exact(g, B, seed, k):
+    """P:116 / S:63-71: one SplitMix64-chosen row per block of B rows (R27) -> the same table
+    and planes as the oracle, bit for bit (B = 1 equals the full table; B >= rows samples
+    one row for the whole matrix)"""
+    A = gi.powerlaw_spd(30000, seed=B % 97)
+    M = g.gse_encode(A.row_ptr, A.col, A.val, A.rows, A.cols, k_max=k, sample_block_rows=B,
+                     seed=seed)
+    R = O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val, k, sample_block_rows=B, seed=seed)
+    P = g.gse_matrix_copy_planes(M)
+    assert list(P["table"]) == list(R.table)
+    for key in ("col_ei", "head", "tail1", "tail2"):
+        assert np.array_equal(P[key], getattr(R, key)), key
+    if B == 1:
+        assert list(P["table"]) == list(O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val, k).table)
+    x = gi.uniform_vec(A.cols, seed=1)
+    for L in (1, 3):
+        yg = g.gse_spmv(M, x, segments=L)
+        assert np.all(np.abs(yg - O.spmv_gse(R, x, L)) <= spmv_bound(R, x, L, 1e-12))
+
+
+def test_encode_sampled_unsampled_max_and_errors(g):
+    n = 64
+    rng = np.random.default_rng(4)
+    d = np.diag(rng.uniform(1, 2, n))
+    r_s = O.sample_row(n, n, 11, 0)
+    d[(r_s + 5) % n, (r_s + 6) % n] = 2.0 ** 40  # never sampled
+    A = gi.from_dense(d)
+    M = g.gse_encode(A.row_ptr, A.col, A.val, n, n, k_max=2, sample_block_rows=n, seed=11)
+    R = O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val, 2, sample_block_rows=n, seed=11)
+    assert list(M.info["table"]) == list(R.table) and max(R.table) == 1023 + 40 + 1
+    assert np.array_equal(g.gse_decode(M, 3), O.decode_all(R, 3))
+    with pytest.raises(g.GseError):
+        g.gse_encode(A.row_ptr, A.col, A.val, n, n, sample_block_rows=-1)
