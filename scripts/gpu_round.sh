@@ -15,4 +15,8 @@ GSE_NO_GRAPH=1 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read
 # full capture of the dominant kernel (level-1 SpMV of the CG: DOT variant) + levels 2/3
 PROF_CG_ITERS=4 GSE_NO_GRAPH=1 timeout 900 ncu --set full --clock-control none --import-source on \
   -k regex:k_spmv -c 5 -o gpurun_out/prof_$TAG python scripts/prof_spmv.py > gpurun_out/prof_$TAG.log 2>&1
-echo done
+echo done-c2
+# the strided-products kernel on configs[2] (power-law, 10M rows)
+PROF_MAT=powerlaw PROF_N=10000000 PROF_CG_ITERS=1 timeout 900 ncu --set full --clock-control none --import-source on \
+  -k regex:k_spmv_sp -c 4 -o gpurun_out/prof_c3_$TAG python scripts/prof_spmv.py > gpurun_out/prof_c3_$TAG.log 2>&1
+echo done-c3

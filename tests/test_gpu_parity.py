@@ -474,3 +474,67 @@ def test_encode_sampled_unsampled_max_and_errors(g):
     assert np.array_equal(g.gse_decode(M, 3), O.decode_all(R, 3))
     with pytest.raises(g.GseError):
         g.gse_encode(A.row_ptr, A.col, A.val, n, n, sample_block_rows=-1)
+
+
+def _sampled_rows_parity(g, A, x, n_rows=3000, seed=0, fp32=False, fp64_too=False):
+    """GPU SpMV at every level vs the oracle on sampled rows (sub-CSR of those rows, encoded
+    by the oracle with the full matrix's table); planes bit-exact in full"""
+    dev = lambda a: torch.from_numpy(a).cuda()
+    M = g.gse_encode(dev(A.row_ptr.astype(np.int32)), dev(A.col), dev(A.val), A.rows, A.cols)
+    R = O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+    P = g.gse_matrix_copy_planes(M)
+    assert list(P["table"]) == list(R.table)
+    for k in ("col_ei", "head", "tail1", "tail2"):
+        assert np.array_equal(P[k], getattr(R, k)), k
+    del P
+    rng = np.random.default_rng(seed)
+    rows = np.unique(np.concatenate([rng.integers(0, A.rows, n_rows), [0, A.rows - 1]]))
+    sel = np.concatenate([np.arange(A.row_ptr[r], A.row_ptr[r + 1]) for r in rows])
+    rp = np.zeros(rows.size + 1, np.int64)
+    np.cumsum(A.row_ptr[rows + 1] - A.row_ptr[rows], out=rp[1:])
+    sub = O.GseCsr(rows.size, A.cols, sel.size, rp, R.col_ei[sel].copy(), None,
+                   R.head[sel].copy(), R.tail1[sel].copy(), R.tail2[sel].copy(), R.table,
+                   R.ei_bits, R.ei_in_column)
+    xt = dev(x)
+    for L in (1, 2, 3):
+        yg = g.gse_spmv(M, xt, segments=L).cpu().numpy()[rows]
+        assert np.all(np.abs(yg - O.spmv_gse(sub, x, L)) <= spmv_bound(sub, x, L, 1e-12)), L
+        if fp32:
+            x32 = x.astype(np.float32)
+            yf = g.gse_spmv_f32acc(M, dev(x32), segments=L).cpu().numpy()[rows].astype(np.float64)
+            x64 = x32.astype(np.float64)
+            assert np.all(np.abs(yf - O.spmv_gse(sub, x64, L)) <= spmv_bound(sub, x64, L, 1e-5)), L
+    if fp64_too:
+        F = g.gse_fp64_matrix(dev(A.row_ptr.astype(np.int32)), dev(A.col), dev(A.val), A.rows, A.cols)
+        yg = g.gse_spmv(F, xt, segments=3).cpu().numpy()[rows]
+        Fs = O.fp64_csr(rows.size, A.cols, rp, A.col[sel], A.val[sel])
+        Fa = O.fp64_csr(rows.size, A.cols, rp, A.col[sel], np.abs(A.val[sel]))
+        assert np.all(np.abs(yg - O.spmv_fp64(Fs, x)) <= 1e-12 * O.spmv_fp64(Fa, np.abs(x)))
+    return M
+
+
+def test_spmv_full_size_c3_sampled(g):
+    """configs[2] (power-law SPD, 10M rows, ~200M nnz) at full size through the strided-
+    products kernel bench.py times: planes bit-exact, sampled rows at every level, FP32
+    accumulation and the FP64-CSR comparator"""
+    O.set_threads(0)
+    A = gi.powerlaw_spd(10_000_000, seed=42)
+    M = _sampled_rows_parity(g, A, gi.uniform_vec(A.cols, seed=7), fp32=True, fp64_too=True)
+    assert M.info["spmv_mode"] == 0
+
+
+def test_spmv_full_size_c4_sampled_and_gmres(g):
+    """configs[3] (conv-diff 256^3, 16.8M rows) at full size: sampled-row SpMV parity, then a
+    stepped GMRES(30) solve to 1e-10 whose true residual is checked with the oracle's FP64
+    SpMV (the oracle GMRES itself is out of reach at this size)"""
+    O.set_threads(0)
+    A = gi.convdiff3d(256)
+    M = _sampled_rows_parity(g, A, gi.uniform_vec(A.cols, seed=3))
+    assert M.info["spmv_mode"] == 1
+    b = gi.ones_rhs(A)
+    x, rep = g.gse_solve_gmres(M, torch.from_numpy(b).cuda(), tol=1e-10,
+                               sched=g.gse_default_schedule("gmres", l=300, t=100, m=100))
+    assert rep["converged"] and rep["n_switches"] >= 1
+    F = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+    res = np.linalg.norm(b - O.spmv_fp64(F, x.cpu().numpy())) / np.linalg.norm(b)
+    assert res <= 1e-10 * 1.01 and abs(res - rep["rel_residual_true"]) <= 1e-3 * res
