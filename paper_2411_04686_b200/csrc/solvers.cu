@@ -524,44 +524,6 @@ __global__ void __launch_bounds__(256, 4) k_gm_scale(const SolveCtrl* __restrict
   GRID_LOOP(i, n) dst[i] = src[i] / den;
 }
 
-// L2 residency for the MGS passes over long vectors (per-step kernels): w is read and
-// written by every pass, the basis vectors once or twice, so w's lines are marked
-// evict_last (a GSE_GM_KEEP fraction of them: at 256^3 w is 134 MB, the L2 126 MB) and the
-// basis reads evict_first.  GSE_GM_KEEP = 0 compiles plain accesses (A/B knob).
-#ifndef GSE_GM_KEEP
-#define GSE_GM_KEEP 0
-#endif
-__device__ __forceinline__ uint64_t pol_keep() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_last.L2::evict_unchanged.b64 %0, %1;"
-      : "=l"(p)
-      : "f"((float)GSE_GM_KEEP));
-  return p;
-}
-__device__ __forceinline__ uint64_t pol_stream() {
-  uint64_t p;
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ double2 ld2(const double2* a, uint64_t pol) {
-  double2 v;
-  if (GSE_GM_KEEP > 0)
-    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-                 : "=d"(v.x), "=d"(v.y)
-                 : "l"(a), "l"(pol));
-  else
-    v = *a;
-  return v;
-}
-__device__ __forceinline__ void st2(double2* a, double2 v, uint64_t pol) {
-  if (GSE_GM_KEEP > 0)
-    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(a), "d"(v.x), "d"(v.y),
-                 "l"(pol)
-                 : "memory");
-  else
-    *a = v;
-}
-
 // MGS step i of inner iteration j: (i > 0) w -= H[i-1][j] v_{i-1}; H[i][j] = w . v_i
 __global__ void __launch_bounds__(256, 4) k_gm_mgs(SolveCtrl* __restrict__ c, double* __restrict__ w,
                                                 const double* __restrict__ V, int64_t n, int i,
@@ -583,16 +545,15 @@ __global__ void __launch_bounds__(256, 4) k_gm_mgs(SolveCtrl* __restrict__ c, do
     double2* w2 = reinterpret_cast<double2*>(w);
     const double2* vi2 = reinterpret_cast<const double2*>(vi);
     const double2* vp2 = reinterpret_cast<const double2*>(vp);
-    const uint64_t pk = pol_keep(), ps = pol_stream();
     for (int64_t q = t0; q < n2; q += 2 * stride) {
       double2 wv[2], a[2], bp[2];
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         const int64_t e = q + k * stride;
         if (e < n2) {
-          wv[k] = ld2(w2 + e, pk);
-          a[k] = vi2[e];  // v_i is read again by the next pass (subtraction): default policy
-          if (i > 0) bp[k] = ld2(vp2 + e, ps);  // last use of v_{i-1} in this inner step
+          wv[k] = w2[e];
+          a[k] = vi2[e];
+          if (i > 0) bp[k] = vp2[e];
         }
       }
 #pragma unroll
@@ -602,7 +563,7 @@ __global__ void __launch_bounds__(256, 4) k_gm_mgs(SolveCtrl* __restrict__ c, do
           if (i > 0) {
             wv[k].x = __dsub_rn(wv[k].x, __dmul_rn(h, bp[k].x));
             wv[k].y = __dsub_rn(wv[k].y, __dmul_rn(h, bp[k].y));
-            st2(w2 + e, wv[k], pk);
+            w2[e] = wv[k];
           }
           acc = __dadd_rn(acc, __dmul_rn(wv[k].x, a[k].x));
           acc = __dadd_rn(acc, __dmul_rn(wv[k].y, a[k].y));
@@ -831,15 +792,14 @@ __global__ void __launch_bounds__(256, 4) k_gm_last(SolveCtrl* __restrict__ c, d
     const int64_t n2 = n >> 1, stride = (int64_t)gridDim.x * blockDim.x;
     double2* w2 = reinterpret_cast<double2*>(w);
     const double2* vj2 = reinterpret_cast<const double2*>(vj);
-    const uint64_t pk = pol_keep(), ps = pol_stream();
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n2; q += 2 * stride) {
       double2 wv[2], a[2];
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         const int64_t e = q + k * stride;
         if (e < n2) {
-          wv[k] = ld2(w2 + e, pk);
-          a[k] = ld2(vj2 + e, ps);
+          wv[k] = w2[e];
+          a[k] = vj2[e];
         }
       }
 #pragma unroll
@@ -848,7 +808,7 @@ __global__ void __launch_bounds__(256, 4) k_gm_last(SolveCtrl* __restrict__ c, d
         if (e < n2) {
           wv[k].x = __dsub_rn(wv[k].x, __dmul_rn(h, a[k].x));
           wv[k].y = __dsub_rn(wv[k].y, __dmul_rn(h, a[k].y));
-          st2(w2 + e, wv[k], pk);
+          w2[e] = wv[k];
           acc = __dadd_rn(acc, __dmul_rn(wv[k].x, wv[k].x));
           acc = __dadd_rn(acc, __dmul_rn(wv[k].y, wv[k].y));
         }

@@ -13,6 +13,10 @@
 //    shuffle tree.
 #include "spmv_common.cuh"
 
+#ifndef GSE_SP_REGTAB  // A/B knob: scales from a packed register table instead of smem
+#define GSE_SP_REGTAB 0
+#endif
+
 namespace gse {
 
 template <int L, bool SIDE, bool FAST, class T>
@@ -56,6 +60,11 @@ __device__ __forceinline__ void products(const SpmvParams<T>& p, const long long
       out[k] = (T)(half_value<L>(h[k]) * (double)xv[k]);
     } else {
       if constexpr (!SIDE) ei[k] = __funnelshift_rc(c[k], 0u, p.ei_shift);
+#if GSE_SP_REGTAB
+      if (FAST && p.regtab)  // (uniform) scale from the packed register table
+        out[k] = dec_reg<L, T>(p, h[k], t1[k], t2[k], ei[k]) * xv[k];
+      else
+#endif
       if constexpr (sizeof(T) == 8)
         out[k] = dec64<L, FAST>(h[k], t1[k], t2[k], sd64, sc64, ei[k]) * xv[k];
       else
@@ -64,89 +73,12 @@ __device__ __forceinline__ void products(const SpmvParams<T>& p, const long long
   }
 }
 
-// Row sums of a short block (< 32 rows, none empty) with few shared-memory wavefronts: the
-// products (strided: lane l holds tile positions l + 32 k) are transposed through the
-// padded tile so that lane l holds positions 8 l .. 8 l + 7 (8-byte accesses without bank
-// conflicts: position q lives at q + q / 8); the row-start flags of the 256 positions come
-// from one warp OR-reduction per 32-position word (lane j <= nrows holds the start of row
-// j; lane nrows' start is the block end, a ghost start that closes the last row).  Each
-// lane sums its positions in order, writing rows that start and end inside it; a segmented
-// inclusive scan over the lanes (flag = "a row starts in this lane") carries the open sums
-// across lanes.  Fixed order: deterministic.
-#ifndef GSE_SP_SEG
-#define GSE_SP_SEG 0
-#endif
-template <bool DOT, class T>
-__device__ __forceinline__ void seg_rows(const SpmvParams<T>& p, T* wp, const T (&v)[EPL],
-                                         uint32_t rs, uint32_t nrows, uint32_t r0, int lane,
-                                         double& dacc) {
-  static_assert(EPL == 8, "one flag word per 32-position slice, 8 positions per lane");
-#pragma unroll
-  for (int k = 0; k < EPL; ++k) wp[(lane + 32 * k) + ((lane + 32 * k) >> 3)] = v[k];
-  const uint32_t wsel = (uint32_t)lane >> 2, sh = 8u * ((uint32_t)lane & 3u);
-  uint32_t word = 0, before = 0;
-#pragma unroll
-  for (int w = 0; w < EPL; ++w) {
-    const uint32_t mine = ((uint32_t)lane <= nrows && (rs >> 5) == (uint32_t)w) ? 1u << (rs & 31) : 0u;
-    const uint32_t m = __reduce_or_sync(0xFFFFFFFFu, mine);
-    before += ((uint32_t)w < wsel) ? (uint32_t)__popc(m) : 0u;
-    word = ((uint32_t)w == wsel) ? m : word;
-  }
-  before += (uint32_t)__popc(word & ((1u << sh) - 1u));
-  const uint32_t fb = (word >> sh) & 0xFFu;
-  __syncwarp();
-  T pv[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) pv[i] = wp[9 * lane + i];
-  const uint32_t rend = r0 + nrows;
-  uint32_t row = r0 + before - 1u;  // the row running into this lane (wraps for lane 0)
-  T acc = 0, head = 0;
-  bool has = false;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    if ((fb >> i) & 1u) {
-      if (has) {
-        if (row < rend) {
-          p.y[row] = acc;
-          if (DOT) dacc += (double)p.x[row] * (double)acc;
-        }
-      } else {
-        head = acc;
-        has = true;
-      }
-      ++row;
-      acc = 0;
-    }
-    acc += pv[i];
-  }
-  // segmented inclusive scan of the open sums: (a, fa) + (b, fb) = (fb ? b : a + b, fa | fb)
-  T sv = acc;
-  uint32_t sf = has ? 1u : 0u;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const T uv = __shfl_up_sync(0xFFFFFFFFu, sv, off);
-    const uint32_t uf = __shfl_up_sync(0xFFFFFFFFu, sf, off);
-    if (lane >= off) {
-      if (!sf) sv = uv + sv;
-      sf |= uf;
-    }
-  }
-  const T ex = __shfl_up_sync(0xFFFFFFFFu, sv, 1);
-  const uint32_t rc = r0 + before - 1u;
-  if (has && before >= 1u && rc < rend) {  // the row running into this lane ends here
-    const T tot = ex + head;
-    p.y[rc] = tot;
-    if (DOT) dacc += (double)p.x[rc] * (double)tot;
-  }
-}
-
 #ifndef GSE_SP_MINB  // resident CTAs per SM the register budget is sized for (A/B knob)
 #define GSE_SP_MINB 4
 #endif
 template <int L, bool SIDE, bool DOT, bool FAST, class T>
 __global__ void __launch_bounds__(SPMV_THREADS, GSE_SP_MINB) k_spmv_sp(const SpmvParams<T> p) {
-  // products tile: position q at q + q / 8 (one pad slot per 8, conflict-free transposes)
-  __shared__ __align__(16) T wprod[SPMV_WARPS][WTILE + WTILE / 8];
+  __shared__ __align__(16) T wprod[SPMV_WARPS][WTILE];
   __shared__ long long sd64[64];
   __shared__ int sd32[64];
   __shared__ double sc64[64];
@@ -198,21 +130,8 @@ __global__ void __launch_bounds__(SPMV_THREADS, GSE_SP_MINB) k_spmv_sp(const Spm
       if (pre && (uint32_t)lane <= nrows) rpl = p.row_ptr[r0 + lane];
       if (DOT && pre && (uint32_t)lane < nrows) xr = (double)p.x[r0 + lane];
       products<L, SIDE, FAST, T>(p, sd64, sd32, sc64, sc32, s + lane, e, v);
-#if GSE_SP_SEG
-      if (pre) {
-        const uint32_t rs = rpl - s;  // lane j <= nrows: start of row j (lane nrows: block end)
-        const uint32_t rn = __shfl_down_sync(0xFFFFFFFFu, rs, 1);
-        if (!__any_sync(0xFFFFFFFFu, (uint32_t)lane < nrows && rn == rs)) {  // no empty row
-          seg_rows<DOT, T>(p, wp, v, rs, nrows, r0, lane, dacc);
-          __syncwarp();
-          d0 = n0;
-          d1 = n1;
-          continue;
-        }
-      }
-#endif
 #pragma unroll
-      for (int k = 0; k < EPL; ++k) wp[(lane + 32 * k) + ((lane + 32 * k) >> 3)] = v[k];
+      for (int k = 0; k < EPL; ++k) wp[lane + 32 * k] = v[k];
       __syncwarp();
       // lpr lanes per row (power of two, 32 / nrows rounded down): with few, longer rows
       // (power-law blocks hold ~10 rows) the sequential sums shrink by lpr; lane-per-row
@@ -236,7 +155,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, GSE_SP_MINB) k_spmv_sp(const Spm
             rb = p.row_ptr[r0 + rr + 1];
             if (DOT) xrow = (double)p.x[r0 + rr];
           }
-          for (uint32_t j = ra - s + sub; j < rb - s; j += lpr) sum += wp[j + (j >> 3)];
+          for (uint32_t j = ra - s + sub; j < rb - s; j += lpr) sum += wp[j];
         }
         for (uint32_t o = lpr >> 1; o > 0; o >>= 1) sum += __shfl_down_sync(0xFFFFFFFFu, sum, o, lpr);
         if (rr < nrows && sub == 0) {
