@@ -204,7 +204,8 @@ def run_reference(args, world, rank, pg):
         return
     import gse_inputs as gi
     import oracle as O
-    cores = O.set_threads(0)
+    # all host cores (torchrun exports OMP_NUM_THREADS=1 to every rank; only rank 0 runs here)
+    cores = O.set_threads(len(os.sched_getaffinity(0)))
     A = gi.poisson3d(args.N, args.variant)
     b = gi.ones_rhs(A)
     iters_full = full_iterations(A, b)
@@ -219,7 +220,9 @@ def run_reference(args, world, rank, pg):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": unit_for(args.N),
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": _config(args, A.rows, A.nnz, world),
+            "data": "synthetic",
+            "config": {**_config(args, A.rows, A.nnz, world),
+                       "parallelism": f"the plain CPU oracle on rank 0's host cores ({cores} threads)"},
             "cpu_baseline": {"value": value, "unit": unit_for(args.N), "cores": cores,
                              "kind": "oracle",
                              "sample": f"oracle encode + {k} CG iterations per step, extrapolated "
@@ -558,7 +561,7 @@ def e2e_measure(args, A, b_h, dev, stream, encode, r0, n_glob):
 
 def cpu_baseline(args, A, b_h, iters_full):
     import oracle as O
-    cores = O.set_threads(0)
+    cores = O.set_threads(len(os.sched_getaffinity(0)))
     te, ti = oracle_sample(A, b_h, args.cpu_iters)
     t = te + ti * iters_full
     return {"value": 1.0 / t, "unit": unit_for(args.N), "cores": cores, "kind": "oracle",

@@ -80,6 +80,7 @@ if "c2v" in secs:
     run("configs[1] shape, varcoef values (3D Poisson 128^3)", gi.poisson3d(128, "varcoef"), "cg",
         [("stepped_default", "gse", g.gse_default_schedule("cg")),
          ("stepped_scaled", "gse", g.gse_default_schedule("cg", l=30, t=10, m=10)),
+         ("stepped_floors", "gse", g.gse_default_schedule("cg", level_floor=(1e-3, 1e-8))),
          ("fixed_L3", "gse", g.fixed_schedule(3)),
          ("fp64", "fp64", None), ("bf16", "bf16", None)], 3)
 if "c4" in secs:
@@ -87,6 +88,7 @@ if "c4" in secs:
     run(f"configs[3] conv-diff {N}^3 GMRES(30)", gi.convdiff3d(N), "gmres",
         [("stepped_default", "gse", g.gse_default_schedule("gmres")),
          ("stepped_scaled", "gse", g.gse_default_schedule("gmres", l=300, t=100, m=100)),
+         ("stepped_floors", "gse", g.gse_default_schedule("gmres", level_floor=(1e-3, 1e-8))),
          ("fp64", "fp64", None), ("bf16", "bf16", None)], 2)
 if "c5" in secs:
     N = int(os.environ.get("C5_N", "512"))

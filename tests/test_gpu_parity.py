@@ -538,3 +538,20 @@ def test_spmv_full_size_c4_sampled_and_gmres(g):
     F = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
     res = np.linalg.norm(b - O.spmv_fp64(F, x.cpu().numpy())) / np.linalg.norm(b)
     assert res <= 1e-10 * 1.01 and abs(res - rep["rel_residual_true"]) <= 1e-3 * res
+
+
+@pytest.mark.parametrize("solver", ["cg", "gmres"])
+@pytest.mark.parametrize("floors", [(1e300, 1e300), (1e-3, 1e-8)])
+def test_level_floors_parity(g, solver, floors):
+    """R17 level floors: the GPU escalates at the same iterations as the oracle (+-2)"""
+    A = gi.poisson2d(32, "varcoef") if solver == "cg" else gi.convdiff3d(12)
+    b = gi.ones_rhs(A)
+    M, R = enc_both(g, A)
+    run_g = g.gse_solve_cg if solver == "cg" else g.gse_solve_gmres
+    run_o = O.cg if solver == "cg" else O.gmres
+    _, rg = run_g(M, b, tol=1e-10, sched=g.gse_default_schedule(solver, level_floor=floors))
+    _, ro = run_o(R, b, tol=1e-10, sched=O.schedule(solver, level_floor=floors))
+    _cmp_reports(rg, ro)
+    assert rg["n_switches"] == ro.n_switches == 2
+    for a, c in zip(rg["switch_iter"], ro.switch_iter):
+        assert abs(a - c) <= 2

@@ -297,3 +297,24 @@ def test_stepped_forced_escalation_reaches_full():
     _, rep = O.cg(enc(A), b, tol=1e-10, sched=s)
     assert rep.n_switches == 2 and rep.switch_to_level == (2, 3)
     assert rep.switch_iter == (t + 1, t + 2)
+
+
+@pytest.mark.parametrize("solver", ["cg", "gmres"])
+def test_level_floors(solver):
+    """R17 level floors (build heuristic, off by default): a floor above every residual
+    escalates after the first iteration at each level (switches at iterations 1 and 2, then
+    the full-precision solve converges); a floor below every residual never fires (the same
+    solve as without floors); floors between act before the monitor's first check at l."""
+    A = gi.poisson2d(24, "varcoef") if solver == "cg" else gi.convdiff3d(8)
+    b = gi.ones_rhs(A)
+    G = enc(A)
+    run = O.cg if solver == "cg" else O.gmres
+    _, rep = run(G, b, tol=1e-10, sched=O.schedule(solver, level_floor=(1e300, 1e300)))
+    assert rep.switch_iter == (1, 2) and rep.switch_to_level == (2, 3)
+    assert rep.converged and rep.rel_residual_true <= 1e-10
+    _, r0 = run(G, b, tol=1e-10, sched=O.schedule(solver))
+    _, r1 = run(G, b, tol=1e-10, sched=O.schedule(solver, level_floor=(1e-300, 1e-300)))
+    assert (r1.iterations, r1.switch_iter) == (r0.iterations, r0.switch_iter)
+    _, rf = run(G, b, tol=1e-10, sched=O.schedule(solver, level_floor=(1e-3, 1e-8)))
+    assert rf.converged and rf.n_switches == 2 and rf.rel_residual_true <= 1e-10
+    assert rf.switch_iter[0] < r0.switch_iter[0]  # before the head-only solve "converges"
