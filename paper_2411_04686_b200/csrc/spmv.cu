@@ -37,25 +37,6 @@ static SpmvParams<T> make_params(const Matrix& M, int level, const T* x, T* y,
   p.dot_result = dot ? dot->result : nullptr;
   p.stop = nullptr;
   const int L = level >= 1 && level <= 3 ? level : 3;
-  // packed register table (spmv_common.cuh dec_reg): <= 8 entries spanning < 256 exponents
-  p.etab[0] = p.etab[1] = 0;
-  p.ebase64 = p.ebase32 = 0;
-  p.regtab = 0;
-  if (M.kind == GSE_KIND_GSE && M.table_len > 0 && M.table_len <= 8) {
-    int emin = 1 << 30, emax = -1;
-    for (int i = 0; i < M.table_len; ++i) {
-      emin = M.table[i] < emin ? M.table[i] : emin;
-      emax = M.table[i] > emax ? M.table[i] : emax;
-    }
-    if (emax - emin < 256) {
-      for (int i = 0; i < M.table_len; ++i)
-        p.etab[i >> 2] |= (uint32_t)(M.table[i] - emin) << (8 * (i & 3));
-      const int sL = L == 1 ? 48 : L == 2 ? 32 : 0;
-      p.ebase64 = emin - 63 + sL;
-      p.ebase32 = emin - 1086 + sL + 127;
-      p.regtab = 1;
-    }
-  }
   for (int i = 0; i < 64; ++i) {
     p.d64[i] = M.htab.d64[L - 1][i];
     p.d32[i] = M.htab.d32[L - 1][i];

@@ -108,12 +108,6 @@ struct SpmvParams {
   const int* stop;    // optional: skip the launch when *stop != 0 (GMRES cycle graphs)
   long long d64[64];  // decode deltas of the launched level (integer form, FP64)
   int d32[64];        // (integer form, FP32)
-  // register form of the scales (SP kernel, tables of <= 8 entries spanning < 256
-  // exponents): byte ei of etab = E_ei - E_min; the biased exponent field of scale_ei is
-  // ebase + byte (ebase64 = E_min - 63 + s_L for FP64, ebase32 = E_min - 1086 + s_L + 127)
-  uint32_t etab[2];
-  int ebase64, ebase32;
-  int regtab;         // 1: etab / ebase valid for the launched level
   double sc64[64];    // multiply-form scales when the table allows it (FAST)
   float sc32[64];
 };
@@ -170,37 +164,6 @@ __device__ __forceinline__ float dec32(uint32_t h, uint32_t t1, uint32_t t2, con
       return decode_f32_u32(((h & 0x7FFFu) << 16) | t1, sd[ei], h);
     else
       return decode_f32(((uint64_t)(h & 0x7FFFu) << 48) | ((uint64_t)t1 << 32) | t2, sd[ei], h);
-  }
-}
-
-// signed level-L value of one element in multiply form with the scale built in registers
-// from the packed exponent table (no shared-memory lookup); equals dec64<L, true> /
-// dec32<L, true> (the sign folded into the scale instead of the significand)
-template <int L, class T>
-__device__ __forceinline__ T dec_reg(const SpmvParams<T>& p, uint32_t h, uint32_t t1, uint32_t t2,
-                                     uint32_t ei) {
-  const uint32_t byte = __byte_perm(p.etab[0], p.etab[1], ei) & 0xFFu;
-  const uint32_t sgn = (h & 0x8000u) << 16;
-  if constexpr (sizeof(T) == 8) {
-    const double sc = __hiloint2double((int)(((byte + (uint32_t)p.ebase64) << 20) | sgn), 0);
-    double m;
-    if constexpr (L == 1)
-      m = (double)(h & 0x7FFFu);
-    else if constexpr (L == 2)
-      m = (double)(((h & 0x7FFFu) << 16) | t1);
-    else
-      m = __ull2double_rz(((uint64_t)(h & 0x7FFFu) << 48) | ((uint64_t)t1 << 32) | t2);
-    return m * sc;
-  } else {
-    const float sc = __uint_as_float(((byte + (uint32_t)p.ebase32) << 23) | sgn);
-    float m;
-    if constexpr (L == 1)
-      m = (float)(h & 0x7FFFu);
-    else if constexpr (L == 2)
-      m = __uint2float_rz(((h & 0x7FFFu) << 16) | t1);
-    else
-      m = __ull2float_rz(((uint64_t)(h & 0x7FFFu) << 48) | ((uint64_t)t1 << 32) | t2);
-    return m * sc;
   }
 }
 

@@ -13,9 +13,6 @@
 //    shuffle tree.
 #include "spmv_common.cuh"
 
-#ifndef GSE_SP_REGTAB  // A/B knob: scales from a packed register table instead of smem
-#define GSE_SP_REGTAB 0
-#endif
 
 namespace gse {
 
@@ -60,11 +57,6 @@ __device__ __forceinline__ void products(const SpmvParams<T>& p, const long long
       out[k] = (T)(half_value<L>(h[k]) * (double)xv[k]);
     } else {
       if constexpr (!SIDE) ei[k] = __funnelshift_rc(c[k], 0u, p.ei_shift);
-#if GSE_SP_REGTAB
-      if (FAST && p.regtab)  // (uniform) scale from the packed register table
-        out[k] = dec_reg<L, T>(p, h[k], t1[k], t2[k], ei[k]) * xv[k];
-      else
-#endif
       if constexpr (sizeof(T) == 8)
         out[k] = dec64<L, FAST>(h[k], t1[k], t2[k], sd64, sc64, ei[k]) * xv[k];
       else
