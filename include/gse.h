@@ -83,6 +83,12 @@ typedef struct {
                               * representable).  Single-GPU gse_encode only.                */
   uint64_t seed;             /* sampling: row of block b = b*B + splitmix64(seed, b+1) mod
                               * len_b (R27: SplitMix64 output for counter b+1)              */
+  int per_shard_table;       /* gse_encode_dist only: 0 = one GLOBAL table from the
+                              * allreduced histogram (R21, default); 1 = each rank selects
+                              * its own table from its rows' histogram (the paper's "group"
+                              * read as the row block): no histogram
+                              * allreduce, rank-local decode constants.  Ignored by
+                              * gse_encode.                                                */
 } gse_encode_opts;
 
 typedef enum {

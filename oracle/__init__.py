@@ -73,6 +73,7 @@ class OrcSchedule(C.Structure):
         ("l", C.c_int64), ("t", C.c_int64), ("m", C.c_int64),
         ("rsd_limit", C.c_double), ("ndec_limit", C.c_int64), ("reldec_limit", C.c_double),
         ("verify_at_full", C.c_int), ("level_floor", C.c_double * 2),
+        ("krylov_gse16", C.c_int),
     ]
 
 
@@ -97,6 +98,9 @@ def _declare(L):
     L.orc_assemble.restype = C.c_uint64
     L.orc_decode.argtypes = [C.c_uint64, i32, _p(C.c_uint16), i32, _p(dbl)]
     L.orc_encode_head16_with_ei.argtypes = [dbl, _p(C.c_uint16), i32, i32, _p(C.c_uint16)]
+    L.orc_decode_head16_with_ei.argtypes = [C.c_uint16, _p(C.c_uint16), i32, i32, _p(dbl)]
+    L.orc_encode_vector16.argtypes = [i64, _p(dbl), i32, _p(C.c_uint16), _p(C.c_uint16), _p(i32)]
+    L.orc_decode_vector16.argtypes = [i64, _p(C.c_uint16), _p(C.c_uint16), i32, i32, _p(dbl)]
     L.orc_encode_csr.argtypes = [i64, i64, i64, _p(i64), _p(C.c_int32), _p(dbl), i32,
                                  _p(C.c_uint16), _p(i32), _p(i32), _p(i32), _p(C.c_uint32),
                                  _p(C.c_uint8), _p(C.c_uint16), _p(C.c_uint16),
@@ -179,6 +183,40 @@ def build_table(hist, k_max: int = 8):
     if st != OK:
         raise OracleError(st, "build_table")
     return table[: n.value].copy()
+
+
+def decode_head16_with_ei(word: int, table, ei_bits: int) -> float:
+    t = np.ascontiguousarray(table, dtype=np.uint16)
+    out = C.c_double()
+    st = lib().orc_decode_head16_with_ei(word, _ptr(t, C.c_uint16), t.size, ei_bits, C.byref(out))
+    if st != OK:
+        raise OracleError(st, "decode_head16_with_ei")
+    return out.value
+
+
+def encode_vector16(v, k_max: int = 8):
+    """NEXT-4: a vector in 16-bit GSE-SEM form (Alg. 1): (words uint16[n], table)."""
+    x = np.ascontiguousarray(v, dtype=np.float64)
+    words = np.zeros(max(x.size, 1), np.uint16)
+    table = np.zeros(64, np.uint16)
+    tl = C.c_int()
+    st = lib().orc_encode_vector16(x.size, _ptr(x, C.c_double), k_max, _ptr(words, C.c_uint16),
+                                   _ptr(table, C.c_uint16), C.byref(tl))
+    if st != OK:
+        raise OracleError(st, "encode_vector16")
+    return words[:x.size].copy(), table[:tl.value].copy()
+
+
+def decode_vector16(words, table, ei_bits: int = 3):
+    w = np.ascontiguousarray(words, dtype=np.uint16)
+    t = np.ascontiguousarray(table, dtype=np.uint16)
+    tt = t if t.size else np.zeros(1, np.uint16)
+    out = np.zeros(max(w.size, 1), np.float64)
+    st = lib().orc_decode_vector16(w.size, _ptr(w, C.c_uint16), _ptr(tt, C.c_uint16), t.size,
+                                   ei_bits, _ptr(out, C.c_double))
+    if st != OK:
+        raise OracleError(st, "decode_vector16")
+    return out[:w.size]
 
 
 def sample_row(rows: int, block_rows: int, seed: int, b: int) -> int:

@@ -275,6 +275,74 @@ int orc_encode_head16_with_ei(double x, const uint16_t* table, int table_len, in
   return ORC_OK;
 }
 
+/* Inverse of the 16-bit SEM word of Alg. 1 (EI inside the word): sign = bit 15, EI = the
+ * ei_bits below it, significand = the remaining mbits = 15 - ei_bits bits with its explicit
+ * one (Alg. 2's reading, applied to the Alg. 1 layout).  Closed form of the
+ * value (R28): |v| = mant * 2^(E_EI - 1023 - mbits), E_EI the stored (e+1) entry; mant = 0
+ * -> signed zero (R10); a result below the normal range -> signed zero (R11). */
+int orc_decode_head16_with_ei(uint16_t w, const uint16_t* table, int table_len, int ei_bits,
+                              double* out) {
+  const int mbits = 15 - ei_bits;
+  const int sign = (w >> 15) & 1;
+  const int ei = (w >> mbits) & ((1 << ei_bits) - 1);
+  const unsigned mant = w & ((1u << mbits) - 1u);
+  if (ei >= table_len && mant) return ORC_ERR_INVALID_EXP_INDEX;
+  double v = 0.0;
+  if (mant) {
+    v = ldexp((double)mant, (int)table[ei] - 1023 - mbits);
+    if (v < 2.2250738585072014e-308) v = 0.0; /* below the normal range: flush (R11) */
+  }
+  *out = sign ? -v : v;
+  return ORC_OK;
+}
+
+/* NEXT-4 -- a vector in 16-bit GSE-SEM form (Alg. 1, verbatim layout): the
+ * table from the vector's own exponent histogram (top k_max, e_max forced),
+ * each element encoded by Alg. 1 into sign | EI | denormalised significand.  Returns the
+ * table (<= 64 entries) and the words; an all-zero vector gives table_len 0, words = signs. */
+int orc_encode_vector16(int64_t n, const double* v, int k_max, uint16_t* words, uint16_t* table,
+                        int* table_len) {
+  uint64_t* hist = (uint64_t*)malloc(2048 * sizeof(uint64_t));
+  int64_t nz, bad;
+  int st = orc_exponent_histogram(n, v, hist, &nz, &bad);
+  if (st != ORC_OK) { free(hist); return st; }
+  int eb = 0;
+  while ((1 << eb) < k_max) ++eb;
+  st = orc_build_table(hist, k_max, table, table_len);
+  free(hist);
+  if (st == ORC_ERR_NO_VALUES) { /* all zero / subnormal */
+    *table_len = 0;
+    for (int64_t i = 0; i < n; ++i) words[i] = (uint16_t)((bits_of(v[i]) >> 63) << 15);
+    return ORC_OK;
+  }
+  if (st != ORC_OK) return st;
+  for (int64_t i = 0; i < n; ++i) {
+    st = orc_encode_head16_with_ei(v[i], table, *table_len, eb, &words[i]);
+    if (st != ORC_OK) return st;
+  }
+  return ORC_OK;
+}
+
+int orc_decode_vector16(int64_t n, const uint16_t* words, const uint16_t* table, int table_len,
+                        int ei_bits, double* out) {
+  for (int64_t i = 0; i < n; ++i) {
+    int st = orc_decode_head16_with_ei(words[i], table, table_len, ei_bits, &out[i]);
+    if (st != ORC_OK) return st;
+  }
+  return ORC_OK;
+}
+
+/* v <- dec16(enc16(v)): the value a Krylov vector takes when stored in 16-bit GSE form
+ * (k = 8: 3 EI bits, 12 significand bits) -- every later use reads these values */
+static void compress16(int64_t n, double* v) {
+  uint16_t* w = (uint16_t*)malloc((size_t)(n ? n : 1) * sizeof(uint16_t));
+  uint16_t table[64];
+  int tl = 0;
+  if (orc_encode_vector16(n, v, 8, w, table, &tl) == ORC_OK)
+    orc_decode_vector16(n, w, table, tl, 3, v);
+  free(w);
+}
+
 /* ------------------------------------------------------------------------------------
  * CSR conversion.  P:168 "the indices of shared exponents can be encoded into the column
  * indices of non-zeros ... When the column size of a sparse matrix is so large that there
@@ -807,6 +875,7 @@ int orc_gmres(const orc_matrix* A, const double* b, double* x, double tol, int r
     }
     if (jg >= max_iters) { status = ORC_NOT_CONVERGED; break; }
     for (int64_t i = 0; i < n; ++i) V[i] = w[i] / beta;
+    if (sched->krylov_gse16) compress16(n, V); /* NEXT-4 (R28) */
     for (int i = 0; i <= m; ++i) g[i] = 0.0;
     g[0] = beta;
     int k = 0;          /* basis vectors used in this cycle */
@@ -853,6 +922,7 @@ int orc_gmres(const orc_matrix* A, const double* b, double* x, double tol, int r
       if (jg >= max_iters) break;
       double* vn = V + (size_t)(jj + 1) * (size_t)n;
       for (int64_t q = 0; q < n; ++q) vn[q] = w[q] / hn;
+      if (sched->krylov_gse16) compress16(n, vn);
     }
     if (status == ORC_NUMERICAL_ABORT) break;
     /* back substitution H[0:k,0:k] y = g[0:k]; x += V y */

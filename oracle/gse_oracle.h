@@ -37,6 +37,12 @@ uint64_t orc_assemble(uint16_t head, uint16_t tail1, uint32_t tail2, int level);
 int orc_decode(uint64_t word, int ei, const uint16_t* table, int table_len, double* out);
 int orc_encode_head16_with_ei(double x, const uint16_t* table, int table_len, int ei_bits,
                               uint16_t* out);
+int orc_decode_head16_with_ei(uint16_t w, const uint16_t* table, int table_len, int ei_bits,
+                              double* out);
+int orc_encode_vector16(int64_t n, const double* v, int k_max, uint16_t* words, uint16_t* table,
+                        int* table_len);
+int orc_decode_vector16(int64_t n, const uint16_t* words, const uint16_t* table, int table_len,
+                        int ei_bits, double* out);
 
 /* ---- CSR conversion ---- */
 int orc_encode_csr(int64_t rows, int64_t cols, int64_t nnz, const int64_t* row_ptr,
@@ -101,6 +107,7 @@ typedef struct {
   double reldec_limit;
   int verify_at_full;
   double level_floor[2];
+  int krylov_gse16; /* GMRES: Krylov basis stored as 16-bit GSE-SEM vectors (NEXT-4, R28) */
 } orc_schedule;
 
 typedef struct {

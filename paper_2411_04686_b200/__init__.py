@@ -63,7 +63,7 @@ class CsrF64(C.Structure):
 
 class EncodeOpts(C.Structure):
     _fields_ = [("k_max", C.c_int), ("device", C.c_int), ("sample_block_rows", C.c_int64),
-                ("seed", C.c_uint64)]
+                ("seed", C.c_uint64), ("per_shard_table", C.c_int)]
 
 
 class MatrixInfo(C.Structure):
@@ -228,7 +228,7 @@ def gse_encode(row_ptr, col_idx, values, rows: int, cols: int, k_max: int = 8,
     dev = _device_of(values, col_idx, row_ptr) if device is None else device
     if dev < 0:
         dev = _current_device()
-    opts = EncodeOpts(k_max, dev, sample_block_rows, seed)
+    opts = EncodeOpts(k_max, dev, sample_block_rows, seed, 0)
     out = C.c_void_p()
     _check(_lib.gse_encode(C.byref(A), C.byref(opts), C.byref(out),
                            _stream(values, col_idx, row_ptr, stream=stream)), "gse_encode")
@@ -467,11 +467,12 @@ def gse_dist_create_thread(group: int, rank: int, device: int = 0) -> Dist:
 
 
 def gse_encode_dist(D: Dist, row_ptr, col_idx, values, row_begin: int, global_rows: int,
-                    k_max: int = 8, stream=None) -> Matrix:
-    """Collective: encode this rank's row block (global column ids)."""
+                    k_max: int = 8, stream=None, per_shard_table: bool = False) -> Matrix:
+    """Collective: encode this rank's row block (global column ids).  per_shard_table: the
+    rank's own table instead of the global one (no histogram allreduce)."""
     rows = int((row_ptr.numel() if _is_torch(row_ptr) else row_ptr.size) - 1)
     A = _csr(rows, global_rows, row_ptr, col_idx, values)
-    opts = EncodeOpts(k_max, -1, 0, 0)
+    opts = EncodeOpts(k_max, -1, 0, 0, 1 if per_shard_table else 0)
     out = C.c_void_p()
     _check(_lib.gse_encode_dist(D.handle, C.byref(A), row_begin, global_rows, C.byref(opts),
                                 C.byref(out), _stream(values, col_idx, row_ptr, stream=stream)),

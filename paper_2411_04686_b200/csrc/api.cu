@@ -206,7 +206,7 @@ static void destroy_matrix(Matrix& M) {
 gse_status create_from_csr(const gse_csr_f64* A, int kind, int k_max, int device,
                            gse_matrix* out, cudaStream_t s, Matrix** mout, Comm* comm,
                            const int32_t* local_col_host, int64_t sample_block_rows,
-                           uint64_t sample_seed) {
+                           uint64_t sample_seed, int shard_table) {
   gse_status rc = check_csr(A);
   if (rc != GSE_OK) return rc;
   if (!out) {
@@ -237,7 +237,7 @@ gse_status create_from_csr(const gse_csr_f64* A, int kind, int k_max, int device
   M.k_max = k_max;
   if (kind == GSE_KIND_GSE)
     rc = encode_matrix(M, *A, rp, A->row_ptr_64, col, val, s, comm, sample_block_rows,
-                       sample_seed);
+                       sample_seed, shard_table);
   else
     rc = fp64_matrix(M, rp, A->row_ptr_64, col, val, s, kind);
   if (rc == GSE_OK) rc = st.finish();
@@ -324,7 +324,7 @@ void gse_default_schedule(int solver, gse_step_schedule* o) {
 
 gse_status gse_encode(const gse_csr_f64* A, const gse_encode_opts* opts, gse_matrix* out,
                       void* stream) {
-  gse_encode_opts o = {8, -1, 0, 0};
+  gse_encode_opts o = {8, -1, 0, 0, 0};
   if (opts) o = *opts;
   if (o.k_max < 1 || o.k_max > 64 || (o.k_max & (o.k_max - 1))) {
     set_error("k_max must be a power of two in [1, 64]");

@@ -599,11 +599,12 @@ gse_status gse_encode_dist(gse_dist Dh, const gse_csr_f64* A, int64_t row_begin,
   // encode the local rows with local column ids and the GLOBAL table
   gse_csr_f64 L = *A;
   L.cols = n_local + (int64_t)halo.size();
-  gse_encode_opts o = {8, comm->device, 0, 0};
+  gse_encode_opts o = {8, comm->device, 0, 0, 0};
   if (opts) o = *opts;
   o.device = comm->device;
   Matrix* M = nullptr;
-  st = create_from_csr(&L, GSE_KIND_GSE, o.k_max, o.device, out, s, &M, comm, local_col.data());
+  st = create_from_csr(&L, GSE_KIND_GSE, o.k_max, o.device, out, s, &M, comm, local_col.data(),
+                       0, 0, o.per_shard_table ? 1 : 0);
   if (st != GSE_OK) return st;
   DistCtx* D = new DistCtx();
   D->comm = comm;

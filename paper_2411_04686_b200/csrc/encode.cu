@@ -488,7 +488,7 @@ static std::string row_col_of(const void* d_row_ptr, int rp64, const int32_t* d_
 
 gse_status encode_matrix(Matrix& M, const gse_csr_f64& A, const void* d_row_ptr, int rp64,
                          const int32_t* d_col, const double* d_val, cudaStream_t s, Comm* comm,
-                         int64_t sample_block_rows, uint64_t sample_seed) {
+                         int64_t sample_block_rows, uint64_t sample_seed, int shard_table) {
   M.kind = GSE_KIND_GSE;
   int eb = 0;
   while ((1 << eb) < M.k_max) ++eb;
@@ -511,9 +511,10 @@ gse_status encode_matrix(Matrix& M, const gse_csr_f64& A, const void* d_row_ptr,
     k_hist<<<g, 512, 0, s>>>(d_val, M.nnz, st);
     GSE_CUDA_TRY(cudaGetLastError());
   }
-  if (comm) {
+  if (comm && !shard_table) {
     // distributed encode: one GLOBAL table (R21) -- sum the histograms (and the zero
-    // counts, which follow hist[] in EncodeStatus) over all ranks before the selection
+    // counts, which follow hist[] in EncodeStatus) over all ranks before the selection.
+    // (shard_table: each rank keeps its own histogram -> its own table, NEXT-3)
     rc = comm_allreduce_u64(comm, st->hist, 2048 + 1, s);
     if (rc != GSE_OK) return rc;
   }

@@ -161,7 +161,7 @@ gse_status build_partition(Matrix& M, cudaStream_t s);
 gse_status encode_matrix(Matrix& M, const gse_csr_f64& A, const void* d_row_ptr, int rp64,
                          const int32_t* d_col, const double* d_val, cudaStream_t s,
                          Comm* comm = nullptr, int64_t sample_block_rows = 0,
-                         uint64_t sample_seed = 0);
+                         uint64_t sample_seed = 0, int shard_table = 0);
 // kind: GSE_KIND_FP64 (values copied) or GSE_KIND_FP16 / GSE_KIND_BF16 (RNE to 16 bits, R26)
 gse_status fp64_matrix(Matrix& M, const void* d_row_ptr, int rp64, const int32_t* d_col,
                        const double* d_val, cudaStream_t s, int kind = GSE_KIND_FP64);
@@ -201,7 +201,7 @@ void free_dist(Matrix& M);
 gse_status create_from_csr(const gse_csr_f64* A, int kind, int k_max, int device,
                            gse_matrix* out, cudaStream_t s, Matrix** mout, Comm* comm,
                            const int32_t* local_col_host, int64_t sample_block_rows = 0,
-                           uint64_t sample_seed = 0);
+                           uint64_t sample_seed = 0, int shard_table = 0);
 
 }  // namespace gse
 

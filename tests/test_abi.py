@@ -54,7 +54,7 @@ def test_invalid_args_fail_without_touching_the_gpu():
     assert lib.gse_spmv(None, None, None, 1, None) == g.GSE_ERR_INVALID_ARG
     assert lib.gse_solve_cg(None, None, None, 1e-6, 10, None, None, None) == g.GSE_ERR_INVALID_ARG
     A = g.CsrF64(2, 2, 2, None, 0, None, None)
-    opts = g.EncodeOpts(3, 0, 0, 0)  # k_max not a power of two
+    opts = g.EncodeOpts(3, 0, 0, 0, 0)  # k_max not a power of two
     out = C.c_void_p()
     assert lib.gse_encode(C.byref(A), C.byref(opts), C.byref(out), None) == g.GSE_ERR_INVALID_ARG
     assert b"k_max" in lib.gse_last_error_detail()

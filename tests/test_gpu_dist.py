@@ -184,3 +184,66 @@ def test_dist_gmres(g, P, mode):
     F = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
     res = np.linalg.norm(b - O.spmv_fp64(F, x)) / np.linalg.norm(b)
     assert res <= 1e-10 * 1.01
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_dist_per_shard_tables(g, P):
+    """NEXT-3 per-shard ("group" = row block) tables: each rank's table, planes and EI bits
+    equal the oracle's encoding of its row block alone; SpMV on the block within the SpMV
+    tolerance of that encoding; a stepped CG over the shards converges with identical
+    decisions on every rank"""
+    A = gi.powerlaw_spd(20000, seed=6)
+    # D A D with D = 2^3 on the second half of the rows: still SPD, and the row blocks'
+    # exponent populations differ, so their tables must too
+    sc = np.where(np.arange(A.rows) >= A.rows // 2, 2.0 ** 3, 1.0)
+    rows_of = np.repeat(np.arange(A.rows), np.diff(A.row_ptr))
+    A = gi.Csr(A.rows, A.cols, A.row_ptr, A.col, A.val * sc[rows_of] * sc[A.col], "scaled")
+    x = gi.uniform_vec(A.cols, seed=2)
+    rr = partition(A.rows, P)
+    B = gi.poisson3d(20, "varcoef")
+    sb = np.where(np.arange(B.rows) >= B.rows // 2, 2.0 ** 3, 1.0)
+    rows_b = np.repeat(np.arange(B.rows), np.diff(B.row_ptr))
+    B = gi.Csr(B.rows, B.cols, B.row_ptr, B.col, B.val * sb[rows_b] * sb[B.col], "scaled")
+    bB = gi.ones_rhs(B)
+    rc = partition(B.rows, P)
+
+    def fn(r, D, st):
+        a, b = rr[r], rr[r + 1]
+        rp, col, val = slab(A, a, b)
+        dev = lambda v: torch.from_numpy(v).cuda()
+        M = g.gse_encode_dist(D, dev(rp), dev(col), dev(val), a, A.rows, stream=st.cuda_stream,
+                              per_shard_table=True)
+        P_ = g.gse_matrix_copy_planes(M)
+        ys = [g.gse_spmv(M, dev(x[a:b].copy()), segments=L, stream=st.cuda_stream).cpu().numpy()
+              for L in (1, 2, 3)]
+        M.close()
+        # CG on a D B D-scaled 3D Poisson (the power-law system converges too slowly)
+        c, d = rc[r], rc[r + 1]
+        rp2, col2, val2 = slab(B, c, d)
+        M2 = g.gse_encode_dist(D, dev(rp2), dev(col2), dev(val2), c, B.rows,
+                               stream=st.cuda_stream, per_shard_table=True)
+        _, rep = g.gse_solve_cg(M2, dev(bB[c:d].copy()), tol=1e-10, stream=st.cuda_stream,
+                                sched=g.gse_default_schedule("cg", l=30, t=10, m=10))
+        torch.cuda.synchronize()
+        M2.close()
+        return P_, ys, rep
+
+    outs = run_ranks(P, fn)
+    tables = []
+    for r, (P_, ys, rep) in enumerate(outs):
+        a, b = rr[r], rr[r + 1]
+        rp, col, val = slab(A, a, b)
+        R = O.encode_csr(b - a, A.cols, rp, col, val)
+        assert list(P_["table"]) == list(R.table)
+        tables.append(tuple(R.table))
+        for k in ("head", "tail1", "tail2"):
+            assert np.array_equal(P_[k], getattr(R, k)), k
+        assert np.array_equal(P_["col_ei"] >> 29, R.col_ei >> 29)
+        absR = O.GseCsr(R.rows, R.cols, R.nnz, R.row_ptr, R.col_ei, R.side_ei,
+                        R.head & np.uint16(0x7FFF), R.tail1, R.tail2, R.table, R.ei_bits,
+                        R.ei_in_column)
+        for L, y in zip((1, 2, 3), ys):
+            assert np.all(np.abs(y - O.spmv_gse(R, x, L)) <= 1e-12 * O.spmv_gse(absR, np.abs(x), L))
+        assert rep["converged"] and rep["rel_residual_true"] <= 1e-10
+        assert rep["iterations"] == outs[0][2]["iterations"]
+    assert len(set(tables)) > 1  # the shards really chose different tables
