@@ -192,6 +192,11 @@ typedef struct {
   double reldec_limit;         /* Condition 2, Eq. 6                                  */
   int verify_at_full;          /* R16: a converged recurrence at L < 3 is checked with A_3   */
   double level_floor[2];       /* R17: escalate when resid < floor[L-1] at L = 1, 2; 0 = off */
+  int krylov_gse16;            /* GMRES only, single GPU: 1 = keep the Krylov basis as 16-bit
+                                * GSE-SEM vectors (Alg. 1 layout, k = 8: 3 EI bits, 12
+                                * significand bits; a table per basis vector; NEXT-4, R28):
+                                * the Arnoldi steps and the solution update read the decoded
+                                * 16-bit values; 0 = FP64 basis (default)                    */
 } gse_step_schedule;
 
 typedef struct {
@@ -226,6 +231,23 @@ gse_status gse_solve_cg(gse_matrix A, const double* b, double* x, double tol, in
 gse_status gse_solve_gmres(gse_matrix A, const double* b, double* x, double tol, int restart,
                            int64_t max_iters, const gse_step_schedule* sched,
                            gse_solve_report* rep, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * 16-bit GSE-SEM vectors (Alg. 1: "converting double-precision vector to GSE-SEM
+ * vector", in its own 16-bit layout; R28).
+ * gse_encode_vector16: table = the k_max most frequent exponents of v (ties to the larger,
+ *   e_max forced into the last slot, entries e + 1), then per element
+ *   word = sign << 15 | EI << (15 - ei_bits) | significand with its explicit one, truncated
+ *   (ei_bits = log2 k_max; zero / subnormal -> signed zero; d > 15 - ei_bits -> signed zero).
+ *   v[n] FP64, words[n] uint16 (host or device), table[16] / table_len host outputs.
+ *   k_max: power of two in [1, 16].  Bit-identical to the oracle.
+ * gse_decode_vector16: |v| = significand * 2^(E_EI - 1023 - (15 - ei_bits)), flush below the
+ *   normal range (R11).  out[n] FP64.  INVALID_ARG for bad sizes / ei_bits > 4.
+ * ------------------------------------------------------------------------------------- */
+gse_status gse_encode_vector16(const double* v, int64_t n, int k_max, uint16_t* words,
+                               uint16_t* table, int* table_len, void* stream);
+gse_status gse_decode_vector16(const uint16_t* words, int64_t n, const uint16_t* table,
+                               int table_len, int ei_bits, double* out, void* stream);
 
 void gse_matrix_free(gse_matrix A);
 

@@ -37,7 +37,7 @@ ABI_SYMBOLS = (
     "gse_solve_gmres", "gse_matrix_free", "gse_status_string", "gse_last_error_detail",
     "gse_set_allocator", "gse_nccl_unique_id", "gse_dist_create", "gse_encode_dist",
     "gse_dist_free", "gse_dist_thread_group_create", "gse_dist_thread_group_free",
-    "gse_dist_create_thread", "gse_dist_plan",
+    "gse_dist_create_thread", "gse_dist_plan", "gse_encode_vector16", "gse_decode_vector16",
 )
 
 
@@ -80,7 +80,7 @@ class StepSchedule(C.Structure):
                 ("l", C.c_int64), ("t", C.c_int64), ("m", C.c_int64),
                 ("rsd_limit", C.c_double), ("ndec_limit", C.c_int64),
                 ("reldec_limit", C.c_double), ("verify_at_full", C.c_int),
-                ("level_floor", C.c_double * 2)]
+                ("level_floor", C.c_double * 2), ("krylov_gse16", C.c_int)]
 
 
 class SolveReport(C.Structure):
@@ -124,6 +124,8 @@ def _declare(L):
     L.gse_dist_free.argtypes = [vp]
     L.gse_dist_free.restype = None
     L.gse_dist_plan.argtypes = [i64, vp, i64, i64, i32, vp, vp, C.POINTER(i64), vp, vp]
+    L.gse_encode_vector16.argtypes = [vp, i64, i32, vp, vp, C.POINTER(i32), vp]
+    L.gse_decode_vector16.argtypes = [vp, i64, vp, i32, i32, vp, vp]
 
 
 _declare(_lib)
@@ -289,8 +291,22 @@ def gse_matrix_get_info(A: Matrix) -> dict:
     }
 
 
-def gse_matrix_copy_planes(A: Matrix) -> dict:
+def _current_stream():
+    """torch's current stream on the current device (None without CUDA): host copies of the
+    library's planes are ordered on it instead of the legacy default stream, which would
+    wait for every other thread's blocking work (multi-rank thread backend)"""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.current_stream().cuda_stream
+    except Exception:
+        pass
+    return None
+
+
+def gse_matrix_copy_planes(A: Matrix, stream=None) -> dict:
     """Copy the encoded planes to host numpy arrays (for bit-exact parity checks)."""
+    stream = _current_stream() if stream is None else _stream(stream=stream)
     inf = A.info
     n = inf["nnz"]
     out = {"col_ei": np.zeros(max(n, 1), np.uint32), "head": np.zeros(max(n, 1), np.uint16),
@@ -300,11 +316,11 @@ def gse_matrix_copy_planes(A: Matrix) -> dict:
     if inf["kind"] != GSE_KIND_GSE:  # FP64: columns; FP16 / BF16: columns + 16-bit codes
         head = out["head"] if inf["kind"] in (GSE_KIND_FP16, GSE_KIND_BF16) else None
         _check(_lib.gse_matrix_copy_planes(A.handle, _addr(out["col_ei"]), None, _addr(head),
-                                           None, None, None, None), "gse_matrix_copy_planes")
+                                           None, None, None, stream), "gse_matrix_copy_planes")
         return {"col": out["col_ei"][:n], "half": None if head is None else head[:n]}
     _check(_lib.gse_matrix_copy_planes(A.handle, _addr(out["col_ei"]), _addr(side),
                                        _addr(out["head"]), _addr(out["tail1"]),
-                                       _addr(out["tail2"]), _addr(out["table"]), None),
+                                       _addr(out["tail2"]), _addr(out["table"]), stream),
            "gse_matrix_copy_planes")
     res = {k: v[:n] for k, v in out.items() if k != "table"}
     res["table"] = out["table"][: inf["table_len"]]
@@ -408,6 +424,38 @@ def gse_solve_gmres(A: Matrix, b, x=None, tol: float = 1e-10, restart: int = 30,
                               _stream(b, x, stream=stream))
     _check(st, "gse_solve_gmres", _SOLVE_OK)
     return x, _report(rep, st)
+
+
+def gse_encode_vector16(v, k_max: int = 8, stream=None):
+    """NEXT-4 / Alg. 1: a vector in 16-bit GSE-SEM form.  Returns (words, table): words a
+    uint16 array like v (torch tensor on v's device, or numpy), table a numpy uint16 array."""
+    n = v.numel() if _is_torch(v) else np.asarray(v).size
+    if _is_torch(v):
+        import torch
+        words = torch.empty(n, dtype=torch.int16, device=v.device)
+    else:
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        words = np.empty(n, np.uint16)
+    table = np.zeros(16, np.uint16)
+    tl = C.c_int()
+    _check(_lib.gse_encode_vector16(_addr(v), n, k_max, _addr(words), _addr(table), C.byref(tl),
+                                    _stream(v, stream=stream)), "gse_encode_vector16")
+    return words, table[: tl.value].copy()
+
+
+def gse_decode_vector16(words, table, ei_bits: int = 3, stream=None):
+    n = words.numel() if _is_torch(words) else np.asarray(words).size
+    t = np.ascontiguousarray(table, dtype=np.uint16)
+    if _is_torch(words):
+        import torch
+        out = torch.empty(n, dtype=torch.float64, device=words.device)
+    else:
+        words = np.ascontiguousarray(words, dtype=np.uint16)
+        out = np.empty(n, np.float64)
+    _check(_lib.gse_decode_vector16(_addr(words), n, _addr(t) if t.size else None, t.size,
+                                    ei_bits, _addr(out), _stream(words, stream=stream)),
+           "gse_decode_vector16")
+    return out
 
 
 def gse_matrix_free(A: Matrix):

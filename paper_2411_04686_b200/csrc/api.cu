@@ -6,6 +6,7 @@
 #include <string>
 
 #include "gse_internal.cuh"
+#include "vec16.cuh"
 
 namespace gse {
 
@@ -574,6 +575,85 @@ gse_status gse_solve_gmres(gse_matrix A, const double* b, double* x, double tol,
                            int64_t max_iters, const gse_step_schedule* sched,
                            gse_solve_report* rep, void* stream) {
   return solve_common(A, b, x, tol, max_iters, sched, restart, rep, stream, true);
+}
+
+gse_status gse_encode_vector16(const double* v, int64_t n, int k_max, uint16_t* words,
+                               uint16_t* table, int* table_len, void* stream) {
+  if (n < 0 || (n > 0 && (!v || !words)) || !table || !table_len || k_max < 1 ||
+      k_max > V16_KMAX || (k_max & (k_max - 1))) {
+    set_error("invalid arguments (k_max a power of two in [1, 16], non-NULL arrays)");
+    return GSE_ERR_INVALID_ARG;
+  }
+  int dev = 0;
+  if (!(v && is_device_ptr(v, &dev))) cudaGetDevice(&dev);
+  DeviceGuard g(dev);
+  cudaStream_t s = (cudaStream_t)stream;
+  int eb = 0;
+  while ((1 << eb) < k_max) ++eb;
+  Staging st(s);
+  const double* dv = nullptr;
+  uint16_t* dw = nullptr;
+  gse_status rc = st.in(v, (size_t)n, dev, &dv);
+  if (rc == GSE_OK) rc = st.out(words, (size_t)n, dev, false, &dw);
+  if (rc != GSE_OK) return rc;
+  unsigned* hist = dev_alloc_n<unsigned>(2048, s);
+  uint16_t* dt = dev_alloc_n<uint16_t>(V16_KMAX, s);
+  int* dl = dev_alloc_n<int>(1, s);
+  if (!hist || !dt || !dl) return GSE_ERR_OOM;
+  GSE_CUDA_TRY(cudaMemsetAsync(hist, 0, 2048 * sizeof(unsigned), s));
+  const int grid = num_sms(dev) * 4;
+  if (n > 0) v16_hist(dv, nullptr, n, hist, nullptr, grid, s);
+  v16_select(hist, k_max, dt, dl, nullptr, s);
+  if (n > 0) v16_encode(dv, nullptr, n, dt, dl, eb, dw, nullptr, nullptr, grid, s);
+  GSE_CUDA_TRY(cudaGetLastError());
+  rc = st.out_done(words, dw, (size_t)n);
+  if (rc != GSE_OK) return rc;
+  uint16_t ht[V16_KMAX];
+  int hl = 0;
+  GSE_CUDA_TRY(cudaMemcpyAsync(ht, dt, sizeof(ht), cudaMemcpyDeviceToHost, s));
+  GSE_CUDA_TRY(cudaMemcpyAsync(&hl, dl, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GSE_CUDA_TRY(cudaStreamSynchronize(s));
+  dev_free(hist, s);
+  dev_free(dt, s);
+  dev_free(dl, s);
+  for (int i = 0; i < hl; ++i) table[i] = ht[i];
+  *table_len = hl;
+  return st.finish();
+}
+
+gse_status gse_decode_vector16(const uint16_t* words, int64_t n, const uint16_t* table,
+                               int table_len, int ei_bits, double* out, void* stream) {
+  if (n < 0 || (n > 0 && (!words || !out)) || (table_len > 0 && !table) || ei_bits < 0 ||
+      ei_bits > 4 || table_len < 0 || table_len > (1 << ei_bits) || table_len > V16_KMAX) {
+    set_error("invalid arguments (ei_bits in [0, 4], table_len <= 2^ei_bits)");
+    return GSE_ERR_INVALID_ARG;
+  }
+  if (n == 0) return GSE_OK;
+  int dev = 0;
+  if (!is_device_ptr(words, &dev)) cudaGetDevice(&dev);
+  DeviceGuard g(dev);
+  cudaStream_t s = (cudaStream_t)stream;
+  Staging st(s);
+  const uint16_t* dw = nullptr;
+  double* dout = nullptr;
+  gse_status rc = st.in(words, (size_t)n, dev, &dw);
+  if (rc == GSE_OK) rc = st.out(out, (size_t)n, dev, false, &dout);
+  if (rc != GSE_OK) return rc;
+  uint16_t ht[V16_KMAX] = {0};
+  for (int i = 0; i < table_len; ++i) ht[i] = table[i];
+  uint16_t* dt = dev_alloc_n<uint16_t>(V16_KMAX, s);
+  int* dl = dev_alloc_n<int>(1, s);
+  if (!dt || !dl) return GSE_ERR_OOM;
+  GSE_CUDA_TRY(cudaMemcpyAsync(dt, ht, sizeof(ht), cudaMemcpyHostToDevice, s));
+  GSE_CUDA_TRY(cudaMemcpyAsync(dl, &table_len, sizeof(int), cudaMemcpyHostToDevice, s));
+  v16_decode(dw, n, dt, dl, ei_bits, dout, num_sms(dev) * 4, s);
+  GSE_CUDA_TRY(cudaGetLastError());
+  rc = st.out_done(out, dout, (size_t)n);
+  if (rc != GSE_OK) return rc;
+  GSE_CUDA_TRY(cudaStreamSynchronize(s));  // (host table staged through pageable memory)
+  dev_free(dt, s);
+  dev_free(dl, s);
+  return st.finish();
 }
 
 void gse_matrix_free(gse_matrix A) {

@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "gse_internal.cuh"
+#include "vec16.cuh"
 
 namespace gse {
 
@@ -65,6 +66,14 @@ struct SolverWs {
   double *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *b = nullptr, *tmp = nullptr;
   double* V = nullptr;  // GMRES basis (restart + 1) x n
   int V_cols = 0;
+  // 16-bit Krylov basis (NEXT-4): words, per-vector tables, histogram, decoded current vector
+  uint16_t* V16 = nullptr;
+  int V16_cols = 0;
+  uint16_t* vtab = nullptr;  // [V16_cols][V16_KMAX]
+  int* vlen = nullptr;       // [V16_cols]
+  unsigned* vhist = nullptr; // [2048]
+  double* vcur = nullptr;    // [n]
+  int gm_k16 = 0;            // basis format the GMRES graphs were built for
   double* partials = nullptr;
   unsigned* ticket = nullptr;
   SolveCtrl* ctrl = nullptr;
@@ -869,6 +878,93 @@ __global__ void __launch_bounds__(256, 4) k_gm_xupdate(const SolveCtrl* __restri
 
 
 
+// ---------------------------------------------------------------- 16-bit Krylov basis
+// NEXT-4 (R28): v_j stored as 16-bit GSE-SEM words with a table per vector (vec16.cuh);
+// the same MGS / norm / update arithmetic as the FP64 kernels above, on the decoded values.
+constexpr int K16_EB = 3;  // k = 8 shared exponents per basis vector: 3 EI bits, 12 significand bits
+
+__global__ void __launch_bounds__(256, 4) k_gm_mgs16(SolveCtrl* __restrict__ c,
+                                                  double* __restrict__ w,
+                                                  const uint16_t* __restrict__ V16,
+                                                  const uint16_t* __restrict__ vtab,
+                                                  const int* __restrict__ vlen, int64_t n, int i,
+                                                  int j, double* partials, unsigned* ticket) {
+  __shared__ double sci[V16_KMAX], scp[V16_KMAX];
+  pdl_wait();
+  pdl_trigger();
+  if (c->stop) return;
+  const int ip = i > 0 ? i - 1 : 0;
+  load_scales16(vtab + (size_t)i * V16_KMAX, vlen[i], K16_EB, sci);
+  load_scales16(vtab + (size_t)ip * V16_KMAX, vlen[ip], K16_EB, scp);
+  __syncthreads();
+  const int m = c->restart;
+  const double h = i > 0 ? c->H[(i - 1) * m + j] : 0.0;
+  const uint16_t* vi = V16 + (size_t)i * n;
+  const uint16_t* vp = V16 + (size_t)ip * n;
+  double acc = 0.0;
+  GRID_LOOP(q, n) {
+    double wv = w[q];
+    if (i > 0) {
+      wv = __dsub_rn(wv, __dmul_rn(h, dec16(vp[q], scp, K16_EB)));
+      w[q] = wv;
+    }
+    acc = __dadd_rn(acc, __dmul_rn(wv, dec16(vi[q], sci, K16_EB)));
+  }
+  double tot;
+  if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0) c->H[i * m + j] = tot;
+}
+
+__global__ void __launch_bounds__(256, 4) k_gm_last16(SolveCtrl* __restrict__ c, double* ring,
+                                                   double* __restrict__ w,
+                                                   const uint16_t* __restrict__ V16,
+                                                   const uint16_t* __restrict__ vtab,
+                                                   const int* __restrict__ vlen, int64_t n, int j,
+                                                   double* partials, unsigned* ticket) {
+  __shared__ double sc[V16_KMAX];
+  pdl_wait();
+  pdl_trigger();
+  if (c->stop) return;
+  load_scales16(vtab + (size_t)j * V16_KMAX, vlen[j], K16_EB, sc);
+  __syncthreads();
+  const int m = c->restart;
+  const double h = c->H[j * m + j];
+  const uint16_t* vj = V16 + (size_t)j * n;
+  double acc = 0.0;
+  GRID_LOOP(q, n) {
+    const double wv = __dsub_rn(w[q], __dmul_rn(h, dec16(vj[q], sc, K16_EB)));
+    w[q] = wv;
+    acc = __dadd_rn(acc, __dmul_rn(wv, wv));
+  }
+  double tot;
+  if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0)
+    gm_finish(c, ring, j, sqrt(tot), c->H + j, m, c->cs, c->sn, c->g);
+}
+
+// x += sum_i y_i v_i over the decoded 16-bit basis (the oracle's per-element order)
+__global__ void __launch_bounds__(256, 4) k_gm_xupdate16(const SolveCtrl* __restrict__ c,
+                                                      double* __restrict__ x,
+                                                      const uint16_t* __restrict__ V16,
+                                                      const uint16_t* __restrict__ vtab,
+                                                      const int* __restrict__ vlen, int64_t n) {
+  __shared__ double sc[MAX_RESTART][V16_KMAX];
+  pdl_wait();
+  pdl_trigger();
+  const int k = c->k;
+  if (k == 0) return;
+  for (int t = threadIdx.x; t < k * V16_KMAX; t += blockDim.x) {
+    const int i = t / V16_KMAX, e = t % V16_KMAX;
+    sc[i][e] = e < vlen[i] ? ldexp(1.0, (int)vtab[(size_t)i * V16_KMAX + e] - 1023 - (15 - K16_EB))
+                           : 0.0;
+  }
+  __syncthreads();
+  GRID_LOOP(q, n) {
+    double xv = x[q];
+    for (int i = 0; i < k; ++i)
+      xv = __dadd_rn(xv, __dmul_rn(c->y[i], dec16(V16[(size_t)i * n + q], sc[i], K16_EB)));
+    x[q] = xv;
+  }
+}
+
 // ---------------------------------------------------------------- workspace
 // Pinned host mirrors of the control block and the capture streams are process-wide
 // caches: cudaMallocHost / cudaStreamCreate cost milliseconds, and a matrix (with its
@@ -904,7 +1000,8 @@ static cudaStream_t capture_stream(int dev) {
   return g_cap_stream[dev];
 }
 
-static gse_status ensure_ws(Matrix& M, int64_t ring_t, int gm_restart, cudaStream_t s) {
+static gse_status ensure_ws(Matrix& M, int64_t ring_t, int gm_restart, cudaStream_t s,
+                            int k16 = 0) {
   SolverWs*& ws = M.ws;
   const int64_t n = M.rows;
   if (!ws) {
@@ -939,11 +1036,25 @@ static gse_status ensure_ws(Matrix& M, int64_t ring_t, int gm_restart, cudaStrea
     ws->ring = dev_alloc_n<double>((size_t)ws->ring_cap, s);
     if (!ws->ring) return GSE_ERR_OOM;
   }
-  if (gm_restart > 0 && gm_restart + 1 > ws->V_cols) {
+  if (gm_restart > 0 && !k16 && gm_restart + 1 > ws->V_cols) {
     if (ws->V) dev_free(ws->V, s);
     ws->V_cols = gm_restart + 1;
     ws->V = dev_alloc_n<double>((size_t)ws->V_cols * (size_t)(n > 0 ? n : 1), s);
     if (!ws->V) return GSE_ERR_OOM;
+  }
+  if (gm_restart > 0 && k16 && gm_restart + 1 > ws->V16_cols) {
+    for (void* p : {(void*)ws->V16, (void*)ws->vtab, (void*)ws->vlen})
+      if (p) dev_free(p, s);
+    ws->V16_cols = gm_restart + 1;
+    const size_t nn = (size_t)(n > 0 ? n : 1);
+    ws->V16 = dev_alloc_n<uint16_t>((size_t)ws->V16_cols * nn, s);
+    ws->vtab = dev_alloc_n<uint16_t>((size_t)ws->V16_cols * V16_KMAX, s);
+    ws->vlen = dev_alloc_n<int>((size_t)ws->V16_cols, s);
+    if (!ws->vhist) ws->vhist = dev_alloc_n<unsigned>(2048, s);
+    if (!ws->vcur) ws->vcur = dev_alloc_n<double>(nn, s);
+    if (!ws->V16 || !ws->vtab || !ws->vlen || !ws->vhist || !ws->vcur) return GSE_ERR_OOM;
+    GSE_CUDA_TRY(cudaMemsetAsync(ws->vhist, 0, 2048 * sizeof(unsigned), s));
+    GSE_CUDA_TRY(cudaMemsetAsync(ws->vlen, 0, (size_t)ws->V16_cols * sizeof(int), s));
   }
   return GSE_OK;
 }
@@ -958,7 +1069,10 @@ void free_solver_ws(Matrix& M) {
     if (ws->gm_exec[L]) cudaGraphExecDestroy(ws->gm_exec[L]);
     if (ws->gm_graph[L]) cudaGraphDestroy(ws->gm_graph[L]);
   }
-  for (double* p : {ws->x, ws->r, ws->p, ws->q, ws->b, ws->tmp, ws->V, ws->partials, ws->ring})
+  for (double* p : {ws->x, ws->r, ws->p, ws->q, ws->b, ws->tmp, ws->V, ws->partials, ws->ring,
+                    ws->vcur})
+    if (p) dev_free(p, s);
+  for (void* p : {(void*)ws->V16, (void*)ws->vtab, (void*)ws->vlen, (void*)ws->vhist})
     if (p) dev_free(p, s);
   if (ws->ticket) dev_free(ws->ticket, s);
   if (ws->ctrl) dev_free(ws->ctrl, s);
@@ -1361,9 +1475,9 @@ static bool gm_coop_config(const Matrix& M, int64_t n, int* grid, int* E, size_t
   return false;
 }
 
-static gse_status build_gm_graph(Matrix& M, int level, int restart) {
+static gse_status build_gm_graph(Matrix& M, int level, int restart, int k16) {
   SolverWs* ws = M.ws;
-  if (ws->gm_restart != restart) {
+  if (ws->gm_restart != restart || ws->gm_k16 != k16) {
     for (int L = 0; L < 3; ++L) {
       if (ws->gm_exec[L]) cudaGraphExecDestroy(ws->gm_exec[L]);
       if (ws->gm_graph[L]) cudaGraphDestroy(ws->gm_graph[L]);
@@ -1371,6 +1485,7 @@ static gse_status build_gm_graph(Matrix& M, int level, int restart) {
       ws->gm_graph[L] = nullptr;
     }
     ws->gm_restart = restart;
+    ws->gm_k16 = k16;
   }
   if (ws->gm_exec[level - 1]) return GSE_OK;
   cudaStream_t cs = ws->cap_stream;
@@ -1380,6 +1495,37 @@ static gse_status build_gm_graph(Matrix& M, int level, int restart) {
   GSE_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
   gse_status rc = launch_spmv(M, level, ws->x, w, nullptr, cs);
   launch_pdl(k_gm_restart, ws->vgrid, 256, 0, cs, c, ws->b, w, n, ws->partials, ws->ticket, 0);
+  if (k16) {
+    // NEXT-4: v_j = w / den in 16-bit GSE form (histogram -> table -> encode); the decoded
+    // v_j also goes to vcur, the SpMV input of the next step.  Every kernel skips on stop.
+    auto encode16 = [&](int col, const double* den) {
+      v16_hist(w, den, n, ws->vhist, &c->stop, ws->vgrid, cs);
+      v16_select(ws->vhist, 8, ws->vtab + (size_t)col * V16_KMAX, ws->vlen + col, &c->stop, cs);
+      v16_encode(w, den, n, ws->vtab + (size_t)col * V16_KMAX, ws->vlen + col, K16_EB,
+                 ws->V16 + (size_t)col * n, ws->vcur, &c->stop, ws->vgrid, cs);
+    };
+    encode16(0, &c->beta);
+    for (int j = 0; j < restart && rc == GSE_OK; ++j) {
+      rc = launch_spmv_guarded(M, level, ws->vcur, w, &c->stop, cs);
+      for (int i = 0; i <= j; ++i)
+        launch_k(k_gm_mgs16, ws->vgrid, 256, 0, cs, c, w, (const uint16_t*)ws->V16,
+                 (const uint16_t*)ws->vtab, (const int*)ws->vlen, n, i, j, ws->partials,
+                 ws->ticket);
+      launch_k(k_gm_last16, ws->vgrid, 256, 0, cs, c, ws->ring, w, (const uint16_t*)ws->V16,
+               (const uint16_t*)ws->vtab, (const int*)ws->vlen, n, j, ws->partials, ws->ticket);
+      if (j + 1 < restart) encode16(j + 1, &c->hn);
+    }
+    launch_k(k_gm_backsolve, 1, 32, 0, cs, c);
+    launch_k(k_gm_xupdate16, ws->vgrid, 256, 0, cs, c, ws->x, (const uint16_t*)ws->V16,
+             (const uint16_t*)ws->vtab, (const int*)ws->vlen, n);
+    cudaGraph_t g;
+    cudaError_t e = cudaStreamEndCapture(cs, &g);
+    if (rc != GSE_OK) return rc;
+    GSE_CUDA_TRY(e);
+    GSE_CUDA_TRY(cudaGraphInstantiate(&ws->gm_exec[level - 1], g, 0));
+    ws->gm_graph[level - 1] = g;
+    return GSE_OK;
+  }
   launch_pdl(k_gm_scale, ws->vgrid, 256, 0, cs, c, w, ws->V, n, 0);
   int cg_grid = 0, cg_e = 0;
   size_t cg_smem = 0;
@@ -1465,7 +1611,12 @@ gse_status solve_gmres(Matrix& M, const double* b, double* x, double tol, int re
   const int64_t n = M.rows;
   const int stepped = sched.enabled && M.kind == GSE_KIND_GSE;
   int level = (M.kind != GSE_KIND_GSE) ? 3 : sched.start_level;  // FP64/FP16/BF16: one precision
-  gse_status rc = ensure_ws(M, stepped ? sched.t : 0, restart, s);
+  const int k16 = sched.krylov_gse16 ? 1 : 0;
+  if (k16 && M.dist) {
+    set_error("the 16-bit Krylov basis (krylov_gse16) is single-GPU only");
+    return GSE_ERR_WRONG_FORMAT;
+  }
+  gse_status rc = ensure_ws(M, stepped ? sched.t : 0, restart, s, k16);
   if (rc != GSE_OK) return rc;
   SolverWs* ws = M.ws;
   GSE_CUDA_TRY(cudaEventRecord(ws->ev0, s));
@@ -1503,7 +1654,7 @@ gse_status solve_gmres(Matrix& M, const double* b, double* x, double tol, int re
       rc = gm_cycle_dist(M, level, restart, s);
       if (rc != GSE_OK) return rc;
     } else {
-      rc = build_gm_graph(M, level, restart);
+      rc = build_gm_graph(M, level, restart, k16);
       if (rc != GSE_OK) return rc;
       GSE_CUDA_TRY(cudaGraphLaunch(ws->gm_exec[level - 1], s));
     }

@@ -75,6 +75,11 @@ def run(name, A, solver, runs, reps):
     print(json.dumps(out), flush=True)
 
 
+def k16(sched):
+    sched.krylov_gse16 = 1
+    return sched
+
+
 secs = os.environ.get("SECTIONS", "c2v,c4,c5").split(",")
 if "c2v" in secs:
     run("configs[1] shape, varcoef values (3D Poisson 128^3)", gi.poisson3d(128, "varcoef"), "cg",
@@ -89,7 +94,11 @@ if "c4" in secs:
         [("stepped_default", "gse", g.gse_default_schedule("gmres")),
          ("stepped_scaled", "gse", g.gse_default_schedule("gmres", l=300, t=100, m=100)),
          ("stepped_floors", "gse", g.gse_default_schedule("gmres", level_floor=(1e-3, 1e-8))),
-         ("fp64", "fp64", None), ("bf16", "bf16", None)], 2)
+         ("fp64", "fp64", None), ("bf16", "bf16", None),
+         # NEXT-4: the Krylov basis as 16-bit GSE-SEM vectors
+         ("fp64_krylov16", "fp64", k16(g.fixed_schedule(3))),
+         ("stepped_floors_krylov16", "gse",
+          k16(g.gse_default_schedule("gmres", level_floor=(1e-3, 1e-8))))], 2)
 if "c5" in secs:
     N = int(os.environ.get("C5_N", "512"))
     run(f"configs[4] 3D Poisson {N}^3 CG, one GPU", gi.poisson3d(N), "cg",
