@@ -902,13 +902,39 @@ __global__ void __launch_bounds__(256, 4) k_gm_mgs16(SolveCtrl* __restrict__ c,
   const uint16_t* vi = V16 + (size_t)i * n;
   const uint16_t* vp = V16 + (size_t)ip * n;
   double acc = 0.0;
-  GRID_LOOP(q, n) {
-    double wv = w[q];
-    if (i > 0) {
-      wv = __dsub_rn(wv, __dmul_rn(h, dec16(vp[q], scp, K16_EB)));
-      w[q] = wv;
+  if ((n & 3) == 0) {
+    // 4 elements per step: 2 x 16-byte w accesses, one 8-byte access per basis vector
+    // (basis rows are n elements apart: 8-byte aligned when n % 4 == 0); the per-element
+    // operation order is the scalar loop's
+    const int64_t n4 = n >> 2;
+    double2* w2 = reinterpret_cast<double2*>(w);
+    const uint2* vi4 = reinterpret_cast<const uint2*>(vi);
+    const uint2* vp4 = reinterpret_cast<const uint2*>(vp);
+    GRID_LOOP(q, n4) {
+      double2 wa = w2[2 * q], wb = w2[2 * q + 1];
+      const uint2 a = vi4[q];
+      double wv[4] = {wa.x, wa.y, wb.x, wb.y};
+      const uint32_t ai[4] = {a.x & 0xFFFFu, a.x >> 16, a.y & 0xFFFFu, a.y >> 16};
+      if (i > 0) {
+        const uint2 bp = vp4[q];
+        const uint32_t bi[4] = {bp.x & 0xFFFFu, bp.x >> 16, bp.y & 0xFFFFu, bp.y >> 16};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) wv[t] = __dsub_rn(wv[t], __dmul_rn(h, dec16(bi[t], scp, K16_EB)));
+        w2[2 * q] = make_double2(wv[0], wv[1]);
+        w2[2 * q + 1] = make_double2(wv[2], wv[3]);
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) acc = __dadd_rn(acc, __dmul_rn(wv[t], dec16(ai[t], sci, K16_EB)));
     }
-    acc = __dadd_rn(acc, __dmul_rn(wv, dec16(vi[q], sci, K16_EB)));
+  } else {
+    GRID_LOOP(q, n) {
+      double wv = w[q];
+      if (i > 0) {
+        wv = __dsub_rn(wv, __dmul_rn(h, dec16(vp[q], scp, K16_EB)));
+        w[q] = wv;
+      }
+      acc = __dadd_rn(acc, __dmul_rn(wv, dec16(vi[q], sci, K16_EB)));
+    }
   }
   double tot;
   if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0) c->H[i * m + j] = tot;
@@ -930,10 +956,29 @@ __global__ void __launch_bounds__(256, 4) k_gm_last16(SolveCtrl* __restrict__ c,
   const double h = c->H[j * m + j];
   const uint16_t* vj = V16 + (size_t)j * n;
   double acc = 0.0;
-  GRID_LOOP(q, n) {
-    const double wv = __dsub_rn(w[q], __dmul_rn(h, dec16(vj[q], sc, K16_EB)));
-    w[q] = wv;
-    acc = __dadd_rn(acc, __dmul_rn(wv, wv));
+  if ((n & 3) == 0) {
+    const int64_t n4 = n >> 2;
+    double2* w2 = reinterpret_cast<double2*>(w);
+    const uint2* vj4 = reinterpret_cast<const uint2*>(vj);
+    GRID_LOOP(q, n4) {
+      const double2 wa = w2[2 * q], wb = w2[2 * q + 1];
+      const uint2 a = vj4[q];
+      double wv[4] = {wa.x, wa.y, wb.x, wb.y};
+      const uint32_t ai[4] = {a.x & 0xFFFFu, a.x >> 16, a.y & 0xFFFFu, a.y >> 16};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        wv[t] = __dsub_rn(wv[t], __dmul_rn(h, dec16(ai[t], sc, K16_EB)));
+        acc = __dadd_rn(acc, __dmul_rn(wv[t], wv[t]));
+      }
+      w2[2 * q] = make_double2(wv[0], wv[1]);
+      w2[2 * q + 1] = make_double2(wv[2], wv[3]);
+    }
+  } else {
+    GRID_LOOP(q, n) {
+      const double wv = __dsub_rn(w[q], __dmul_rn(h, dec16(vj[q], sc, K16_EB)));
+      w[q] = wv;
+      acc = __dadd_rn(acc, __dmul_rn(wv, wv));
+    }
   }
   double tot;
   if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0)
