@@ -562,10 +562,15 @@ def e2e_measure(args, A, b_h, dev, stream, encode, r0, n_glob):
 def cpu_baseline(args, A, b_h, iters_full):
     import oracle as O
     cores = O.set_threads(len(os.sched_getaffinity(0)))
-    te, ti = oracle_sample(A, b_h, args.cpu_iters)
+    # bounded sample (~20 s of CPU work): 2 iterations first, more when they are cheap
+    te, ti = oracle_sample(A, b_h, 2)
+    k = 2
+    if ti * args.cpu_iters < 20.0:
+        k = args.cpu_iters
+        te, ti = oracle_sample(A, b_h, k)
     t = te + ti * iters_full
     return {"value": 1.0 / t, "unit": unit_for(args.N), "cores": cores, "kind": "oracle",
-            "sample": f"oracle encode of the full matrix ({te:.2f} s) + {args.cpu_iters} level-1 "
+            "sample": f"oracle encode of the full matrix ({te:.2f} s) + {k} level-1 "
                       f"CG iterations ({ti * 1e3:.1f} ms each), extrapolated to the GPU run's "
                       f"{iters_full} iterations; OpenMP rows in SpMV/encode, sequential dots"}
 

@@ -8,6 +8,7 @@ oracle:
   * P-rank stepped CG: iterations within 2 of the single-GPU solve, true residual <= tol.
 """
 import threading
+import time
 
 import numpy as np
 import pytest
@@ -48,13 +49,17 @@ def run_ranks(P, fn):
         except Exception as e:  # pragma: no cover - surfaced below
             errs.append((r, repr(e)))
 
-    th = [threading.Thread(target=body, args=(r,)) for r in range(P)]
+    # daemon threads and a bounded wait: a rank that fails (or a collective that never
+    # completes) fails the test instead of blocking the whole suite
+    th = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(P)]
     for t in th:
         t.start()
+    deadline = time.time() + 180
     for t in th:
-        t.join(timeout=600)
+        t.join(timeout=max(1.0, deadline - time.time()))
+    alive = [r for r, t in enumerate(th) if t.is_alive()]
+    assert not alive and not errs, (alive, errs)
     g.gse_dist_thread_group_free(grp)
-    assert not errs, errs
     return out
 
 
@@ -77,10 +82,10 @@ def test_dist_encode_and_spmv(g, P, name):
         rp, col, val = slab(A, a, b)
         dev = lambda v: torch.from_numpy(v).cuda()
         M = g.gse_encode_dist(D, dev(rp), dev(col), dev(val), a, A.rows, stream=st.cuda_stream)
-        P_ = g.gse_matrix_copy_planes(M)
         ys = [g.gse_spmv(M, dev(x[a:b].copy()), segments=L, stream=st.cuda_stream)
               for L in (1, 2, 3)]
-        torch.cuda.synchronize()
+        st.synchronize()
+        P_ = g.gse_matrix_copy_planes(M)  # host copies after the last collective
         res = (P_, [y.cpu().numpy() for y in ys], M.info)
         M.close()
         return res
@@ -119,7 +124,7 @@ def test_dist_cg(g, P, variant):
         M = g.gse_encode_dist(D, dev(rp), dev(col), dev(val), a, A.rows, stream=st.cuda_stream)
         x, rep = g.gse_solve_cg(M, dev(b[a:bb].copy()), tol=1e-10, sched=sched(),
                                 stream=st.cuda_stream)
-        torch.cuda.synchronize()
+        st.synchronize()
         M.close()
         return x.cpu().numpy(), rep
 
@@ -167,7 +172,7 @@ def test_dist_gmres(g, P, mode):
             s = g.fixed_schedule(3)
         x, rep = g.gse_solve_gmres(M, dev(b[a:bb].copy()), tol=1e-10, sched=s,
                                    stream=st.cuda_stream)
-        torch.cuda.synchronize()
+        st.synchronize()
         M.close()
         return x.cpu().numpy(), rep
 
@@ -213,10 +218,8 @@ def test_dist_per_shard_tables(g, P):
         dev = lambda v: torch.from_numpy(v).cuda()
         M = g.gse_encode_dist(D, dev(rp), dev(col), dev(val), a, A.rows, stream=st.cuda_stream,
                               per_shard_table=True)
-        P_ = g.gse_matrix_copy_planes(M)
-        ys = [g.gse_spmv(M, dev(x[a:b].copy()), segments=L, stream=st.cuda_stream).cpu().numpy()
+        ys = [g.gse_spmv(M, dev(x[a:b].copy()), segments=L, stream=st.cuda_stream)
               for L in (1, 2, 3)]
-        M.close()
         # CG on a D B D-scaled 3D Poisson (the power-law system converges too slowly)
         c, d = rc[r], rc[r + 1]
         rp2, col2, val2 = slab(B, c, d)
@@ -224,7 +227,11 @@ def test_dist_per_shard_tables(g, P):
                                stream=st.cuda_stream, per_shard_table=True)
         _, rep = g.gse_solve_cg(M2, dev(bB[c:d].copy()), tol=1e-10, stream=st.cuda_stream,
                                 sched=g.gse_default_schedule("cg", l=30, t=10, m=10))
-        torch.cuda.synchronize()
+        st.synchronize()
+        # host copies only after this rank's last collective
+        P_ = g.gse_matrix_copy_planes(M)
+        ys = [y.cpu().numpy() for y in ys]
+        M.close()
         M2.close()
         return P_, ys, rep
 
