@@ -1494,6 +1494,17 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
 static bool gm_coop_config(const Matrix& M, int64_t n, int* grid, int* E, size_t* smem) {
   const char* env = getenv("GSE_GM_COOP");
   if ((env && env[0] == '0') || n <= 0) return false;
+  // the dynamic shared-memory attribute is per function and process-wide, and graphs built
+  // for other vector lengths (or other threads' solves) launch with other sizes: set it
+  // once to the largest size this configuration uses (200 KB), never lower
+  static std::once_flag attr_once;
+  static bool attr_ok = false;
+  std::call_once(attr_once, [] {
+    attr_ok = cudaFuncSetAttribute(k_gm_arnoldi, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   200 * 1024) == cudaSuccess;
+    cudaGetLastError();
+  });
+  if (!attr_ok) return false;
   const int sms = num_sms(M.device);
   for (int per = 1; per >= 1; --per) {
     int64_t G = (int64_t)sms * per;
@@ -1502,9 +1513,6 @@ static bool gm_coop_config(const Matrix& M, int64_t n, int* grid, int* E, size_t
     const int64_t e = (n + G * GM_THREADS - 1) / (G * GM_THREADS);
     const size_t sm = (size_t)e * GM_THREADS * sizeof(double);
     if (sm > 200 * 1024) continue;
-    if (cudaFuncSetAttribute(k_gm_arnoldi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
-        cudaSuccess)
-      continue;
     int blocks = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_gm_arnoldi, GM_THREADS, sm) !=
         cudaSuccess)

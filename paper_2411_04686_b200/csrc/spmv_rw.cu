@@ -19,6 +19,9 @@
 #include "spmv_common.cuh"
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <utility>
 
 namespace gse {
 
@@ -311,24 +314,43 @@ __global__ void __launch_bounds__(SPMV_THREADS, RW_MINB(L)) k_spmv_rw(const Spmv
   if constexpr (DOT) finalize_dot(warp_sum(dacc), p.partials, p.ticket, p.dot_result);
 }
 
+// Launch configuration of one kernel instantiation.  The dynamic shared-memory attribute
+// is per function and process-wide, while matrices (and host threads -- one per rank in the
+// thread backend) launch it with different stage sizes: the attribute only ever grows
+// (under a lock), and the occupancy is cached per stage size.
+struct RwLaunchCache {
+  std::mutex mu;
+  int max_smem[64] = {0};
+  std::map<std::pair<int, size_t>, int> grid;  // (device, smem) -> resident CTAs x SMs
+};
+
 template <int L, int RPL, bool DOT, bool FAST, class T>
 static void go_rpl(const Matrix& M, const SpmvParams<T>& p, cudaStream_t s) {
-  static int cache[64] = {0};
-  static uint32_t cache_smem[64] = {0};
+  static RwLaunchCache lc;
   const int dev = M.device < 64 ? M.device : 0;
   const uint32_t N = RPL == 1 ? p.rw_stage : p.rw_stage2;
   const size_t smem = (size_t)SPMV_WARPS * 2 * N * rw_elem_bytes<L>();
   auto kern = k_spmv_rw<L, RPL, DOT, FAST, T>;
-  if (cache_smem[dev] != smem) {  // occupancy depends on the stage size of this matrix
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int blocks = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, SPMV_THREADS, smem);
-    cache[dev] = (blocks < 1 ? 1 : blocks) * num_sms(M.device);
-    cache_smem[dev] = (uint32_t)smem;
+  int cap = 0;
+  {
+    std::lock_guard<std::mutex> lk(lc.mu);
+    if ((int)smem > lc.max_smem[dev]) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      lc.max_smem[dev] = (int)smem;
+    }
+    auto it = lc.grid.find({dev, smem});
+    if (it == lc.grid.end()) {
+      int blocks = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, SPMV_THREADS, smem);
+      cap = (blocks < 1 ? 1 : blocks) * num_sms(M.device);
+      lc.grid[{dev, smem}] = cap;
+    } else {
+      cap = it->second;
+    }
   }
   const int64_t ng = (M.rows + RW_ROWS * RPL - 1) / (RW_ROWS * RPL);
   const int64_t want = (ng + SPMV_WARPS - 1) / SPMV_WARPS;
-  int g = (int)(want < cache[dev] ? want : cache[dev]);
+  int g = (int)(want < cap ? want : cap);
   if (g < 1) g = 1;
   launch_k(kern, g, SPMV_THREADS, smem, s, p);
 }

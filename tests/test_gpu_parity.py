@@ -555,3 +555,51 @@ def test_level_floors_parity(g, solver, floors):
     assert rg["n_switches"] == ro.n_switches == 2
     for a, c in zip(rg["switch_iter"], ro.switch_iter):
         assert abs(a - c) <= 2
+
+
+def test_full_size_c5_sampled_and_cg(g):
+    """configs[4] (3D Poisson 512^3: 134M rows, 938M nnz) at full size on one GPU: planes of
+    sampled row slabs bit-exact against the oracle's encoding of those slabs (the table is
+    the global one), sampled-row SpMV at every level, and the stepped CG to 1e-10 whose
+    true residual is checked with the oracle's FP64 SpMV"""
+    O.set_threads(0)
+    N = 512
+    A = gi.poisson3d(N)
+    n = A.rows
+    dev = lambda a: torch.from_numpy(a).cuda()
+    M = g.gse_encode(dev(A.row_ptr.astype(np.int32)), dev(A.col), dev(A.val), n, n)
+    info = M.info
+    # the whole-matrix table from the oracle's encoding of a slab with every stencil value
+    nnz = A.nnz
+    planes = {k: torch.empty(nnz, dtype=dt, device="cuda") for k, dt in
+              (("col_ei", torch.int32), ("head", torch.int16), ("tail1", torch.int16),
+               ("tail2", torch.int32))}
+    st = g._lib.gse_matrix_copy_planes(M.handle, planes["col_ei"].data_ptr(), None,
+                                       planes["head"].data_ptr(), planes["tail1"].data_ptr(),
+                                       planes["tail2"].data_ptr(), None, None)
+    assert st == 0
+    rng = np.random.default_rng(1)
+    slabs = [0, n // 2, n - N * N] + list(rng.integers(0, n - N * N, 3))
+    x = gi.uniform_vec(n, seed=5)
+    xt = dev(x)
+    ys = {L: g.gse_spmv(M, xt, segments=L).cpu().numpy() for L in (1, 2, 3)}
+    for r0 in slabs:
+        r1 = r0 + N * N
+        sl = slice(A.row_ptr[r0], A.row_ptr[r1])
+        rp = (A.row_ptr[r0:r1 + 1] - A.row_ptr[r0]).astype(np.int64)
+        R = O.encode_csr(r1 - r0, n, rp, A.col[sl], A.val[sl])
+        assert list(R.table) == list(info["table"])  # const Poisson: the slab has every value
+        for k in ("col_ei", "head", "tail1", "tail2"):
+            got = planes[k][sl.start:sl.stop].cpu().numpy().view(getattr(R, k).dtype)
+            assert np.array_equal(got, getattr(R, k)), (k, r0)
+        for L in (1, 2, 3):
+            yo = O.spmv_gse(R, x, L)
+            assert np.all(np.abs(ys[L][r0:r1] - yo) <= spmv_bound(R, x, L, 1e-12)), (L, r0)
+    del planes
+    b = gi.ones_rhs(A)
+    xs, rep = g.gse_solve_cg(M, dev(b), tol=1e-10, max_iters=20000,
+                             sched=g.gse_default_schedule("cg"))
+    assert rep["converged"] and rep["iters_per_level"][0] == rep["iterations"]
+    F = O.fp64_csr(n, n, A.row_ptr, A.col, A.val)
+    res = np.linalg.norm(b - O.spmv_fp64(F, xs.cpu().numpy())) / np.linalg.norm(b)
+    assert res <= 1e-10 * 1.01
