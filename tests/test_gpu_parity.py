@@ -603,3 +603,38 @@ def test_full_size_c5_sampled_and_cg(g):
     F = O.fp64_csr(n, n, A.row_ptr, A.col, A.val)
     res = np.linalg.norm(b - O.spmv_fp64(F, xs.cpu().numpy())) / np.linalg.norm(b)
     assert res <= 1e-10 * 1.01
+
+
+def test_concurrent_spmv_threads(g):
+    """include/gse.h: concurrent gse_spmv on different streams is safe -- here from host
+    threads on matrices whose row-walk stages differ in size (the per-function dynamic
+    shared-memory attribute must never drop below a concurrent launch's need)"""
+    import threading
+    mats = [gi.poisson3d(40, "varcoef"), gi.convdiff3d(24), gi.poisson2d(64, "varcoef"),
+            gi.powerlaw_spd(20000, seed=3)]
+    Ms = [g.gse_encode(A.row_ptr, A.col, A.val, A.rows, A.cols) for A in mats]
+    xs = [torch.from_numpy(gi.uniform_vec(A.cols, seed=i)).cuda() for i, A in enumerate(mats)]
+    ref = {(i, L): g.gse_spmv(Ms[i], xs[i], segments=L).cpu().numpy()
+           for i in range(len(mats)) for L in (1, 2, 3)}
+    errs = []
+
+    def body(t):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                for it in range(30):
+                    i = (t + it) % len(mats)
+                    L = 1 + (it % 3)
+                    y = g.gse_spmv(Ms[i], xs[i], segments=L)
+                    st.synchronize()
+                    if not np.array_equal(y.cpu().numpy(), ref[(i, L)]):
+                        errs.append((t, it, i, L))
+        except Exception as e:  # pragma: no cover
+            errs.append((t, repr(e)))
+
+    th = [threading.Thread(target=body, args=(t,), daemon=True) for t in range(6)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not any(t.is_alive() for t in th) and not errs, errs
