@@ -11,6 +11,19 @@ peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspa
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 tag = os.environ.get("TAG", "")
 
+def timeit_steady(fn, reps=80):
+    """back-to-back launches (as in the CG loop), average per launch"""
+    fn()
+    flush.fill_(0); flush.sum()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e-3 / reps
+
+
 def timeit(fn, reps=30):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
     fn()
@@ -47,4 +60,8 @@ for name, mk in mats.items():
         res[f"L{L}f32"] = round(b / t / 1e9, 1)
     t = timeit(lambda: g.gse_spmv(F, x, y, segments=3))
     res["fp64"] = round((nnz * 12 + 4 * (n + 1) + 16 * n) / t / 1e9, 1)
+    if os.environ.get("AB_STEADY", "1") == "1":
+        for L, s_l in ((1, 2), (2, 4), (3, 8)):
+            t = timeit_steady(lambda: g.gse_spmv(M, x, y, segments=L))
+            res[f"L{L}_steady"] = round((nnz * (4 + s_l) + 4 * (n + 1) + 16 * n) / t / 1e9, 1)
     print(json.dumps({"tag": tag, "mat": name, "nnz": nnz, "GBps": res, "peak": peak}), flush=True)
