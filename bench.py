@@ -333,6 +333,13 @@ def run_gse(args, world, rank, local, pg):
             "fp64_csr_cg": extra["cg_fp64_ms"],
             "speedup_vs_fp64_csr": extra["cg_fp64_ms"] / extra["cg_gse_ms"]}
         line["time_to_1e-10_ms"]["half_storage_cg"] = extra["cg_half"]
+        # P:534-537 Eq. 7: GSE-SEM* = TIME_FP16 / ITERS_FP16 x ITERS_GSE -- the stepped solve
+        # with the FP16 solver's per-iteration time, i.e. without the decode overhead
+        h16 = extra["cg_half"]["fp16"]
+        if h16["iterations"] > 0:
+            star = h16["ms"] / h16["iterations"] * rep["iterations"]
+            line["time_to_1e-10_ms"]["gse_sem_star_eq7_ms"] = star
+            line["time_to_1e-10_ms"]["gse_sem_star_speedup_vs_fp64_csr"] = extra["cg_fp64_ms"] / star
         line["solve"]["fp64_iterations"] = extra["cg_fp64_iters"]
         line["spmv_sweep"] = extra["spmv"]
         line["spmv_sweep_steady"] = extra["spmv_steady"]
