@@ -462,14 +462,13 @@ gse_status gse_spmv(gse_matrix A, const double* x, double* y, int segments, void
   gse_status rc = st.in(x, (size_t)xlen, M.device, &dx);
   if (rc == GSE_OK) rc = st.out(y, (size_t)M.rows, M.device, false, &dy);
   if (rc != GSE_OK) return rc;
-  if (M.dist) {  // owned entries -> x_ext, halo exchange, SpMV over the local column space
+  if (M.dist) {  // owned entries -> x_ext, halo exchange (interior rows overlapped), SpMV
     double* xe = dist_xext(M);
     if (xlen) GSE_CUDA_TRY(cudaMemcpyAsync(xe, dx, 8 * xlen, cudaMemcpyDeviceToDevice, s));
-    rc = dist_halo_exchange(M, xe, s);
-    if (rc != GSE_OK) return rc;
-    dx = xe;
+    rc = dist_spmv(M, segments, xe, dy, nullptr, s, nullptr);
+  } else {
+    rc = launch_spmv(M, segments, dx, dy, nullptr, s);
   }
-  rc = launch_spmv(M, segments, dx, dy, nullptr, s);
   if (rc != GSE_OK) return rc;
   rc = st.out_done(y, dy, (size_t)M.rows);
   if (rc != GSE_OK) return rc;

@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -319,7 +320,57 @@ struct DistCtx {
   double* d_send_buf = nullptr;
   double* d_xext = nullptr;         // n_local + n_halo, used by gse_spmv on this matrix
   int64_t send_total = 0;
+  // halo / interior overlap (row-walk matrices): rows [ov_i0, ov_i1) read owned columns only
+  // and run on `side` while the halo is exchanged; the other rows follow on the caller's
+  // stream.  Three partial dots (interior, top, bottom) summed in that order.
+  bool overlap = false;
+  int64_t ov_i0 = 0, ov_i1 = 0;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_x = nullptr, ev_int = nullptr;
+  DotOut part[3];
+  double* part_buf = nullptr;
+  unsigned* part_ticket = nullptr;
 };
+
+// first row / end of the longest run of rows whose columns are all owned (< n_local),
+// aligned inward to 64 rows; empty when shorter than max(4096, n_local / 8)
+static void interior_range(int64_t n_local, const std::vector<int64_t>& rp,
+                           const std::vector<int32_t>& local_col, int64_t* i0, int64_t* i1) {
+  int64_t best0 = 0, best1 = 0, run0 = 0;
+  for (int64_t r = 0; r <= n_local; ++r) {
+    bool interior = false;
+    if (r < n_local) {
+      interior = true;
+      for (int64_t j = rp[r]; j < rp[r + 1]; ++j)
+        if (local_col[(size_t)j] >= n_local) {
+          interior = false;
+          break;
+        }
+    }
+    if (!interior) {
+      if (r - run0 > best1 - best0) {
+        best0 = run0;
+        best1 = r;
+      }
+      run0 = r + 1;
+    }
+  }
+  int64_t a = (best0 + 63) / 64 * 64, b = best1 / 64 * 64;
+  const int64_t min_len = n_local / 8 > 4096 ? n_local / 8 : 4096;
+  if (b - a < min_len) a = b = 0;
+  *i0 = a;
+  *i1 = b;
+}
+
+__global__ void k_add_parts(const double* a, const double* b, const double* c, int use_b,
+                            int use_c, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = *a;
+    if (use_b) s += *b;
+    if (use_c) s += *c;
+    *out = s;
+  }
+}
 
 }  // namespace gse
 
@@ -349,6 +400,40 @@ gse_status dist_halo_exchange(const Matrix& M, double* x_ext, cudaStream_t s) {
                            D->recv_cnt, D->recv_off, s);
 }
 
+gse_status dist_spmv(const Matrix& M, int level, double* xe, double* y, const DotOut* dot,
+                     cudaStream_t s, const int* stop) {
+  DistCtx* D = M.dist;
+  if (!D->overlap || getenv("GSE_NO_OVERLAP")) {
+    gse_status rc = dist_halo_exchange(M, xe, s);
+    if (rc != GSE_OK) return rc;
+    return launch_spmv(M, level, xe, y, dot, s, stop);
+  }
+  // interior rows on the side stream as soon as the owned entries are ready
+  GSE_CUDA_TRY(cudaEventRecord(D->ev_x, s));
+  GSE_CUDA_TRY(cudaStreamWaitEvent(D->side, D->ev_x, 0));
+  gse_status rc = launch_spmv_rows(M, level, xe, y, dot ? &D->part[0] : nullptr, D->side, stop,
+                                   D->ov_i0, D->ov_i1);
+  if (rc != GSE_OK) return rc;
+  GSE_CUDA_TRY(cudaEventRecord(D->ev_int, D->side));
+  rc = dist_halo_exchange(M, xe, s);
+  if (rc != GSE_OK) return rc;
+  const int64_t n = M.rows;
+  const bool top = D->ov_i0 > 0, bot = D->ov_i1 < n;
+  if (top) rc = launch_spmv_rows(M, level, xe, y, dot ? &D->part[1] : nullptr, s, stop, 0, D->ov_i0);
+  if (rc == GSE_OK && bot)
+    rc = launch_spmv_rows(M, level, xe, y, dot ? &D->part[2] : nullptr, s, stop, D->ov_i1, n);
+  if (rc != GSE_OK) return rc;
+  GSE_CUDA_TRY(cudaStreamWaitEvent(s, D->ev_int, 0));
+  if (dot) {  // fixed order: interior, top, bottom
+    const double* a = D->part[0].result;
+    const double* b = top ? D->part[1].result : D->part[2].result;
+    const double* c = D->part[2].result;
+    k_add_parts<<<1, 32, 0, s>>>(a, b, c, (top || bot) ? 1 : 0, (top && bot) ? 1 : 0, dot->result);
+    GSE_CUDA_TRY(cudaGetLastError());
+  }
+  return GSE_OK;
+}
+
 gse_status dist_allreduce_sum(const Matrix& M, double* d_vals, int count, cudaStream_t s) {
   if (!M.dist) return GSE_OK;
   return M.dist->comm->allreduce_sum_f64(d_vals, count, s);
@@ -365,6 +450,14 @@ void free_dist(Matrix& M) {
   dev_free(D->d_send_idx, nullptr);
   dev_free(D->d_send_buf, nullptr);
   dev_free(D->d_xext, nullptr);
+  if (D->side) {
+    cudaStreamSynchronize(D->side);
+    cudaStreamDestroy(D->side);
+  }
+  if (D->ev_x) cudaEventDestroy(D->ev_x);
+  if (D->ev_int) cudaEventDestroy(D->ev_int);
+  if (D->part_buf) dev_free(D->part_buf, nullptr);
+  if (D->part_ticket) dev_free(D->part_ticket, nullptr);
   delete D;
   M.dist = nullptr;
 }
@@ -639,8 +732,40 @@ gse_status gse_encode_dist(gse_dist Dh, const gse_csr_f64* A, int64_t row_begin,
   }
   if (so)
     GSE_CUDA_TRY(cudaMemcpyAsync(D->d_send_idx, send_idx.data(), 4 * so, cudaMemcpyHostToDevice, s));
-  GSE_CUDA_TRY(cudaStreamSynchronize(s));
   M->dist = D;
+  // halo / interior overlap for row-walk matrices (local decision: every rank issues the
+  // same collectives either way)
+  if (M->spmv_mode == SPMV_RW && n_local > 0 && !getenv("GSE_NO_OVERLAP")) {
+    std::vector<int64_t> rp_h((size_t)n_local + 1);
+    if (A->row_ptr_64) {
+      GSE_CUDA_TRY(cudaMemcpyAsync(rp_h.data(), A->row_ptr, 8 * rp_h.size(), cudaMemcpyDefault, s));
+    } else {
+      std::vector<int32_t> t(rp_h.size());
+      GSE_CUDA_TRY(cudaMemcpyAsync(t.data(), A->row_ptr, 4 * t.size(), cudaMemcpyDefault, s));
+      GSE_CUDA_TRY(cudaStreamSynchronize(s));
+      for (size_t i = 0; i < t.size(); ++i) rp_h[i] = t[i];
+    }
+    GSE_CUDA_TRY(cudaStreamSynchronize(s));
+    interior_range(n_local, rp_h, local_col, &D->ov_i0, &D->ov_i1);
+    if (D->ov_i1 > D->ov_i0) {
+      const int np = 2048;  // partials per part (>= any persistent SpMV grid)
+      D->part_buf = dev_alloc_n<double>((size_t)3 * (np + 1), s);
+      D->part_ticket = dev_alloc_n<unsigned>(4, s);
+      if (!D->part_buf || !D->part_ticket) return GSE_ERR_OOM;
+      GSE_CUDA_TRY(cudaMemsetAsync(D->part_ticket, 0, 16, s));
+      GSE_CUDA_TRY(cudaMemsetAsync(D->part_buf, 0, 8 * (size_t)3 * (np + 1), s));
+      for (int k = 0; k < 3; ++k) {
+        D->part[k].partials = D->part_buf + (size_t)k * (np + 1);
+        D->part[k].result = D->part_buf + (size_t)k * (np + 1) + np;
+        D->part[k].ticket = D->part_ticket + k;
+      }
+      GSE_CUDA_TRY(cudaStreamCreateWithFlags(&D->side, cudaStreamNonBlocking));
+      GSE_CUDA_TRY(cudaEventCreateWithFlags(&D->ev_x, cudaEventDisableTiming));
+      GSE_CUDA_TRY(cudaEventCreateWithFlags(&D->ev_int, cudaEventDisableTiming));
+      D->overlap = true;
+    }
+  }
+  GSE_CUDA_TRY(cudaStreamSynchronize(s));
   return GSE_OK;
 }
 

@@ -178,6 +178,9 @@ gse_status launch_spmv(const Matrix& M, int level, const double* x, double* y,
                        const DotOut* dot, cudaStream_t s, const int* stop = nullptr);
 gse_status launch_spmv_guarded(const Matrix& M, int level, const double* x, double* y,
                                const int* stop, cudaStream_t s);
+gse_status launch_spmv_rows(const Matrix& M, int level, const double* x, double* y,
+                            const DotOut* dot, cudaStream_t s, const int* stop, int64_t r0,
+                            int64_t r1);
 gse_status launch_spmv_f32(const Matrix& M, int level, const float* x, float* y,
                            cudaStream_t s);
 
@@ -191,6 +194,10 @@ void free_solver_ws(Matrix& M);
 
 // dist.cu
 gse_status dist_halo_exchange(const Matrix& M, double* x_local_ext, cudaStream_t s);
+// SpMV of a distributed matrix on x_ext (owned entries in place): the halo exchange, with the
+// interior rows' SpMV overlapped on a side stream when the matrix has an interior row range
+gse_status dist_spmv(const Matrix& M, int level, double* x_ext, double* y, const DotOut* dot,
+                     cudaStream_t s, const int* stop);
 gse_status dist_allreduce_sum(const Matrix& M, double* d_vals, int count, cudaStream_t s);
 gse_status comm_allreduce_u64(Comm* c, unsigned long long* d, int count, cudaStream_t s);
 gse_status comm_any(Comm* c, int local_flag, int* any);  // host: OR over ranks

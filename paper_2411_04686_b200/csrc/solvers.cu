@@ -1269,16 +1269,13 @@ static void log_switch(gse_solve_report& rep, int64_t j, int lvl) {
 // owned entries are copied to x_ext and the halo is exchanged first
 static gse_status spmv_local(Matrix& M, int level, const double* v, double* out,
                              const DotOut* dot, cudaStream_t s, const int* stop = nullptr) {
-  const double* in = v;
   if (M.dist) {
     double* xe = dist_xext(M);
     if (v != xe)
       GSE_CUDA_TRY(cudaMemcpyAsync(xe, v, 8 * M.rows, cudaMemcpyDeviceToDevice, s));
-    gse_status rc = dist_halo_exchange(M, xe, s);
-    if (rc != GSE_OK) return rc;
-    in = xe;
+    return dist_spmv(M, level, xe, out, dot, s, stop);
   }
-  return launch_spmv(M, level, in, out, dot, s, stop);
+  return launch_spmv(M, level, v, out, dot, s, stop);
 }
 
 // r = b - A_level x (p = r when p != null); *out = ||r||^2 (allreduced over ranks)
@@ -1386,9 +1383,7 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
       do {
         DotOut d = dot_to(ws, &ws->ctrl->pq);
         for (int bt = 0; bt < 16; ++bt) {
-          rc = dist_halo_exchange(M, ws->p, s);
-          if (rc != GSE_OK) return rc;
-          rc = launch_spmv(M, level, ws->p, ws->q, &d, s, &ws->ctrl->event);
+          rc = dist_spmv(M, level, ws->p, ws->q, &d, s, &ws->ctrl->event);
           if (rc != GSE_OK) return rc;
           rc = dist_allreduce_sum(M, &ws->ctrl->pq, 1, s);
           if (rc != GSE_OK) return rc;

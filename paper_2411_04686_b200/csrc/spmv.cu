@@ -31,6 +31,7 @@ static SpmvParams<T> make_params(const Matrix& M, int level, const T* x, T* y,
                    ? ((1u << (32 - M.ei_bits)) - 1u)
                    : 0xFFFFFFFFu;
   p.x = x;
+  p.xd = x;
   p.y = y;
   p.partials = dot ? dot->partials : nullptr;
   p.ticket = dot ? dot->ticket : nullptr;
@@ -80,6 +81,30 @@ gse_status launch_spmv(const Matrix& M, int level, const double* x, double* y,
   SpmvParams<double> p = make_params<double>(M, level, x, y, dot);
   p.stop = stop;
   dispatch<double>(M, level, dot != nullptr, p, s);
+  GSE_CUDA_TRY(cudaGetLastError());
+  return GSE_OK;
+}
+
+// y[r0:r1) = (A_L x)[r0:r1): the row-walk kernel over a row view (row_ptr + r0, y + r0;
+// the gathers still index the whole x).  r0 must be a multiple of 64 so the view's groups
+// are the matrix's own groups (their staged spans are what rw_span bounds).
+gse_status launch_spmv_rows(const Matrix& M, int level, const double* x, double* y,
+                            const DotOut* dot, cudaStream_t s, const int* stop, int64_t r0,
+                            int64_t r1) {
+  if (r1 <= r0) return GSE_OK;
+  if (M.spmv_mode != SPMV_RW || (r0 & 63) || r1 > M.rows) {
+    set_error("internal: row views need a row-walk matrix and 64-aligned starts");
+    return GSE_ERR_INVALID_ARG;
+  }
+  SpmvParams<double> p = make_params<double>(M, level, x, y, dot);
+  p.stop = stop;
+  p.row_ptr = M.row_ptr + r0;
+  p.rows = (uint32_t)(r1 - r0);
+  p.y = y + r0;
+  p.xd = x + r0;
+  launch_rw<double>(M, level, dot != nullptr,
+                    M.kind == GSE_KIND_GSE && M.htab.fast64[(level >= 1 && level <= 3 ? level : 3) - 1],
+                    p, s);
   GSE_CUDA_TRY(cudaGetLastError());
   return GSE_OK;
 }

@@ -101,6 +101,7 @@ struct SpmvParams {
   int ei_shift;       // 32 - ei_bits
   uint32_t col_mask;  // (1 << (32 - ei_bits)) - 1, or ~0u
   const T* __restrict__ x;
+  const T* __restrict__ xd;  // x of the launch's rows for the fused dot (x + first row)
   T* __restrict__ y;
   double* partials;
   unsigned* ticket;

@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, RW_MINB(L)) k_spmv_rw(const Spmv
       const uint32_t row = r0 + 32 * k + lane;
       if (row < rows) {
         p.y[row] = sa;
-        if (DOT) dacc += (double)p.x[row] * (double)sa;
+        if (DOT) dacc += (double)p.xd[row] * (double)sa;
       }
     }
     __syncwarp();

@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, GSE_SP_MINB) k_spmv_sp(const Spm
       acc = warp_sum(acc);
       if (lane == 0) {
         p.y[r0] = acc;
-        if (DOT) dacc += (double)p.x[r0] * (double)acc;
+        if (DOT) dacc += (double)p.xd[r0] * (double)acc;
       }
     } else {
       T v[EPL];
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, GSE_SP_MINB) k_spmv_sp(const Spm
       uint32_t rpl = 0;
       double xr = 0.0;
       if (pre && (uint32_t)lane <= nrows) rpl = p.row_ptr[r0 + lane];
-      if (DOT && pre && (uint32_t)lane < nrows) xr = (double)p.x[r0 + lane];
+      if (DOT && pre && (uint32_t)lane < nrows) xr = (double)p.xd[r0 + lane];
       products<L, SIDE, FAST, T>(p, sd64, sd32, sc64, sc32, s + lane, e, v);
 #pragma unroll
       for (int k = 0; k < EPL; ++k) wp[lane + 32 * k] = v[k];
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, GSE_SP_MINB) k_spmv_sp(const Spm
           if (!pre) {
             ra = p.row_ptr[r0 + rr];
             rb = p.row_ptr[r0 + rr + 1];
-            if (DOT) xrow = (double)p.x[r0 + rr];
+            if (DOT) xrow = (double)p.xd[r0 + rr];
           }
           for (uint32_t j = ra - s + sub; j < rb - s; j += lpr) sum += wp[j];
         }

@@ -254,3 +254,52 @@ def test_dist_per_shard_tables(g, P):
         assert rep["converged"] and rep["rel_residual_true"] <= 1e-10
         assert rep["iterations"] == outs[0][2]["iterations"]
     assert len(set(tables)) > 1  # the shards really chose different tables
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_dist_overlap_interior_rows(g, P):
+    """slabs large enough for the halo / interior overlap (row-walk matrices: the interior
+    rows' SpMV runs on a side stream during the exchange, the boundary rows after it, three
+    partial dots summed in a fixed order): SpMV within the oracle's tolerance at every
+    level, CG within 2 iterations of the single-GPU solve, GMRES converging"""
+    A = gi.poisson3d(40, "varcoef")
+    R = O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+    x = gi.uniform_vec(A.cols, seed=9)
+    b = gi.ones_rhs(A)
+    M1 = g.gse_encode(A.row_ptr, A.col, A.val, A.rows, A.cols)
+    sched = lambda: g.gse_default_schedule("cg", l=30, t=10, m=10)
+    _, r1 = g.gse_solve_cg(M1, b, tol=1e-10, sched=sched())
+    rr = partition(A.rows, P)
+
+    def fn(r, D, st):
+        a, bb = rr[r], rr[r + 1]
+        rp, col, val = slab(A, a, bb)
+        dev = lambda v: torch.from_numpy(v).cuda()
+        M = g.gse_encode_dist(D, dev(rp), dev(col), dev(val), a, A.rows, stream=st.cuda_stream)
+        ys = [g.gse_spmv(M, dev(x[a:bb].copy()), segments=L, stream=st.cuda_stream)
+              for L in (1, 2, 3)]
+        xs, rep = g.gse_solve_cg(M, dev(b[a:bb].copy()), tol=1e-10, sched=sched(),
+                                 stream=st.cuda_stream)
+        xg, repg = g.gse_solve_gmres(M, dev(b[a:bb].copy()), tol=1e-10, stream=st.cuda_stream,
+                                     sched=g.gse_default_schedule("gmres", l=30, t=10, m=10))
+        st.synchronize()
+        out = ([y.cpu().numpy() for y in ys], xs.cpu().numpy(), rep, repg, M.info["spmv_mode"])
+        M.close()
+        return out
+
+    outs = run_ranks(P, fn)
+    absR = O.GseCsr(R.rows, R.cols, R.nnz, R.row_ptr, R.col_ei, R.side_ei,
+                    R.head & np.uint16(0x7FFF), R.tail1, R.tail2, R.table, R.ei_bits,
+                    R.ei_in_column)
+    for r, (ys, xs, rep, repg, mode) in enumerate(outs):
+        assert mode == 1  # row walk: the overlap applies
+        a, bb = rr[r], rr[r + 1]
+        for L, y in zip((1, 2, 3), ys):
+            yo = O.spmv_gse(R, x, L)[a:bb]
+            assert np.all(np.abs(y - yo) <= 1e-12 * O.spmv_gse(absR, np.abs(x), L)[a:bb]), (r, L)
+        assert rep["iterations"] == outs[0][2]["iterations"]
+        assert abs(rep["iterations"] - r1["iterations"]) <= 2, (rep, r1)
+        assert repg["converged"] and repg["iterations"] == outs[0][3]["iterations"]
+    x_all = np.concatenate([o[1] for o in outs])
+    F = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+    assert np.linalg.norm(b - O.spmv_fp64(F, x_all)) / np.linalg.norm(b) <= 1e-10 * 1.01
