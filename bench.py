@@ -357,6 +357,7 @@ def run_gse(args, world, rank, local, pg):
                      "timing": "one launch between CUDA events, L2 flushed before it"}}
     if rank == 0 and world == 1 and not args.no_c3 and not args.no_sweep:
         line["spmv_sweep_c3"] = c3_sweep(args, dev, stream, flush, hbm_peak)
+        line["gmres_c4"] = c4_gmres(dev, stream, flush)
     print(json.dumps(line), flush=True)
 
 
@@ -527,6 +528,54 @@ def c3_sweep(args, dev, stream, flush, hbm_peak):
         H = g.gse_half_matrix(rp, col, val, n, n, kind=k)
         rec(k, lambda: g.gse_spmv(H, x, y, segments=3), nnz * 6 + rows_b + 16 * n)
         H.close()
+    del rp, col, val
+    torch.cuda.empty_cache()
+    return out
+
+
+def c4_gmres(dev, stream, flush):
+    """configs[3]: conv-diff 256^3, restarted GMRES(30) to a true relative residual of 1e-10
+    (one solve per variant, CUDA events, L2 flushed before each): FP64-CSR, stepped GSE with
+    the paper-default schedule, with the R17 level floors, and with the 16-bit Krylov basis
+    (NEXT-4)."""
+    import torch
+    import gse_inputs as gi
+    import paper_2411_04686_b200 as g
+    A = gi.convdiff3d(256)
+    n = A.rows
+    rp = torch.from_numpy(A.row_ptr.astype(np.int32)).to(dev)
+    col = torch.from_numpy(A.col).to(dev)
+    val = torch.from_numpy(A.val).to(dev)
+    b = torch.from_numpy(gi.ones_rhs(A)).to(dev)
+    del A
+    x = torch.zeros(n, dtype=torch.float64, device=dev)
+    out = {"n": n, "tol": 1e-10, "restart": 30}
+    k16 = g.gse_default_schedule("gmres", level_floor=(1e-3, 1e-8))
+    k16.krylov_gse16 = 1
+    runs = [("fp64_csr", "fp64", None),
+            ("stepped_default", "gse", g.gse_default_schedule("gmres")),
+            ("stepped_floors", "gse", g.gse_default_schedule("gmres", level_floor=(1e-3, 1e-8))),
+            ("stepped_floors_krylov16", "gse", k16)]
+    for name, kind, sched in runs:
+        M = (g.gse_fp64_matrix(rp, col, val, n, n) if kind == "fp64"
+             else g.gse_encode(rp, col, val, n, n))
+        x.zero_()
+        g.gse_solve_gmres(M, b, x, tol=1e-10, sched=sched)  # graphs built outside the timing
+        x.zero_()
+        l2_flush(flush, 0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rep = g.gse_solve_gmres(M, b, x, tol=1e-10, sched=sched)[1]
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1)
+        out[name] = {"ms": round(t, 1), "iterations": rep["iterations"],
+                     "iters_per_level": rep["iters_per_level"],
+                     "rel_residual_true": rep["rel_residual_true"]}
+        M.close()
+    f = out["fp64_csr"]["ms"]
+    for name, _, _ in runs[1:]:
+        out[name]["speedup_vs_fp64_csr"] = round(f / out[name]["ms"], 3)
     del rp, col, val
     torch.cuda.empty_cache()
     return out
