@@ -683,12 +683,16 @@ __device__ __forceinline__ double gm_grid_total(double part, double* partials, i
   return *s_tot;
 }
 
+// GW = false: w's slice lives in shared memory (vectors up to ~3.8M rows); GW = true (longer
+// vectors): w stays in global memory -- the same HBM traffic as the per-step kernels, but
+// one kernel per Arnoldi step (grid barriers instead of j + 3 kernel boundaries)
+template <bool GW>
 __global__ void __launch_bounds__(GM_THREADS, 1) k_gm_arnoldi(SolveCtrl* __restrict__ c,
                                                              double* ring,
-                                                             const double* __restrict__ w_in,
+                                                             double* __restrict__ w_in,
                                                              double* __restrict__ V, int64_t n,
                                                              int j, int E, double* partials) {
-  extern __shared__ double wsm[];  // E * GM_THREADS: this thread's slice of w at [k * GM_THREADS + t]
+  extern __shared__ double wsm_[];  // !GW: E * GM_THREADS, this thread's slice at [k * GM_THREADS + t]
   __shared__ unsigned long long sctrl[CTRL_HEAD_WORDS];
   __shared__ double s_col[MAX_RESTART + 1], s_cs[MAX_RESTART], s_sn[MAX_RESTART];
   __shared__ double s_g[MAX_RESTART + 1];
@@ -709,9 +713,18 @@ __global__ void __launch_bounds__(GM_THREADS, 1) k_gm_arnoldi(SolveCtrl* __restr
   }
   const int64_t T = (int64_t)gridDim.x * GM_THREADS;
   const int64_t e0 = (int64_t)blockIdx.x * GM_THREADS + tid;
-  for (int k = 0; k < E; ++k) {
-    const int64_t e = e0 + k * T;
-    wsm[k * GM_THREADS + tid] = e < n ? w_in[e] : 0.0;
+  // element k of this thread's slice: e0 + k T, stored at W(k)
+  auto W = [&](int k) -> double& {
+    if constexpr (GW)
+      return w_in[e0 + (int64_t)k * T];
+    else
+      return wsm_[k * GM_THREADS + tid];
+  };
+  if constexpr (!GW) {
+    for (int k = 0; k < E; ++k) {
+      const int64_t e = e0 + k * T;
+      wsm_[k * GM_THREADS + tid] = e < n ? w_in[e] : 0.0;
+    }
   }
   double h_prev = 0.0;
   for (int i = 0; i <= j; ++i) {
@@ -720,22 +733,23 @@ __global__ void __launch_bounds__(GM_THREADS, 1) k_gm_arnoldi(SolveCtrl* __restr
     double acc = 0.0;
     // batches of 4 slice elements: all 8 loads issued before the dependent arithmetic
     for (int k0 = 0; k0 < E; k0 += 4) {
-      double a[4], bp[4];
+      double a[4], bp[4], wq[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int64_t e = e0 + (int64_t)(k0 + q) * T;
         const bool in = k0 + q < E && e < n;
         a[q] = in ? __ldg(vi + e) : 0.0;
         bp[q] = (in && i > 0) ? __ldg(vp + e) : 0.0;
+        if constexpr (GW) wq[q] = in ? w_in[e] : 0.0;
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int64_t e = e0 + (int64_t)(k0 + q) * T;
         if (k0 + q < E && e < n) {
-          double wv = wsm[(k0 + q) * GM_THREADS + tid];
+          double wv = GW ? wq[q] : W(k0 + q);
           if (i > 0) {
             wv = __dsub_rn(wv, __dmul_rn(h_prev, bp[q]));
-            wsm[(k0 + q) * GM_THREADS + tid] = wv;
+            W(k0 + q) = wv;
           }
           acc = __dadd_rn(acc, __dmul_rn(wv, a[q]));
         }
@@ -748,18 +762,20 @@ __global__ void __launch_bounds__(GM_THREADS, 1) k_gm_arnoldi(SolveCtrl* __restr
     const double* vj = V + (size_t)j * n;
     double acc = 0.0;
     for (int k0 = 0; k0 < E; k0 += 4) {
-      double a[4];
+      double a[4], wq[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int64_t e = e0 + (int64_t)(k0 + q) * T;
-        a[q] = (k0 + q < E && e < n) ? __ldg(vj + e) : 0.0;
+        const bool in = k0 + q < E && e < n;
+        a[q] = in ? __ldg(vj + e) : 0.0;
+        if constexpr (GW) wq[q] = in ? w_in[e] : 0.0;
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int64_t e = e0 + (int64_t)(k0 + q) * T;
         if (k0 + q < E && e < n) {
-          const double wv = __dsub_rn(wsm[(k0 + q) * GM_THREADS + tid], __dmul_rn(h_prev, a[q]));
-          wsm[(k0 + q) * GM_THREADS + tid] = wv;
+          const double wv = __dsub_rn(GW ? wq[q] : W(k0 + q), __dmul_rn(h_prev, a[q]));
+          W(k0 + q) = wv;
           acc = __dadd_rn(acc, __dmul_rn(wv, wv));
         }
       }
@@ -768,7 +784,7 @@ __global__ void __launch_bounds__(GM_THREADS, 1) k_gm_arnoldi(SolveCtrl* __restr
     double* vn = V + (size_t)(j + 1) * n;  // V holds restart + 1 vectors
     for (int k = 0; k < E; ++k) {
       const int64_t e = e0 + k * T;
-      if (e < n) vn[e] = wsm[k * GM_THREADS + tid] / hn;
+      if (e < n) vn[e] = W(k) / hn;
     }
     if (blockIdx.x == 0 && tid == 0) {
       SolveCtrl* sc = reinterpret_cast<SolveCtrl*>(sctrl);
@@ -1486,22 +1502,25 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
 // ---------------------------------------------------------------- GMRES
 // Launch shape of k_gm_arnoldi: one CTA of GM_THREADS per SM, E elements of w per thread
 // in shared memory.  False (per-step kernels) when the slice does not fit or GSE_GM_COOP=0.
-static bool gm_coop_config(const Matrix& M, int64_t n, int* grid, int* E, size_t* smem) {
+static bool gm_coop_config(const Matrix& M, int64_t n, int* grid, int* E, size_t* smem,
+                           bool* gw) {
   const char* env = getenv("GSE_GM_COOP");
   if ((env && env[0] == '0') || n <= 0) return false;
+  *gw = false;
   // the dynamic shared-memory attribute is per function and process-wide, and graphs built
   // for other vector lengths (or other threads' solves) launch with other sizes: set it
   // once to the largest size this configuration uses (200 KB), never lower
   static std::once_flag attr_once;
   static bool attr_ok = false;
   std::call_once(attr_once, [] {
-    attr_ok = cudaFuncSetAttribute(k_gm_arnoldi, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr_ok = cudaFuncSetAttribute(k_gm_arnoldi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    200 * 1024) == cudaSuccess;
     cudaGetLastError();
   });
   if (!attr_ok) return false;
   const int sms = num_sms(M.device);
-  for (int per = 1; per >= 1; --per) {
+  // GSE_GM_COOP=g: the global-w variant at any size (tests)
+  for (int per = (env && env[0] == 'g') ? 0 : 1; per >= 1; --per) {
     int64_t G = (int64_t)sms * per;
     const int64_t need = (n + GM_THREADS - 1) / GM_THREADS;
     if (G > need) G = need;
@@ -1509,7 +1528,7 @@ static bool gm_coop_config(const Matrix& M, int64_t n, int* grid, int* E, size_t
     const size_t sm = (size_t)e * GM_THREADS * sizeof(double);
     if (sm > 200 * 1024) continue;
     int blocks = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_gm_arnoldi, GM_THREADS, sm) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_gm_arnoldi<false>, GM_THREADS, sm) !=
         cudaSuccess)
       continue;
     if ((int64_t)blocks * sms >= G) {
@@ -1518,6 +1537,20 @@ static bool gm_coop_config(const Matrix& M, int64_t n, int* grid, int* E, size_t
       *smem = sm;
       return true;
     }
+  }
+  // longer vectors: w stays in global memory, one CTA of GM_THREADS per SM
+  // (GSE_GM_COOP=s keeps the per-step kernels for them)
+  if (env && env[0] == 's') return false;
+  int blocks = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_gm_arnoldi<true>, GM_THREADS, 0) ==
+          cudaSuccess &&
+      blocks >= 1) {
+    const int64_t G = sms;
+    *grid = (int)G;
+    *E = (int)((n + G * GM_THREADS - 1) / (G * GM_THREADS));
+    *smem = 0;
+    *gw = true;
+    return true;
   }
   cudaGetLastError();
   return false;
@@ -1577,7 +1610,8 @@ static gse_status build_gm_graph(Matrix& M, int level, int restart, int k16) {
   launch_pdl(k_gm_scale, ws->vgrid, 256, 0, cs, c, w, ws->V, n, 0);
   int cg_grid = 0, cg_e = 0;
   size_t cg_smem = 0;
-  const bool coop = gm_coop_config(M, n, &cg_grid, &cg_e, &cg_smem);
+  bool cg_gw = false;
+  const bool coop = gm_coop_config(M, n, &cg_grid, &cg_e, &cg_smem, &cg_gw);
   for (int j = 0; j < restart && rc == GSE_OK; ++j) {
     rc = launch_spmv_guarded(M, level, ws->V + (size_t)j * n, w, &c->stop, cs);
     if (coop) {
@@ -1591,8 +1625,11 @@ static gse_status build_gm_graph(Matrix& M, int level, int restart, int k16) {
       at[0].val.cooperative = 1;
       cfg.attrs = at;
       cfg.numAttrs = 1;
-      const cudaError_t le = cudaLaunchKernelEx(&cfg, k_gm_arnoldi, c, ws->ring, (const double*)w,
-                                                ws->V, n, j, cg_e, ws->partials);
+      const cudaError_t le =
+          cg_gw ? cudaLaunchKernelEx(&cfg, k_gm_arnoldi<true>, c, ws->ring, w, ws->V, n, j, cg_e,
+                                     ws->partials)
+                : cudaLaunchKernelEx(&cfg, k_gm_arnoldi<false>, c, ws->ring, w, ws->V, n, j, cg_e,
+                                     ws->partials);
       if (le != cudaSuccess) {
         cudaStreamEndCapture(cs, nullptr);
         return cuda_status(le, "cooperative k_gm_arnoldi");

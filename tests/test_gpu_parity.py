@@ -391,11 +391,11 @@ def test_cg_breakdown_abort(g):
     assert r["status"] == g.GSE_NUMERICAL_ABORT
 
 
-@pytest.mark.parametrize("coop", ["1", "0"])
+@pytest.mark.parametrize("coop", ["1", "0", "g"])
 @pytest.mark.parametrize("mode", ["fp64", "stepped", "stepped_scaled"])
 def test_gmres_parity(g, mode, coop, monkeypatch):
-    """coop 1: one cooperative Arnoldi kernel per inner step (w in shared memory);
-    coop 0: the per-MGS-step kernels (fallback for long vectors)."""
+    """coop 1: one cooperative Arnoldi kernel per inner step (w in shared memory); g: the
+    same with w in global memory (long vectors); 0: the per-MGS-step kernels."""
     monkeypatch.setenv("GSE_GM_COOP", coop)
     A = gi.convdiff3d(16)
     b = gi.ones_rhs(A)
