@@ -12,10 +12,13 @@ GPUs (gse_encode_dist: global table by histogram allreduce, local renumbering; C
 NCCL halo exchange + allreduced dots) -> "scaling": "strong".  --workload c5 selects the
 512^3 Poisson of configs[4] (the multi-GPU config).
 
-Also reported (N = 1): the SpMV segment sweep (GB/s, GFLOP/s, fraction of the measured HBM
-peak per segment count, FP64 / FP32 accumulation, FP64-CSR comparator), the FP64-CSR CG
-time-to-1e-10, the roofline of the dominant kernel, the oracle CPU baseline, the end-to-end
-number through the C-ABI with host buffers, SM clocks.
+Also reported (N = 1): the SpMV segment sweep on C2 (GB/s, GFLOP/s, fraction of the measured
+HBM peak per segment count, FP64 / FP32 accumulation, FP64-CSR comparator, FP16 / BF16
+storage baselines; cold and back-to-back), the FP64-CSR / FP16 / BF16 CG time-to-1e-10 and
+the paper's GSE-SEM* projection (Eq. 7), the roofline of the dominant kernel, the configs[2]
+power-law SpMV segment sweep (`spmv_sweep_c3`), the configs[3] conv-diff 256^3 GMRES(30)
+times (`gmres_c4`, at 1e-10 and at the paper's 1e-6), the oracle CPU baseline, the
+end-to-end number through the C-ABI with host buffers, SM clocks.  About one minute.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gse|reference]
 """
