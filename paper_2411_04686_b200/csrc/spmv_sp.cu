@@ -8,11 +8,14 @@
 //    latency-bound at 0.25 Gnnz/s per B200: profiles/ncu_spmv_r01_v1.txt);
 //  * lane l owns elements s + l + 32k (k < 8): each plane load / x gather instruction of a
 //    warp covers 32 consecutive non-zeros, so the load is balanced whatever the row lengths;
-//  * products go to a warp-private shared tile and lane l sums row l sequentially in
-//    storage order (the oracle's order); long rows: per-lane sequential partials + a fixed
-//    shuffle tree.
+//  * products go to a warp-private shared tile and lpr lanes per row sum it (storage order
+//    for lpr = 1, the oracle's order); the bounds of a block's rows are loaded with its
+//    planes (one dependent round trip less); long rows: per-lane sequential partials + a
+//    fixed shuffle tree;
+//  * register budget for 4 CTAs (32 warps) per SM: on the power-law matrix the kernel is
+//    bound by the L1 data pipe (x gathers + the products tile, ~0.94 wavefronts per
+//    non-zero); DESIGN.md 6.2 lists the measured alternatives.
 #include "spmv_common.cuh"
-
 
 namespace gse {
 
