@@ -72,6 +72,7 @@ struct SolverWs {
   uint16_t* vtab = nullptr;  // [V16_cols][V16_KMAX]
   int* vlen = nullptr;       // [V16_cols]
   unsigned* vhist = nullptr; // [2048]
+  unsigned* vhist2 = nullptr; // [2][2048] (cooperative 16-bit Arnoldi)
   double* vcur = nullptr;    // [n]
   int gm_k16 = 0;            // basis format the GMRES graphs were built for
   double* partials = nullptr;
@@ -1026,6 +1027,239 @@ __global__ void __launch_bounds__(256, 4) k_gm_xupdate16(const SolveCtrl* __rest
   }
 }
 
+// One Arnoldi step on the 16-bit basis (NEXT-4) as ONE cooperative kernel (w in global
+// memory): the MGS passes and the norm on the decoded v_i (grid reductions as in
+// k_gm_arnoldi), then v_{j+1} = w / h_{j+1,j} encoded in 16-bit form -- exponent histogram
+// of the grid (shared-memory bins -> global atomics into hist[j & 1]), grid barrier, the
+// table selected redundantly by every CTA (same histogram, same rule -> the same table;
+// CTA 0 stores it), the encode of this CTA's slice plus the decoded copy for the next SpMV.
+// hist[(j + 1) & 1] is cleared for the next step (both are cleared at every restart).
+__device__ void v16_select_block(const unsigned* hist, int k_max, int* sel, int* take_out,
+                                 unsigned long long* key, unsigned long long* red) {
+  __shared__ int s_nd, s_emax;
+  if (threadIdx.x == 0) {
+    s_nd = 0;
+    s_emax = 0;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < 2048; e += blockDim.x) {
+    const unsigned cnt = (e >= 1 && e <= 2046) ? __ldcg(hist + e) : 0u;
+    key[e] = cnt ? (((unsigned long long)cnt << 11) | (unsigned long long)e) : 0ull;
+    if (cnt) {
+      atomicAdd(&s_nd, 1);
+      atomicMax(&s_emax, e);
+    }
+  }
+  __syncthreads();
+  const int take = s_nd < k_max ? s_nd : k_max;
+  for (int k = 0; k < take; ++k) {
+    unsigned long long loc = 0;
+    for (int e = threadIdx.x; e < 2048; e += blockDim.x) loc = max(loc, key[e]);
+    for (int o = 16; o > 0; o >>= 1) loc = max(loc, __shfl_xor_sync(0xFFFFFFFFu, loc, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = loc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long b = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b = max(b, red[w]);
+      sel[k] = (int)(b & 0x7FFull);
+      key[b & 0x7FFull] = 0ull;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    bool have = false;
+    for (int k = 0; k < take; ++k) have |= (sel[k] == s_emax);
+    if (take > 0 && !have) sel[take - 1] = s_emax;  // P:123 (R5)
+    *take_out = take;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(GM_THREADS, 1) k_gm_arnoldi16(
+    SolveCtrl* __restrict__ c, double* ring, double* __restrict__ w,
+    uint16_t* __restrict__ V16, uint16_t* __restrict__ vtab, int* __restrict__ vlen,
+    double* __restrict__ vcur, unsigned* __restrict__ hist2, int64_t n, int j, int E,
+    double* partials) {
+  __shared__ unsigned long long sctrl[CTRL_HEAD_WORDS];
+  __shared__ double s_col[MAX_RESTART + 1], s_cs[MAX_RESTART], s_sn[MAX_RESTART];
+  __shared__ double s_g[MAX_RESTART + 1];
+  __shared__ double red[GM_THREADS / 32];
+  __shared__ double s_tot;
+  __shared__ double sci[V16_KMAX], scp[V16_KMAX];
+  __shared__ unsigned long long key[2048];
+  __shared__ unsigned long long redk[GM_THREADS / 32];
+  __shared__ unsigned hsm[2048];
+  __shared__ int sel[V16_KMAX];
+  __shared__ int s_take;
+  __shared__ int Etab[V16_KMAX];
+  if (c->stop) return;  // uniform: written only before this launch
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (blockIdx.x == 0) {
+    if (warp == 0) ctrl_load_head(c, sctrl);
+    if (warp == 1)
+      for (int i = lane; i < j; i += 32) {
+        s_cs[i] = c->cs[i];
+        s_sn[i] = c->sn[i];
+      }
+    if (warp == 2)
+      for (int i = lane; i <= j + 1; i += 32) s_g[i] = c->g[i];
+  }
+  const int64_t T = (int64_t)gridDim.x * GM_THREADS;
+  const int64_t e0 = (int64_t)blockIdx.x * GM_THREADS + tid;  // first 4-element chunk
+  const int64_t n4 = n >> 2;  // n % 4 == 0 (host check)
+  // clear the other step's histogram (unused in this step)
+  unsigned* hcur = hist2 + (size_t)(j & 1) * 2048;
+  unsigned* hnext = hist2 + (size_t)((j + 1) & 1) * 2048;
+  for (int e = (int)(blockIdx.x * GM_THREADS + tid); e < 2048; e += (int)T) hnext[e] = 0u;
+  double h_prev = 0.0;
+  for (int i = 0; i <= j; ++i) {
+    const int ip = i > 0 ? i - 1 : 0;
+    load_scales16(vtab + (size_t)i * V16_KMAX, vlen[i], K16_EB, sci);
+    load_scales16(vtab + (size_t)ip * V16_KMAX, vlen[ip], K16_EB, scp);
+    __syncthreads();
+    const uint2* vi4 = reinterpret_cast<const uint2*>(V16 + (size_t)i * n);
+    const uint2* vp4 = reinterpret_cast<const uint2*>(V16 + (size_t)ip * n);
+    double2* w2 = reinterpret_cast<double2*>(w);
+    double acc = 0.0;
+    // 4 consecutive elements per chunk: one 8-byte load per basis vector, two 16-byte w
+    // accesses; chunks c = c0 + k T, two chunks in flight
+    for (int k0 = 0; k0 < E; k0 += 2) {
+      double2 wa[2], wb[2];
+      uint2 a4[2], b4[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int64_t cc = e0 + (int64_t)(k0 + q) * T;
+        const bool in = k0 + q < E && cc < n4;
+        a4[q] = in ? vi4[cc] : make_uint2(0u, 0u);
+        b4[q] = (in && i > 0) ? vp4[cc] : make_uint2(0u, 0u);
+        wa[q] = in ? w2[2 * cc] : make_double2(0.0, 0.0);
+        wb[q] = in ? w2[2 * cc + 1] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int64_t cc = e0 + (int64_t)(k0 + q) * T;
+        if (k0 + q < E && cc < n4) {
+          double wv[4] = {wa[q].x, wa[q].y, wb[q].x, wb[q].y};
+          const uint32_t av[4] = {a4[q].x & 0xFFFFu, a4[q].x >> 16, a4[q].y & 0xFFFFu, a4[q].y >> 16};
+          if (i > 0) {
+            const uint32_t bv[4] = {b4[q].x & 0xFFFFu, b4[q].x >> 16, b4[q].y & 0xFFFFu, b4[q].y >> 16};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) wv[t] = __dsub_rn(wv[t], __dmul_rn(h_prev, dec16(bv[t], scp, K16_EB)));
+            w2[2 * cc] = make_double2(wv[0], wv[1]);
+            w2[2 * cc + 1] = make_double2(wv[2], wv[3]);
+          }
+#pragma unroll
+          for (int t = 0; t < 4; ++t) acc = __dadd_rn(acc, __dmul_rn(wv[t], dec16(av[t], sci, K16_EB)));
+        }
+      }
+    }
+    h_prev = gm_grid_total(acc, partials, i & 1, red, &s_tot);
+    if (blockIdx.x == 0 && tid == 0) s_col[i] = h_prev;
+    __syncthreads();  // sci / scp reused by the next pass
+  }
+  double hn;
+  {  // w -= h_{j,j} v_j ; ||w||
+    load_scales16(vtab + (size_t)j * V16_KMAX, vlen[j], K16_EB, sci);
+    __syncthreads();
+    const uint2* vj4 = reinterpret_cast<const uint2*>(V16 + (size_t)j * n);
+    double2* w2 = reinterpret_cast<double2*>(w);
+    double acc = 0.0;
+    for (int k0 = 0; k0 < E; k0 += 2) {
+      double2 wa[2], wb[2];
+      uint2 a4[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int64_t cc = e0 + (int64_t)(k0 + q) * T;
+        const bool in = k0 + q < E && cc < n4;
+        a4[q] = in ? vj4[cc] : make_uint2(0u, 0u);
+        wa[q] = in ? w2[2 * cc] : make_double2(0.0, 0.0);
+        wb[q] = in ? w2[2 * cc + 1] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int64_t cc = e0 + (int64_t)(k0 + q) * T;
+        if (k0 + q < E && cc < n4) {
+          double wv[4] = {wa[q].x, wa[q].y, wb[q].x, wb[q].y};
+          const uint32_t av[4] = {a4[q].x & 0xFFFFu, a4[q].x >> 16, a4[q].y & 0xFFFFu, a4[q].y >> 16};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            wv[t] = __dsub_rn(wv[t], __dmul_rn(h_prev, dec16(av[t], sci, K16_EB)));
+            acc = __dadd_rn(acc, __dmul_rn(wv[t], wv[t]));
+          }
+          w2[2 * cc] = make_double2(wv[0], wv[1]);
+          w2[2 * cc + 1] = make_double2(wv[2], wv[3]);
+        }
+      }
+    }
+    hn = sqrt(gm_grid_total(acc, partials, (j + 1) & 1, red, &s_tot));
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    SolveCtrl* sc = reinterpret_cast<SolveCtrl*>(sctrl);
+    gm_finish(sc, ring, j, hn, s_col, 1, s_cs, s_sn, s_g);
+    const int m = sc->restart;
+    for (int i = 0; i <= j + 1; ++i) c->H[i * m + j] = s_col[i];
+    c->cs[j] = s_cs[j];
+    c->sn[j] = s_sn[j];
+    c->g[j] = s_g[j];
+    c->g[j + 1] = s_g[j + 1];
+    ctrl_store_head(c, sctrl);
+  }
+  if (j + 1 >= c->restart) return;  // (uniform) no v_{j+1} in this cycle
+  // v_{j+1} = w / hn in 16-bit form: histogram of the grid ...
+  for (int e = tid; e < 2048; e += GM_THREADS) hsm[e] = 0u;
+  __syncthreads();
+  for (int k = 0; k < E; ++k) {
+    const int64_t cc = e0 + (int64_t)k * T;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      unsigned ex = 0xFFFFFFFFu;
+      if (cc < n4) {
+        const double v = w[4 * cc + t] / hn;
+        ex = (unsigned)((unsigned long long)__double_as_longlong(v) >> 52) & 0x7FFu;
+        if (ex == 0u || ex == 0x7FFu) ex = 0xFFFFFFFFu;
+      }
+      const unsigned peers = __match_any_sync(0xFFFFFFFFu, ex);
+      if (ex != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hsm[ex], (unsigned)__popc(peers));
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < 2048; e += GM_THREADS)
+    if (hsm[e]) atomicAdd(&hcur[e], hsm[e]);
+  __threadfence();
+  cooperative_groups::this_grid().sync();
+  // ... the table (every CTA, same result) ...
+  v16_select_block(hcur, 8, sel, &s_take, key, redk);
+  const int take = s_take;
+  if (tid < V16_KMAX) Etab[tid] = tid < take ? sel[tid] + 1 : 0;
+  __syncthreads();
+  uint16_t* tabn = vtab + (size_t)(j + 1) * V16_KMAX;
+  if (blockIdx.x == 0 && tid < V16_KMAX) tabn[tid] = (uint16_t)Etab[tid];
+  if (blockIdx.x == 0 && tid == 0) vlen[j + 1] = take;
+  if (tid < V16_KMAX) sci[tid] = tid < take ? ldexp(1.0, Etab[tid] - 1023 - (15 - K16_EB)) : 0.0;
+  __syncthreads();
+  // ... and the encode of this CTA's slice (+ the decoded copy for the next SpMV)
+  uint2* vn4 = reinterpret_cast<uint2*>(V16 + (size_t)(j + 1) * n);
+  const double2* w2c = reinterpret_cast<const double2*>(w);
+  double2* vc2 = reinterpret_cast<double2*>(vcur);
+  for (int k = 0; k < E; ++k) {
+    const int64_t cc = e0 + (int64_t)k * T;
+    if (cc < n4) {
+      const double2 wa = w2c[2 * cc], wb = w2c[2 * cc + 1];
+      const double wv[4] = {wa.x, wa.y, wb.x, wb.y};
+      uint32_t wd[4];
+      double dv[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        wd[t] = enc16(wv[t] / hn, Etab, take, K16_EB);
+        dv[t] = dec16(wd[t], sci, K16_EB);
+      }
+      vn4[cc] = make_uint2(wd[0] | (wd[1] << 16), wd[2] | (wd[3] << 16));
+      vc2[2 * cc] = make_double2(dv[0], dv[1]);
+      vc2[2 * cc + 1] = make_double2(dv[2], dv[3]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- workspace
 // Pinned host mirrors of the control block and the capture streams are process-wide
 // caches: cudaMallocHost / cudaStreamCreate cost milliseconds, and a matrix (with its
@@ -1112,8 +1346,10 @@ static gse_status ensure_ws(Matrix& M, int64_t ring_t, int gm_restart, cudaStrea
     ws->vtab = dev_alloc_n<uint16_t>((size_t)ws->V16_cols * V16_KMAX, s);
     ws->vlen = dev_alloc_n<int>((size_t)ws->V16_cols, s);
     if (!ws->vhist) ws->vhist = dev_alloc_n<unsigned>(2048, s);
+    if (!ws->vhist2) ws->vhist2 = dev_alloc_n<unsigned>(2 * 2048, s);
     if (!ws->vcur) ws->vcur = dev_alloc_n<double>(nn, s);
-    if (!ws->V16 || !ws->vtab || !ws->vlen || !ws->vhist || !ws->vcur) return GSE_ERR_OOM;
+    if (!ws->V16 || !ws->vtab || !ws->vlen || !ws->vhist || !ws->vhist2 || !ws->vcur)
+      return GSE_ERR_OOM;
     GSE_CUDA_TRY(cudaMemsetAsync(ws->vhist, 0, 2048 * sizeof(unsigned), s));
     GSE_CUDA_TRY(cudaMemsetAsync(ws->vlen, 0, (size_t)ws->V16_cols * sizeof(int), s));
   }
@@ -1133,7 +1369,8 @@ void free_solver_ws(Matrix& M) {
   for (double* p : {ws->x, ws->r, ws->p, ws->q, ws->b, ws->tmp, ws->V, ws->partials, ws->ring,
                     ws->vcur})
     if (p) dev_free(p, s);
-  for (void* p : {(void*)ws->V16, (void*)ws->vtab, (void*)ws->vlen, (void*)ws->vhist})
+  for (void* p : {(void*)ws->V16, (void*)ws->vtab, (void*)ws->vlen, (void*)ws->vhist,
+                  (void*)ws->vhist2})
     if (p) dev_free(p, s);
   if (ws->ticket) dev_free(ws->ticket, s);
   if (ws->ctrl) dev_free(ws->ctrl, s);
@@ -1586,6 +1823,38 @@ static gse_status build_gm_graph(Matrix& M, int level, int restart, int k16) {
                  ws->V16 + (size_t)col * n, ws->vcur, &c->stop, ws->vgrid, cs);
     };
     encode16(0, &c->beta);
+    // one cooperative kernel per inner step when the grid fits (w in global memory)
+    const char* env = getenv("GSE_GM_COOP");
+    const bool coop16 = !(env && (env[0] == '0' || env[0] == 's'));
+    int occ = 0;
+    if (coop16)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gm_arnoldi16, GM_THREADS, 0);
+    cudaGetLastError();
+    if (coop16 && occ >= 1 && n > 0 && (n & 3) == 0) {
+      GSE_CUDA_TRY(cudaMemsetAsync(ws->vhist2, 0, 2 * 2048 * sizeof(unsigned), cs));
+      const int G = num_sms(M.device);
+      const int64_t n4 = n >> 2;
+      const int E = (int)((n4 + (int64_t)G * GM_THREADS - 1) / ((int64_t)G * GM_THREADS));
+      for (int j = 0; j < restart && rc == GSE_OK; ++j) {
+        rc = launch_spmv_guarded(M, level, ws->vcur, w, &c->stop, cs);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(G);
+        cfg.blockDim = dim3(GM_THREADS);
+        cfg.stream = cs;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        const cudaError_t le = cudaLaunchKernelEx(&cfg, k_gm_arnoldi16, c, ws->ring, w, ws->V16,
+                                                  ws->vtab, ws->vlen, ws->vcur, ws->vhist2, n,
+                                                  j, E, ws->partials);
+        if (le != cudaSuccess) {
+          cudaStreamEndCapture(cs, nullptr);
+          return cuda_status(le, "cooperative k_gm_arnoldi16");
+        }
+      }
+    } else
     for (int j = 0; j < restart && rc == GSE_OK; ++j) {
       rc = launch_spmv_guarded(M, level, ws->vcur, w, &c->stop, cs);
       for (int i = 0; i <= j; ++i)

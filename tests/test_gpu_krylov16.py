@@ -70,8 +70,12 @@ def _cmp(rg, ro):
     assert 0.1 <= ratio <= 10, (rg, ro)
 
 
+@pytest.mark.parametrize("coop", ["1", "s"])
 @pytest.mark.parametrize("mode", ["fp64_matrix", "fixed3", "stepped_scaled"])
-def test_gmres_krylov16_parity(g, mode):
+def test_gmres_krylov16_parity(g, mode, coop, monkeypatch):
+    """coop 1: one cooperative kernel per Arnoldi step (MGS, norm, histogram, table, encode);
+    s: the per-step kernels"""
+    monkeypatch.setenv("GSE_GM_COOP", coop)
     A = gi.convdiff3d(16)
     b = gi.ones_rhs(A)
     if mode == "fp64_matrix":
