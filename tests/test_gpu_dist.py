@@ -303,3 +303,32 @@ def test_dist_overlap_interior_rows(g, P):
     x_all = np.concatenate([o[1] for o in outs])
     F = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
     assert np.linalg.norm(b - O.spmv_fp64(F, x_all)) / np.linalg.norm(b) <= 1e-10 * 1.01
+
+
+def test_nccl_backend_single_rank(g):
+    """the NCCL backend on the one GPU this box has: a 1-rank communicator runs the real
+    NCCL calls of the distributed path (unique id, init, allgather / alltoall of the plan,
+    histogram and dot allreduces, grouped send/recv with no peers) through encode, SpMV,
+    CG and GMRES; results equal the single-GPU matrix's"""
+    A = gi.poisson3d(24, "varcoef")
+    n = A.rows
+    D = g.gse_dist_create(g.gse_nccl_unique_id(), 0, 1, 0)
+    dev = lambda v: torch.from_numpy(v).cuda()
+    M = g.gse_encode_dist(D, dev(A.row_ptr), dev(A.col), dev(A.val), 0, n)
+    M1 = g.gse_encode(A.row_ptr, A.col, A.val, n, n)
+    assert list(M.info["table"]) == list(M1.info["table"])
+    x = gi.uniform_vec(n, seed=4)
+    for L in (1, 2, 3):
+        yd = g.gse_spmv(M, dev(x), segments=L).cpu().numpy()
+        y1 = g.gse_spmv(M1, x, segments=L)
+        assert np.array_equal(yd, y1), L  # same kernels, same order on one rank
+    b = gi.ones_rhs(A)
+    sched = lambda s: g.gse_default_schedule(s, l=30, t=10, m=10)
+    _, rd = g.gse_solve_cg(M, dev(b), tol=1e-10, sched=sched("cg"))
+    _, r1 = g.gse_solve_cg(M1, b, tol=1e-10, sched=sched("cg"))
+    assert rd["converged"] and abs(rd["iterations"] - r1["iterations"]) <= 2
+    _, rd = g.gse_solve_gmres(M, dev(b), tol=1e-10, sched=sched("gmres"))
+    _, r1 = g.gse_solve_gmres(M1, b, tol=1e-10, sched=sched("gmres"))
+    assert rd["converged"] and abs(rd["iterations"] - r1["iterations"]) <= 2
+    M.close()
+    D.close()
