@@ -156,7 +156,8 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 
 // ---------------------------------------------------------------- kernels (launchers)
 // encode.cu
-gse_status build_partition(Matrix& M, cudaStream_t s);
+gse_status build_partition(Matrix& M, cudaStream_t s, const void* extra_d = nullptr,
+                           void* extra_h = nullptr, size_t extra_bytes = 0);
 // sample_block_rows > 0: table from one sampled row per row block (NEXT-3)
 gse_status encode_matrix(Matrix& M, const gse_csr_f64& A, const void* d_row_ptr, int rp64,
                          const int32_t* d_col, const double* d_val, cudaStream_t s,

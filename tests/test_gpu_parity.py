@@ -93,6 +93,51 @@ def test_encode_k_sweep_bit_exact(g, k):
         assert np.array_equal(P[key], getattr(R, key)), key
 
 
+@pytest.mark.parametrize("offset", [0, 1])
+def test_encode_alignment_and_tail(g, offset):
+    """k_hist / k_encode take four nonzeros per thread when every array is 16-byte aligned
+    and one otherwise; nnz % 4 != 0 leaves a scalar tail.  offset 1: val / col are views one
+    element into their buffers (8 / 4 bytes: the one-element path).  Planes bit-exact, and
+    the FIRST bad element is the one reported (in the quad body and in the tail)."""
+    A = gi.random_csr(3001, 2900, 7, seed=14, value_kind="mixed", empty_rows=0.1)
+    assert A.nnz % 4 != 0
+    R = O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val, 8)
+
+    def views(val, col):
+        vb = torch.zeros(A.nnz + offset, dtype=torch.float64, device="cuda")
+        cb = torch.zeros(A.nnz + offset, dtype=torch.int32, device="cuda")
+        vb[offset:] = torch.from_numpy(val).cuda()
+        cb[offset:] = torch.from_numpy(col).cuda()
+        return vb[offset:], cb[offset:]
+
+    rp = torch.from_numpy(A.row_ptr).cuda()
+    v, c = views(A.val, A.col)
+    assert (v.data_ptr() % 16 == 0) == (offset == 0)
+    M = g.gse_encode(rp, c, v, A.rows, A.cols, k_max=8)
+    P = g.gse_matrix_copy_planes(M)
+    assert list(P["table"]) == list(R.table)
+    for k in ("col_ei", "head", "tail1", "tail2"):
+        assert np.array_equal(P[k], getattr(R, k)), k
+    M.close()
+    for first, second in ((A.nnz - 2, A.nnz - 1), (9, A.nnz - 1), (6, 7)):
+        val = A.val.copy()
+        val[second] = np.nan
+        val[first] = np.inf
+        v, c = views(val, A.col)
+        with pytest.raises(g.GseError) as e:
+            g.gse_encode(rp, c, v, A.rows, A.cols)
+        assert e.value.status == g.GSE_ERR_NONFINITE
+        assert f"(element {first})" in e.value.detail, e.value.detail
+        col = A.col.copy()
+        col[second] = -1
+        col[first] = A.cols
+        v, c = views(A.val, col)
+        with pytest.raises(g.GseError) as e:
+            g.gse_encode(rp, c, v, A.rows, A.cols)
+        assert e.value.status == g.GSE_ERR_INVALID_ARG
+        assert f"element {first}" in e.value.detail, e.value.detail
+
+
 def test_encode_side_array(g):
     """cols >= 2^(32 - ei_bits): EI in a side array."""
     rng = np.random.default_rng(4)
