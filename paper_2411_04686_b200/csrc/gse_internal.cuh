@@ -175,6 +175,9 @@ struct DotOut {
   unsigned* ticket = nullptr;   // last-block counter (reset by the last block)
   double* result = nullptr;     // deterministic sum of partials
 };
+gse_status launch_spmv_cgp(const Matrix& M, int level, const double* p_old, const double* r,
+                           double* p_new, double* x, const double* alpha, const double* beta,
+                           double* q, const DotOut* dot, cudaStream_t s, const int* stop);
 gse_status launch_spmv(const Matrix& M, int level, const double* x, double* y,
                        const DotOut* dot, cudaStream_t s, const int* stop = nullptr);
 gse_status launch_spmv_guarded(const Matrix& M, int level, const double* x, double* y,

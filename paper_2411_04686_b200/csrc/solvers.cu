@@ -47,6 +47,8 @@ struct SolveCtrl {
   double dot;  // scratch reduction target
   double rr_part;  // distributed CG: this rank's r.r partial (allreduced before k_cg_events)
   double alpha;    // CG: step of the current iteration, applied to x by k_cg_xpay (0: none)
+  double pend_alpha;  // CG with the p update in the SpMV: last alpha and the buffer of its p
+  long long pend_buf;  // (applied to x by k_cg_xfin after the loop)
   int upd_ok;
   long long iter, max_iters;
   int level, event, stop, stepped, max_level;
@@ -64,6 +66,7 @@ struct SolverWs {
   int64_t n = 0;
   int vgrid = 0;
   double *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *b = nullptr, *tmp = nullptr;
+  double* p2 = nullptr;  // second p buffer of the fused CG graph (p_old / p_new alternate)
   double* V = nullptr;  // GMRES basis (restart + 1) x n
   int V_cols = 0;
   // 16-bit Krylov basis (NEXT-4): words, per-vector tables, histogram, decoded current vector
@@ -278,7 +281,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_update(SolveCtrl* __restrict__ c,
                                                    const double* __restrict__ q, int64_t n,
                                                    double* partials, unsigned* ticket,
                                                    cudaGraphConditionalHandle handle,
-                                                   int in_graph, int defer) {
+                                                   int in_graph, int defer, int pbuf) {
   pdl_wait();
   pdl_trigger();
   __shared__ unsigned long long sctrl[CTRL_HEAD_WORDS];
@@ -332,6 +335,8 @@ __global__ void __launch_bounds__(256, 4) k_cg_update(SolveCtrl* __restrict__ c,
   if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0) {
     SolveCtrl* sc = reinterpret_cast<SolveCtrl*>(sctrl);
     sc->alpha = ok ? alpha : 0.0;
+    sc->pend_alpha = sc->alpha;
+    sc->pend_buf = pbuf;
     if (defer) {  // distributed: r.r is this rank's partial; k_cg_events runs after the allreduce
       sc->rr_part = tot;
       sc->upd_ok = ok ? 1 : 0;
@@ -414,6 +419,20 @@ __global__ void __launch_bounds__(256, 4) k_cg_fused(SolveCtrl* __restrict__ c, 
     const int64_t j = i0 + k * stride;
     if (j < n) p[j] = __dadd_rn(rv[k], __dmul_rn(beta, p[j]));
   }
+}
+
+// After the fused CG graph's loop: the x update of the last iteration (its SpMV, which
+// would have applied it, was stopped by the event): x += pend_alpha p[pend_buf]
+__global__ void __launch_bounds__(256) k_cg_xfin(const SolveCtrl* __restrict__ c,
+                                                 double* __restrict__ x,
+                                                 const double* __restrict__ p0,
+                                                 const double* __restrict__ p1, int64_t n) {
+  const double a = c->pend_alpha;
+  if (a == 0.0) return;
+  const double* pp = c->pend_buf ? p1 : p0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    x[i] = __dadd_rn(x[i], __dmul_rn(a, pp[i]));
 }
 
 // x += alpha p (the update deferred by k_cg_update) ; p = r + beta p (skipped when an event
@@ -1309,6 +1328,7 @@ static gse_status ensure_ws(Matrix& M, int64_t ring_t, int gm_restart, cudaStrea
     // p is gathered by the SpMV: distributed -> owned + halo entries
     ws->p = dev_alloc_n<double>((size_t)dist_ext_cols(M) + 1, s);
     ws->q = dev_alloc_n<double>(nn, s);
+    if (!M.dist) ws->p2 = dev_alloc_n<double>((size_t)dist_ext_cols(M) + 1, s);
     ws->b = dev_alloc_n<double>(nn, s);
     ws->tmp = dev_alloc_n<double>(nn, s);
     const int64_t np = (M.n_blocks > 2 * ws->vgrid ? M.n_blocks : 2 * ws->vgrid) + 1;
@@ -1366,8 +1386,8 @@ void free_solver_ws(Matrix& M) {
     if (ws->gm_exec[L]) cudaGraphExecDestroy(ws->gm_exec[L]);
     if (ws->gm_graph[L]) cudaGraphDestroy(ws->gm_graph[L]);
   }
-  for (double* p : {ws->x, ws->r, ws->p, ws->q, ws->b, ws->tmp, ws->V, ws->partials, ws->ring,
-                    ws->vcur})
+  for (double* p : {ws->x, ws->r, ws->p, ws->p2, ws->q, ws->b, ws->tmp, ws->V, ws->partials,
+                    ws->ring, ws->vcur})
     if (p) dev_free(p, s);
   for (void* p : {(void*)ws->V16, (void*)ws->vtab, (void*)ws->vlen, (void*)ws->vhist,
                   (void*)ws->vhist2})
@@ -1440,6 +1460,16 @@ static int fused_grid(const Matrix& M) {
   return fits ? (int)want : 0;
 }
 
+// The CG p update fused into the next SpMV (launch_spmv_cgp): row-walk matrices, single
+// GPU, graph path; opt-in (GSE_CG_FUSEP=1, read when a graph is built).  Results are
+// bitwise those of the separate xpay kernel, but the second gathered vector (r and p_old
+// instead of p) costs more than the pass it saves: C2 stepped CG 56.5 vs 46.2 us per
+// iteration (64^3: 17.2 vs 17.7), profiles/ab_cg_fusep_r01.txt.
+static bool cg_fuse_p(const Matrix& M) {
+  const char* e = getenv("GSE_CG_FUSEP");
+  return e && atoi(e) == 1 && M.spmv_mode == SPMV_RW && M.rows > 0 && M.ws && M.ws->p2;
+}
+
 // ---------------------------------------------------------------- CG graph per level
 static gse_status build_cg_graph(Matrix& M, int level) {
   SolverWs* ws = M.ws;
@@ -1469,10 +1499,24 @@ static gse_status build_cg_graph(Matrix& M, int level) {
     const int u = e ? atoi(e) : 8;
     return u < 1 ? 1 : (u > 8 ? 8 : u);
   }();
-  gse_status rc = GSE_OK;
-  for (int u = 0; u < unroll && rc == GSE_OK; ++u) {
-  rc = launch_spmv(M, level, ws->p, ws->q, &d, cs, &ws->ctrl->event);
   const int fg = fused_grid(M);
+  const bool fp = fg == 0 && cg_fuse_p(M);
+  // fused p update: p_old / p_new alternate between ws->p and ws->p2, so the body holds an
+  // even number of iterations (every pass starts with p in ws->p)
+  const int nu = fp ? (unroll + 1) & ~1 : unroll;
+  gse_status rc = GSE_OK;
+  for (int u = 0; u < nu && rc == GSE_OK; ++u) {
+  if (fp) {
+    double* po = (u & 1) ? ws->p2 : ws->p;
+    double* pn = (u & 1) ? ws->p : ws->p2;
+    rc = launch_spmv_cgp(M, level, po, ws->r, pn, ws->x, &ws->ctrl->alpha, &ws->ctrl->beta,
+                         ws->q, &d, cs, &ws->ctrl->event);
+    if (rc == GSE_OK)
+      launch_k(k_cg_update, ws->vgrid, 256, 0, cs, ws->ctrl, ws->ring, ws->r,
+               (const double*)ws->q, n, ws->partials, ws->ticket, h, 1, 0, (u + 1) & 1);
+    continue;
+  }
+  rc = launch_spmv(M, level, ws->p, ws->q, &d, cs, &ws->ctrl->event);
   if (fg > 0) {
     // cooperative fused tail (one grid barrier), see k_cg_fused
     cudaLaunchConfig_t cfg = {};
@@ -1492,7 +1536,7 @@ static gse_status build_cg_graph(Matrix& M, int level) {
     }
   } else {
     launch_k(k_cg_update, ws->vgrid, 256, 0, cs, ws->ctrl, ws->ring, ws->r, ws->q, n, ws->partials,
-                                           ws->ticket, h, 1, 0);
+                                           ws->ticket, h, 1, 0, 0);
     launch_k(k_cg_xpay, ws->vgrid, 256, 0, cs, ws->ctrl, ws->x, ws->p, ws->r, n);
   }
   }
@@ -1500,6 +1544,14 @@ static gse_status build_cg_graph(Matrix& M, int level) {
   cudaError_t e = cudaStreamEndCapture(cs, &captured);
   if (rc != GSE_OK) return rc;
   GSE_CUDA_TRY(e);
+  if (fp) {  // after the loop: the last iteration's x update
+    GSE_CUDA_TRY(cudaStreamBeginCaptureToGraph(cs, g, &node, nullptr, 1,
+                                               cudaStreamCaptureModeRelaxed));
+    launch_k(k_cg_xfin, ws->vgrid, 256, 0, cs, (const SolveCtrl*)ws->ctrl, ws->x,
+             (const double*)ws->p, (const double*)ws->p2, n);
+    e = cudaStreamEndCapture(cs, &captured);
+    GSE_CUDA_TRY(e);
+  }
   GSE_CUDA_TRY(cudaGraphInstantiate(&ws->cg_exec[level - 1], g, 0));
   ws->cg_graph[level - 1] = g;
   return GSE_OK;
@@ -1632,6 +1684,8 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
     hc->max_iters = max_iters;
     hc->level = level;
     hc->event = EV_NONE;
+    hc->alpha = hc->beta = hc->pend_alpha = 0.0;  // fused p update: p_1 = r_0 + 0 p_0
+    hc->pend_buf = 0;
     fill_sched(hc, sched, stepped);
     GSE_CUDA_TRY(cudaMemcpyAsync(ws->ctrl, hc, sizeof(SolveCtrl), cudaMemcpyHostToDevice, s));
   }
@@ -1652,7 +1706,7 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
           rc = dist_allreduce_sum(M, &ws->ctrl->pq, 1, s);
           if (rc != GSE_OK) return rc;
           launch_k(k_cg_update, ws->vgrid, 256, 0, s, ws->ctrl, ws->ring, ws->r, ws->q, n,
-                                                ws->partials, ws->ticket, 0, 0, 1);
+                                                ws->partials, ws->ticket, 0, 0, 1, 0);
           rc = dist_allreduce_sum(M, &ws->ctrl->rr_part, 1, s);
           if (rc != GSE_OK) return rc;
           launch_k(k_cg_events, 1, 32, 0, s, ws->ctrl, ws->ring);
@@ -1670,7 +1724,7 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
           rc = launch_spmv(M, level, ws->p, ws->q, &d, s, &ws->ctrl->event);
           if (rc != GSE_OK) return rc;
           launch_k(k_cg_update, ws->vgrid, 256, 0, s, ws->ctrl, ws->ring, ws->r, ws->q, n,
-                                                ws->partials, ws->ticket, 0, 0, 0);
+                                                ws->partials, ws->ticket, 0, 0, 0, 0);
           launch_k(k_cg_xpay, ws->vgrid, 256, 0, s, ws->ctrl, ws->x, ws->p, ws->r, n);
         }
         GSE_CUDA_TRY(cudaGetLastError());
@@ -1726,6 +1780,10 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
       if (rc != GSE_OK) return rc;
       rc = set_field(ws, &SolveCtrl::event, (int)EV_NONE, s);
       if (rc != GSE_OK) return rc;
+      for (double SolveCtrl::*f : {&SolveCtrl::alpha, &SolveCtrl::beta, &SolveCtrl::pend_alpha}) {
+        rc = set_field(ws, f, 0.0, s);
+        if (rc != GSE_OK) return rc;
+      }
       if (iter >= max_iters) {
         status = GSE_NOT_CONVERGED;
         break;

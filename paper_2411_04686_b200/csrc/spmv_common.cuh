@@ -107,6 +107,13 @@ struct SpmvParams {
   unsigned* ticket;
   double* dot_result;
   const int* stop;    // optional: skip the launch when *stop != 0 (GMRES cycle graphs)
+  // CG p update fused into the SpMV (row walk, FP64; x is p_old): the operand is
+  // r + beta p_old, p_new and x += alpha p_old are written for the launch's rows
+  const double* fr;
+  double* fpn;
+  double* fx;
+  const double* falpha;
+  const double* fbeta;
   long long d64[64];  // decode deltas of the launched level (integer form, FP64)
   int d32[64];        // (integer form, FP32)
   double sc64[64];    // multiply-form scales when the table allows it (FAST)

@@ -109,11 +109,12 @@ __device__ __forceinline__ void issue_stage(const SpmvParams<T>& p, const Stage<
 constexpr uint32_t SSC_ZERO = 128;
 
 // sum of one row, elements [j0, j1) of the stage, in storage order
-template <int L, bool FAST, class T>
+template <int L, bool FAST, class T, bool FUSE = false>
 __device__ __forceinline__ T walk_row(const SpmvParams<T>& p, const Stage<L>& st, uint32_t j0,
                                       uint32_t j1, const double* ssc64, const float* ssc32,
                                       const long long* sd64, const int* sd32,
-                                      const double* sc64, const float* sc32) {
+                                      const double* sc64, const float* sc32,
+                                      double fbeta = 0.0) {
   T sum = 0;
   for (uint32_t j = j0; j < j1; j += 8) {
     const uint32_t nrem = j1 - j;  // slots q >= nrem lie past the row end
@@ -132,6 +133,20 @@ __device__ __forceinline__ T walk_row(const SpmvParams<T>& p, const Stage<L>& st
       if constexpr (has_t2<L>()) t2[q] = st.tail2[j + q];
     }
     // all 8 gathers issued before any product (ld.global.nc, volatile asm keeps the order)
+    if constexpr (FUSE) {  // operand r + beta p_old (the CG p update, same rounding)
+      double rv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t cc = c[q] & p.col_mask;
+        double v, w;
+        asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p.fr + cc));
+        asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(w) : "l"(p.x + cc));
+        rv[q] = v;
+        xv[q] = (T)w;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) xv[q] = (T)__dadd_rn(rv[q], __dmul_rn(fbeta, (double)xv[q]));
+    } else {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const T* a = p.x + (c[q] & p.col_mask);
@@ -144,6 +159,7 @@ __device__ __forceinline__ T walk_row(const SpmvParams<T>& p, const Stage<L>& st
         asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(a));
         xv[q] = v;
       }
+    }
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -205,7 +221,7 @@ __device__ __forceinline__ T walk_row(const SpmvParams<T>& p, const Stage<L>& st
 #else
 #define RW_MINB(L) 3
 #endif
-template <int L, int RPL, bool DOT, bool FAST, class T>
+template <int L, int RPL, bool DOT, bool FAST, class T, bool FUSE>
 __global__ void __launch_bounds__(SPMV_THREADS, RW_MINB(L)) k_spmv_rw(const SpmvParams<T> p) {
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t bars[SPMV_WARPS][2];
@@ -275,6 +291,11 @@ __global__ void __launch_bounds__(SPMV_THREADS, RW_MINB(L)) k_spmv_rw(const Spmv
     return;
   }
   pdl_trigger();
+  double fa = 0.0, fb = 0.0;
+  if constexpr (FUSE) {
+    fa = *p.falpha;
+    fb = *p.fbeta;
+  }
   uint32_t it = 0;
   for (; g < ng; g += W, ++it) {
     const uint32_t cur = it & 1u;
@@ -299,12 +320,20 @@ __global__ void __launch_bounds__(SPMV_THREADS, RW_MINB(L)) k_spmv_rw(const Spmv
     const Stage<L> st(wbase + cur * SB, N);
 #pragma unroll
     for (int k = 0; k < RPL; ++k) {
-      const T sa = walk_row<L, FAST, T>(p, st, cur_b.a[k] - base, ea[k] - base, ssc64, ssc32,
-                                        sd64, sd32, sc64, sc32);
+      const T sa = walk_row<L, FAST, T, FUSE>(p, st, cur_b.a[k] - base, ea[k] - base, ssc64,
+                                              ssc32, sd64, sd32, sc64, sc32, fb);
       const uint32_t row = r0 + 32 * k + lane;
       if (row < rows) {
         p.y[row] = sa;
-        if (DOT) dacc += (double)p.xd[row] * (double)sa;
+        if constexpr (FUSE) {
+          const double po = p.x[row];
+          const double pn = __dadd_rn(p.fr[row], __dmul_rn(fb, po));
+          p.fpn[row] = pn;
+          p.fx[row] = __dadd_rn(p.fx[row], __dmul_rn(fa, po));
+          dacc += pn * (double)sa;
+        } else if (DOT) {
+          dacc += (double)p.xd[row] * (double)sa;
+        }
       }
     }
     __syncwarp();
@@ -324,13 +353,13 @@ struct RwLaunchCache {
   std::map<std::pair<int, size_t>, int> grid;  // (device, smem) -> resident CTAs x SMs
 };
 
-template <int L, int RPL, bool DOT, bool FAST, class T>
+template <int L, int RPL, bool DOT, bool FAST, class T, bool FUSE>
 static void go_rpl(const Matrix& M, const SpmvParams<T>& p, cudaStream_t s) {
   static RwLaunchCache lc;
   const int dev = M.device < 64 ? M.device : 0;
   const uint32_t N = RPL == 1 ? p.rw_stage : p.rw_stage2;
   const size_t smem = (size_t)SPMV_WARPS * 2 * N * rw_elem_bytes<L>();
-  auto kern = k_spmv_rw<L, RPL, DOT, FAST, T>;
+  auto kern = k_spmv_rw<L, RPL, DOT, FAST, T, FUSE>;
   int cap = 0;
   {
     std::lock_guard<std::mutex> lk(lc.mu);
@@ -371,47 +400,49 @@ static int rw_rpl(const Matrix& M, uint32_t rw_stage2) {
   return (M.rows + 2 * RW_ROWS - 1) / (2 * RW_ROWS) >= 32 * warps ? 2 : 1;
 }
 
-template <int L, bool DOT, bool FAST, class T>
+template <int L, bool DOT, bool FAST, class T, bool FUSE>
 static void go(const Matrix& M, const SpmvParams<T>& p, cudaStream_t s) {
   if (rw_rpl<L>(M, p.rw_stage2) == 2)
-    go_rpl<L, 2, DOT, FAST, T>(M, p, s);
+    go_rpl<L, 2, DOT, FAST, T, FUSE>(M, p, s);
   else
-    go_rpl<L, 1, DOT, FAST, T>(M, p, s);
+    go_rpl<L, 1, DOT, FAST, T, FUSE>(M, p, s);
 }
 
-template <int L, bool DOT, class T>
+template <int L, bool DOT, class T, bool FUSE>
 static void go_l(const Matrix& M, bool fast, const SpmvParams<T>& p, cudaStream_t s) {
   if (fast)
-    go<L, DOT, true, T>(M, p, s);
+    go<L, DOT, true, T, FUSE>(M, p, s);
   else
-    go<L, DOT, false, T>(M, p, s);
+    go<L, DOT, false, T, FUSE>(M, p, s);
 }
 
-template <bool DOT, class T>
+template <bool DOT, class T, bool FUSE = false>
 static void go_dot(const Matrix& M, int level, bool fast, const SpmvParams<T>& p,
                    cudaStream_t s) {
   if (M.kind == GSE_KIND_FP64) {
-    go<0, DOT, false, T>(M, p, s);
+    go<0, DOT, false, T, FUSE>(M, p, s);
   } else if (M.kind == GSE_KIND_FP16 || M.kind == GSE_KIND_BF16) {
     if constexpr (sizeof(T) == 8) {  // FP64 accumulation only
       if (M.kind == GSE_KIND_FP16)
-        go<L_FP16, DOT, false, T>(M, p, s);
+        go<L_FP16, DOT, false, T, FUSE>(M, p, s);
       else
-        go<L_BF16, DOT, false, T>(M, p, s);
+        go<L_BF16, DOT, false, T, FUSE>(M, p, s);
     }
   } else if (level == 1) {
-    go_l<1, DOT, T>(M, fast, p, s);
+    go_l<1, DOT, T, FUSE>(M, fast, p, s);
   } else if (level == 2) {
-    go_l<2, DOT, T>(M, fast, p, s);
+    go_l<2, DOT, T, FUSE>(M, fast, p, s);
   } else {
-    go_l<3, DOT, T>(M, fast, p, s);
+    go_l<3, DOT, T, FUSE>(M, fast, p, s);
   }
 }
 
 template <>
 void launch_rw<double>(const Matrix& M, int level, bool dot, bool fast,
                        const SpmvParams<double>& p, cudaStream_t s) {
-  if (dot)
+  if (p.fr)  // the CG p update fused in (launch_spmv_cgp; always with the dot)
+    go_dot<true, double, true>(M, level, fast, p, s);
+  else if (dot)
     go_dot<true, double>(M, level, fast, p, s);
   else
     go_dot<false, double>(M, level, fast, p, s);

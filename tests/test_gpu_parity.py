@@ -412,6 +412,43 @@ def test_cg_parity_c1(g, variant, mode):
     assert rg["converged"] and rg["rel_residual_true"] <= 1e-10
 
 
+@pytest.mark.parametrize("mode", ["stepped_scaled", "fixed3", "fp64"])
+def test_cg_fused_p_update(g, mode, monkeypatch):
+    """opt-in GSE_CG_FUSEP=1 (the p update inside the row-walk SpMV, p double-buffered, the
+    last x update after the graph loop): oracle parity, and for GSE matrices bitwise the
+    solution of the separate-xpay graph (same rounding), across escalations"""
+    A = gi.poisson3d(24, "varcoef")
+    b = gi.ones_rhs(A)
+    if mode == "fp64":
+        mk = lambda: g.gse_fp64_matrix(A.row_ptr, A.col, A.val, A.rows, A.cols)
+        Rm = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+        sg, so = None, None
+    else:
+        mk = lambda: g.gse_encode(A.row_ptr, A.col, A.val, A.rows, A.cols)
+        Rm = O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+        if mode == "fixed3":
+            sg, so = g.fixed_schedule(3), O.fixed_schedule(3)
+        else:
+            sg = g.gse_default_schedule("cg", l=30, t=10, m=10)
+            so = O.schedule("cg", l=30, t=10, m=10)
+    M0 = mk()
+    assert M0.info["spmv_mode"] == 1  # row walk: the fused kernel applies
+    x0, r0 = g.gse_solve_cg(M0, b, tol=1e-10, max_iters=5000, sched=sg)
+    monkeypatch.setenv("GSE_CG_FUSEP", "1")
+    M1 = mk()
+    x1, r1 = g.gse_solve_cg(M1, b, tol=1e-10, max_iters=5000, sched=sg)
+    # a second solve on the same handle reuses the graph (fresh alpha / beta / pending x)
+    x2, r2 = g.gse_solve_cg(M1, b, tol=1e-10, max_iters=5000, sched=sg)
+    xo, ro = O.cg(Rm, b, tol=1e-10, max_iters=5000, sched=so)
+    _cmp_reports(r1, ro)
+    assert r1["converged"] and r1["rel_residual_true"] <= 1e-10
+    assert r1["iterations"] == r2["iterations"] and np.array_equal(x1, x2)
+    if mode != "fp64":
+        assert r1["iterations"] == r0["iterations"]
+        assert r1["switch_iter"] == r0["switch_iter"]
+        assert np.array_equal(x1.view(np.uint64), x0.view(np.uint64))
+
+
 def test_cg_parity_c2_full_size(g):
     """configs[1]: 3D Poisson 128^3 stepped CG to 1e-10 on one B200 vs the oracle."""
     A = gi.poisson3d(128)
