@@ -368,9 +368,17 @@ def estimate_launches(rep, world):
     """Kernels launched per step: encode (rowptr, hist, select, encode, flags, group stats,
     2 CUB select kernels, fill_desc = 9), CG setup (dot, spmv, residual = 3), per iteration
     3 (single GPU, graph while-loop body) or 5 (+ pack + events, distributed), verify /
-    final residual (2 each)."""
-    per_it = 3 if world == 1 else 5
-    return 9 + 3 + per_it * rep["iterations"] + 2 * (1 + rep["n_switches"]) + 2
+    final residual (2 each).  The single-GPU graph body holds 8 iterations (GSE_CG_UNROLL):
+    the kernels of the pass that sees the event still launch (and return at once), so each
+    level's count rounds up to a multiple of 8."""
+    if world == 1:
+        u = int(os.environ.get("GSE_CG_UNROLL", "8"))
+        u = min(max(u, 1), 8)
+        its = sum(-(-i // u) * u for i in rep["iters_per_level"] if i > 0)
+        # outside the graph: 9 encode + 3 SpMV + 3 residual kernels (ncu launch list of
+        # scripts/count_launches.py; ncu does not list the conditional body's kernels)
+        return 9 + 6 + 2 * rep["n_switches"] + 3 * its
+    return 9 + 3 + 5 * rep["iterations"] + 2 * (1 + rep["n_switches"]) + 2
 
 
 def _profiled_traffic():
