@@ -373,7 +373,7 @@ def estimate_launches(rep, world):
     level's count rounds up to a multiple of 8."""
     if world == 1:
         u = int(os.environ.get("GSE_CG_UNROLL", "8"))
-        u = min(max(u, 1), 8)
+        u = min(max(u, 1), 32)
         its = sum(-(-i // u) * u for i in rep["iters_per_level"] if i > 0)
         # outside the graph: 9 encode + 3 SpMV + 3 residual kernels (ncu launch list of
         # scripts/count_launches.py; ncu does not list the conditional body's kernels)

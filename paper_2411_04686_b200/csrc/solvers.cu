@@ -1497,7 +1497,7 @@ static gse_status build_cg_graph(Matrix& M, int level) {
   static const int unroll = [] {
     const char* e = getenv("GSE_CG_UNROLL");
     const int u = e ? atoi(e) : 8;
-    return u < 1 ? 1 : (u > 8 ? 8 : u);
+    return u < 1 ? 1 : (u > 32 ? 32 : u);
   }();
   const int fg = fused_grid(M);
   const bool fp = fg == 0 && cg_fuse_p(M);
