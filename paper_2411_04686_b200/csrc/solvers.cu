@@ -1494,7 +1494,7 @@ static gse_status build_cg_graph(Matrix& M, int level) {
   // iterations per pass of the while body (the kernels of an iteration after an event are
   // no-ops, so the body may hold several): each evaluation of the conditional node costs
   // ~1.7 us; 8 per body: 49.0 -> 45.5 us per C2 iteration (GSE_CG_UNROLL overrides)
-  static const int unroll = [] {
+  const int unroll = [] {  // read when a graph is built (once per matrix and level)
     const char* e = getenv("GSE_CG_UNROLL");
     const int u = e ? atoi(e) : 8;
     return u < 1 ? 1 : (u > 32 ? 32 : u);

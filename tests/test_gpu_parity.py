@@ -449,6 +449,36 @@ def test_cg_fused_p_update(g, mode, monkeypatch):
         assert np.array_equal(x1.view(np.uint64), x0.view(np.uint64))
 
 
+@pytest.mark.parametrize("mode", ["stepped_scaled", "stepped", "fp64"])
+def test_cg_graph_unroll_invariant(g, mode, monkeypatch):
+    """the CG graph's while body holds GSE_CG_UNROLL iterations; the kernels after an event
+    are no-ops, so 1, 3 (odd: events mid-body) and 8 iterations per body give bitwise the
+    same solution, iteration counts and switch points, escalations included"""
+    A = gi.poisson3d(24, "varcoef")
+    b = gi.ones_rhs(A)
+    res = []
+    for u in ("1", "3", "8"):
+        monkeypatch.setenv("GSE_CG_UNROLL", u)
+        if mode == "fp64":
+            M, sg = g.gse_fp64_matrix(A.row_ptr, A.col, A.val, A.rows, A.cols), None
+        else:
+            M = g.gse_encode(A.row_ptr, A.col, A.val, A.rows, A.cols)
+            sg = (g.gse_default_schedule("cg", l=30, t=10, m=10) if mode == "stepped_scaled"
+                  else g.gse_default_schedule("cg"))
+        x, r = g.gse_solve_cg(M, b, tol=1e-10, max_iters=5000, sched=sg)
+        res.append((x, r))
+        M.close()
+    x1, r1 = res[0]
+    assert r1["converged"]
+    if mode == "stepped_scaled":
+        assert r1["n_switches"] >= 1
+    for x, r in res[1:]:
+        assert r["iterations"] == r1["iterations"]
+        assert r["iters_per_level"] == r1["iters_per_level"]
+        assert r["switch_iter"] == r1["switch_iter"]
+        assert np.array_equal(x.view(np.uint64), x1.view(np.uint64))
+
+
 def test_cg_parity_c2_full_size(g):
     """configs[1]: 3D Poisson 128^3 stepped CG to 1e-10 on one B200 vs the oracle."""
     A = gi.poisson3d(128)
