@@ -94,6 +94,13 @@ class Clocks:
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+        # nvidia-smi's start-up (NVML init, driver locks) can stall CUDA calls for tens of
+        # ms: wait for its first sample so that happens before the timed region
+        t0 = time.time()
+        while self.proc and time.time() - t0 < 10.0:
+            if self.proc.poll() is not None or os.path.getsize(self.path) > 0:
+                break
+            time.sleep(0.05)
         time.sleep(0.25)
         return self
 

@@ -108,6 +108,129 @@ __device__ __forceinline__ void issue_stage(const SpmvParams<T>& p, const Stage<
 // index of the zero entry of the sign-folded scale tables: masked slots decode to exact 0
 constexpr uint32_t SSC_ZERO = 128;
 
+#ifndef GSE_RW_PAIR
+#define GSE_RW_PAIR 1
+#endif
+
+template <class T>
+struct Chunk8 {
+  uint32_t c[8], h[8], t1[8], t2[8];
+  double v0[8];
+  T xv[8];
+};
+
+// the 8 staged slots from j on and their gathered operands (all gathers issued here)
+template <int L, class T, bool FUSE>
+__device__ __forceinline__ void load_chunk(const SpmvParams<T>& p, const Stage<L>& st,
+                                           uint32_t j, Chunk8<T>& K, double fbeta) {
+  uint32_t* c = K.c;
+  uint32_t* h = K.h;
+  uint32_t* t1 = K.t1;
+  uint32_t* t2 = K.t2;
+  double* v0 = K.v0;
+  T* xv = K.xv;
+  // 8 slots read unconditionally at immediate offsets: the stage holds >= 8 over-copied
+  // stored entries past every row (issue_stage), so the columns are valid; slots past
+  // the row end are masked to exact zeros below
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    c[q] = st.col[j + q];
+    if constexpr (L == 0) v0[q] = st.val[j + q];
+    if constexpr (has_head<L>()) h[q] = st.head[j + q];
+    if constexpr (has_t1<L>()) t1[q] = st.tail1[j + q];
+    if constexpr (has_t2<L>()) t2[q] = st.tail2[j + q];
+  }
+  // all 8 gathers issued before any product (ld.global.nc, volatile asm keeps the order)
+  if constexpr (FUSE) {  // operand r + beta p_old (the CG p update, same rounding)
+    double rv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t cc = c[q] & p.col_mask;
+      double v, w;
+      asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p.fr + cc));
+      asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(w) : "l"(p.x + cc));
+      rv[q] = v;
+      xv[q] = (T)w;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) xv[q] = (T)__dadd_rn(rv[q], __dmul_rn(fbeta, (double)xv[q]));
+  } else {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const T* a = p.x + (c[q] & p.col_mask);
+    if constexpr (sizeof(T) == 8) {
+      double v;
+      asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(a));
+      xv[q] = v;
+    } else {
+      float v;
+      asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(a));
+      xv[q] = v;
+    }
+  }
+  }
+}
+
+// sum += the chunk's products in slot order (slots q >= nrem lie past the row end)
+template <int L, bool FAST, class T>
+__device__ __forceinline__ T sum_chunk(const SpmvParams<T>& p, const Chunk8<T>& K,
+                                       uint32_t nrem, T sum, const double* ssc64,
+                                       const float* ssc32, const long long* sd64,
+                                       const int* sd32, const double* sc64, const float* sc32) {
+  const uint32_t* c = K.c;
+  const uint32_t* h = K.h;
+  const uint32_t* t1 = K.t1;
+  const uint32_t* t2 = K.t2;
+  const double* v0 = K.v0;
+  const T* xv = K.xv;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const bool ok = (uint32_t)q < nrem;
+    T prod;
+    if constexpr (L == 0) {
+      prod = (T)__dmul_rn(ok ? v0[q] : 0.0, (double)xv[q]);
+    } else if constexpr (is_half<L>()) {  // P:406 baselines: exact code value x x in FP64
+      prod = (T)__dmul_rn(ok ? half_value<L>(h[q]) : 0.0, (double)xv[q]);
+    } else if constexpr (FAST) {
+      // scale index = EI | sign << ei_bits in one funnel shift (col's top bits are EI);
+      // a masked slot selects the zero entry
+      uint32_t idx = __funnelshift_rc(c[q], h[q] >> 15, p.ei_shift);
+      idx = ok ? idx : SSC_ZERO;
+      if constexpr (L == 1) {
+        const uint32_t D = h[q] & 0x7FFFu;
+        if constexpr (sizeof(T) == 8)
+          prod = __dmul_rn(__dmul_rn((double)D, ssc64[idx]), xv[q]);
+        else
+          prod = __fmul_rn(__fmul_rn((float)D, ssc32[idx]), xv[q]);
+      } else if constexpr (L == 2) {
+        const uint32_t D = ((h[q] & 0x7FFFu) << 16) | t1[q];
+        if constexpr (sizeof(T) == 8)
+          prod = __dmul_rn(__dmul_rn((double)D, ssc64[idx]), xv[q]);
+        else
+          prod = __fmul_rn(__fmul_rn(__uint2float_rz(D), ssc32[idx]), xv[q]);
+      } else {
+        const uint64_t D = ((uint64_t)(h[q] & 0x7FFFu) << 48) | ((uint64_t)t1[q] << 32) | t2[q];
+        if constexpr (sizeof(T) == 8)
+          prod = __dmul_rn(__dmul_rn(__ull2double_rz(D), ssc64[idx]), xv[q]);
+        else
+          prod = __fmul_rn(__fmul_rn(__ull2float_rz(D), ssc32[idx]), xv[q]);
+      }
+    } else {
+      const uint32_t ei = __funnelshift_rc(c[q], 0u, p.ei_shift);
+      const uint32_t tt1 = L >= 2 ? t1[q] : 0u, tt2 = L == 3 ? t2[q] : 0u;
+      if constexpr (sizeof(T) == 8) {
+        const double a = dec64<L, false>(h[q], tt1, tt2, sd64, sc64, ei);
+        prod = __dmul_rn(ok ? a : 0.0, xv[q]);
+      } else {
+        const float a = dec32<L, false>(h[q], tt1, tt2, sd32, sc32, ei);
+        prod = __fmul_rn(ok ? a : 0.0f, xv[q]);
+      }
+    }
+    sum += prod;
+  }
+  return sum;
+}
+
 // sum of one row, elements [j0, j1) of the stage, in storage order
 template <int L, bool FAST, class T, bool FUSE = false>
 __device__ __forceinline__ T walk_row(const SpmvParams<T>& p, const Stage<L>& st, uint32_t j0,
@@ -117,95 +240,9 @@ __device__ __forceinline__ T walk_row(const SpmvParams<T>& p, const Stage<L>& st
                                       double fbeta = 0.0) {
   T sum = 0;
   for (uint32_t j = j0; j < j1; j += 8) {
-    const uint32_t nrem = j1 - j;  // slots q >= nrem lie past the row end
-    uint32_t c[8], h[8], t1[8], t2[8];
-    double v0[8];
-    T xv[8];
-    // 8 slots read unconditionally at immediate offsets: the stage holds >= 8 over-copied
-    // stored entries past every row (issue_stage), so the columns are valid; slots past
-    // the row end are masked to exact zeros below
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      c[q] = st.col[j + q];
-      if constexpr (L == 0) v0[q] = st.val[j + q];
-      if constexpr (has_head<L>()) h[q] = st.head[j + q];
-      if constexpr (has_t1<L>()) t1[q] = st.tail1[j + q];
-      if constexpr (has_t2<L>()) t2[q] = st.tail2[j + q];
-    }
-    // all 8 gathers issued before any product (ld.global.nc, volatile asm keeps the order)
-    if constexpr (FUSE) {  // operand r + beta p_old (the CG p update, same rounding)
-      double rv[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const uint32_t cc = c[q] & p.col_mask;
-        double v, w;
-        asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p.fr + cc));
-        asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(w) : "l"(p.x + cc));
-        rv[q] = v;
-        xv[q] = (T)w;
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) xv[q] = (T)__dadd_rn(rv[q], __dmul_rn(fbeta, (double)xv[q]));
-    } else {
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const T* a = p.x + (c[q] & p.col_mask);
-      if constexpr (sizeof(T) == 8) {
-        double v;
-        asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(a));
-        xv[q] = v;
-      } else {
-        float v;
-        asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(a));
-        xv[q] = v;
-      }
-    }
-    }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const bool ok = (uint32_t)q < nrem;
-      T prod;
-      if constexpr (L == 0) {
-        prod = (T)__dmul_rn(ok ? v0[q] : 0.0, (double)xv[q]);
-      } else if constexpr (is_half<L>()) {  // P:406 baselines: exact code value x x in FP64
-        prod = (T)__dmul_rn(ok ? half_value<L>(h[q]) : 0.0, (double)xv[q]);
-      } else if constexpr (FAST) {
-        // scale index = EI | sign << ei_bits in one funnel shift (col's top bits are EI);
-        // a masked slot selects the zero entry
-        uint32_t idx = __funnelshift_rc(c[q], h[q] >> 15, p.ei_shift);
-        idx = ok ? idx : SSC_ZERO;
-        if constexpr (L == 1) {
-          const uint32_t D = h[q] & 0x7FFFu;
-          if constexpr (sizeof(T) == 8)
-            prod = __dmul_rn(__dmul_rn((double)D, ssc64[idx]), xv[q]);
-          else
-            prod = __fmul_rn(__fmul_rn((float)D, ssc32[idx]), xv[q]);
-        } else if constexpr (L == 2) {
-          const uint32_t D = ((h[q] & 0x7FFFu) << 16) | t1[q];
-          if constexpr (sizeof(T) == 8)
-            prod = __dmul_rn(__dmul_rn((double)D, ssc64[idx]), xv[q]);
-          else
-            prod = __fmul_rn(__fmul_rn(__uint2float_rz(D), ssc32[idx]), xv[q]);
-        } else {
-          const uint64_t D = ((uint64_t)(h[q] & 0x7FFFu) << 48) | ((uint64_t)t1[q] << 32) | t2[q];
-          if constexpr (sizeof(T) == 8)
-            prod = __dmul_rn(__dmul_rn(__ull2double_rz(D), ssc64[idx]), xv[q]);
-          else
-            prod = __fmul_rn(__fmul_rn(__ull2float_rz(D), ssc32[idx]), xv[q]);
-        }
-      } else {
-        const uint32_t ei = __funnelshift_rc(c[q], 0u, p.ei_shift);
-        const uint32_t tt1 = L >= 2 ? t1[q] : 0u, tt2 = L == 3 ? t2[q] : 0u;
-        if constexpr (sizeof(T) == 8) {
-          const double a = dec64<L, false>(h[q], tt1, tt2, sd64, sc64, ei);
-          prod = __dmul_rn(ok ? a : 0.0, xv[q]);
-        } else {
-          const float a = dec32<L, false>(h[q], tt1, tt2, sd32, sc32, ei);
-          prod = __fmul_rn(ok ? a : 0.0f, xv[q]);
-        }
-      }
-      sum += prod;
-    }
+    Chunk8<T> K;
+    load_chunk<L, T, FUSE>(p, st, j, K, fbeta);
+    sum = sum_chunk<L, FAST, T>(p, K, j1 - j, sum, ssc64, ssc32, sd64, sd32, sc64, sc32);
   }
   return sum;
 }
@@ -318,10 +355,38 @@ __global__ void __launch_bounds__(SPMV_THREADS, RW_MINB(L)) k_spmv_rw(const Spmv
     }
     mbar_wait(&bars[warp][cur], (it >> 1) & 1u);
     const Stage<L> st(wbase + cur * SB, N);
+    T sums[RPL];
+    bool paired = false;
+#if GSE_RW_PAIR
+    if constexpr (RPL == 2 && sizeof(T) == 4) {
+      // both rows of the lane fit one 8-slot chunk (stencils): issue the 16 gathers of the
+      // two rows before any product.  FP32 accumulation only: C2 level-1 cold 4221 -> 4566
+      // GB/s; with FP64 accumulation it lost (steady 5253 -> 4855 GB/s, CG 46.0 -> 49.9 us
+      // per iteration; profiles/ab_rw_pair_r01.txt)
+      const uint32_t n0 = ea[0] - cur_b.a[0], n1 = ea[1] - cur_b.a[1];
+      if (__all_sync(0xFFFFFFFFu, n0 <= 8u && n1 <= 8u)) {
+        Chunk8<T> K0, K1;
+        load_chunk<L, T, FUSE>(p, st, cur_b.a[0] - base, K0, fb);
+        load_chunk<L, T, FUSE>(p, st, cur_b.a[1] - base, K1, fb);
+        sums[0] = n0 ? sum_chunk<L, FAST, T>(p, K0, n0, T(0), ssc64, ssc32, sd64, sd32, sc64,
+                                             sc32)
+                     : T(0);
+        sums[1] = n1 ? sum_chunk<L, FAST, T>(p, K1, n1, T(0), ssc64, ssc32, sd64, sd32, sc64,
+                                             sc32)
+                     : T(0);
+        paired = true;
+      }
+    }
+#endif
+    if (!paired) {
+#pragma unroll
+      for (int k = 0; k < RPL; ++k)
+        sums[k] = walk_row<L, FAST, T, FUSE>(p, st, cur_b.a[k] - base, ea[k] - base, ssc64,
+                                             ssc32, sd64, sd32, sc64, sc32, fb);
+    }
 #pragma unroll
     for (int k = 0; k < RPL; ++k) {
-      const T sa = walk_row<L, FAST, T, FUSE>(p, st, cur_b.a[k] - base, ea[k] - base, ssc64,
-                                              ssc32, sd64, sd32, sc64, sc32, fb);
+      const T sa = sums[k];
       const uint32_t row = r0 + 32 * k + lane;
       if (row < rows) {
         p.y[row] = sa;
