@@ -108,7 +108,7 @@ typedef struct {
   int device;
   size_t plane_bytes[5]; /* col_ei, head, tail1, tail2, side_ei (kind GSE); col, val (FP64);
                           col, 16-bit codes (FP16 / BF16)                                 */
-  int spmv_mode;      /* SpMV kernel chosen at encode: 0 = warp blocks, 1 = row walk */
+  int spmv_mode;      /* SpMV kernel chosen at encode: 1 = row walk, 2 = x window (0 = warp blocks, A/B only) */
 } gse_matrix_info;
 
 /* ---------------------------------------------------------------------------------------

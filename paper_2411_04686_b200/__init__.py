@@ -42,6 +42,13 @@ ABI_SYMBOLS = (
 
 
 def _load():
+    # torch (when installed) goes first: the library needs libnccl.so.2, and torch's bundled
+    # NCCL must be the copy the process loads (a system NCCL loaded first shadows it and
+    # torch's CUDA library then fails to resolve its symbols)
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
     if LIB_PATH == _build.LIB and _build.stale():
         if shutil.which(_build.NVCC) or os.path.exists(_build.NVCC):
             _build.build()

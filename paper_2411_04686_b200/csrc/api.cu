@@ -199,7 +199,8 @@ static void destroy_matrix(Matrix& M) {
   cudaStream_t s = nullptr;
   free_solver_ws(M);
   free_dist(M);
-  void* ps[] = {M.row_ptr, M.col_ei, M.side_ei, M.head, M.tail1, M.tail2, M.val, M.blocks, M.dtab};
+  void* ps[] = {M.row_ptr, M.col_ei, M.side_ei, M.head, M.tail1, M.tail2, M.val, M.blocks,
+                M.tiles, M.rowbits, M.chunk_prev, M.dtab};
   for (void* p : ps) dev_free(p, s);
   cudaStreamSynchronize(s);
 }

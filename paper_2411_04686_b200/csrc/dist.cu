@@ -730,6 +730,8 @@ gse_status gse_encode_dist(gse_dist Dh, const gse_csr_f64* A, int64_t row_begin,
     *out = nullptr;
     return GSE_ERR_OOM;
   }
+  // x_ext starts zeroed: no SpMV ever reads pool garbage
+  GSE_CUDA_TRY(cudaMemsetAsync(D->d_xext, 0, sizeof(double) * ((size_t)(n_local + D->n_halo) + 1), s));
   if (so)
     GSE_CUDA_TRY(cudaMemcpyAsync(D->d_send_idx, send_idx.data(), 4 * so, cudaMemcpyHostToDevice, s));
   M->dist = D;

@@ -11,10 +11,8 @@
 //                   D = 1<<(63-d) | f<<(11-d) (or f>>(d-11)), truncation (R1); zero ->
 //                   signed zero (R2); d > 63 -> signed zero (R3); split head/tail1/tail2
 //                   (P:163); EI into the column index or the side array.
-#include <cub/cub.cuh>
 #include <cstdlib>
 #include <cstring>
-#include <thrust/iterator/counting_iterator.h>
 
 #include "decode.cuh"
 #include "gse_internal.cuh"
@@ -352,6 +350,143 @@ __global__ void k_fill_desc(const uint32_t* __restrict__ starts, const int* __re
   }
 }
 
+// ---- stream compaction of row flags (hand-written; ascending, deterministic): 3 kernels,
+// 4096 flags per CTA -- counts, one-CTA exclusive scan of the counts, ordered scatter.
+constexpr int CMP_THREADS = 256, CMP_ITEMS = 16, CMP_TILE = CMP_THREADS * CMP_ITEMS;
+
+// exclusive scan of one value per thread over the CTA (blockDim.x <= 1024); *total gets the sum
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total) {
+  __shared__ uint32_t wsum[32], wtot;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  uint32_t inc = v;
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+    if (lane >= d) inc += o;
+  }
+  __syncthreads();  // wsum reuse across calls
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < nw ? wsum[lane] : 0u, wi = w;
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, wi, d);
+      if (lane >= d) wi += o;
+    }
+    if (lane < nw) wsum[lane] = wi - w;
+    if (lane == 31) wtot = wi;  // lanes >= nw add 0: lane 31 holds the CTA total
+  }
+  __syncthreads();
+  *total = wtot;
+  return wsum[warp] + inc - v;
+}
+
+__global__ void __launch_bounds__(CMP_THREADS) k_cmp_count(const uint8_t* __restrict__ f,
+                                                            int64_t n, uint32_t* __restrict__ cnt) {
+  const int64_t base = (int64_t)blockIdx.x * CMP_TILE + (int64_t)threadIdx.x * CMP_ITEMS;
+  uint32_t c = 0;
+  for (int i = 0; i < CMP_ITEMS; ++i) c += (base + i < n && f[base + i]) ? 1u : 0u;
+  uint32_t tot;
+  block_excl_scan(c, &tot);
+  if (threadIdx.x == 0) cnt[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) k_cmp_scan(uint32_t* __restrict__ cnt, int64_t nb,
+                                                   int* __restrict__ total) {
+  uint32_t run = 0;
+  for (int64_t b0 = 0; b0 < nb; b0 += 1024) {
+    const int64_t i = b0 + threadIdx.x;
+    const uint32_t v = i < nb ? cnt[i] : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_excl_scan(v, &tot);
+    if (i < nb) cnt[i] = run + ex;
+    run += tot;
+  }
+  if (threadIdx.x == 0) *total = (int)run;
+}
+
+__global__ void __launch_bounds__(CMP_THREADS) k_cmp_scatter(const uint8_t* __restrict__ f,
+                                                              int64_t n,
+                                                              const uint32_t* __restrict__ off,
+                                                              uint32_t* __restrict__ out) {
+  const int64_t base = (int64_t)blockIdx.x * CMP_TILE + (int64_t)threadIdx.x * CMP_ITEMS;
+  uint32_t c = 0;
+  for (int i = 0; i < CMP_ITEMS; ++i) c += (base + i < n && f[base + i]) ? 1u : 0u;
+  uint32_t tot;
+  uint32_t o = off[blockIdx.x] + block_excl_scan(c, &tot);
+  for (int i = 0; i < CMP_ITEMS; ++i)
+    if (base + i < n && f[base + i]) out[o++] = (uint32_t)(base + i);
+}
+
+// indices of the set flags, ascending, into out[]; the count lands in *d_count (device)
+static gse_status compact_flags(const uint8_t* flags, int64_t n, uint32_t* out, int* d_count,
+                                cudaStream_t s) {
+  const int64_t nb = (n + CMP_TILE - 1) / CMP_TILE;
+  if (nb == 0) return cuda_status(cudaMemsetAsync(d_count, 0, sizeof(int), s), "memset");
+  uint32_t* cnt = dev_alloc_n<uint32_t>((size_t)nb, s);
+  if (!cnt) return GSE_ERR_OOM;
+  k_cmp_count<<<(unsigned)nb, CMP_THREADS, 0, s>>>(flags, n, cnt);
+  k_cmp_scan<<<1, 1024, 0, s>>>(cnt, nb, d_count);
+  k_cmp_scatter<<<(unsigned)nb, CMP_THREADS, 0, s>>>(flags, n, cnt, out);
+  GSE_CUDA_TRY(cudaGetLastError());
+  dev_free(cnt, s);
+  return GSE_OK;
+}
+
+// ---- window-mode structures (spmv_win.cu) ------------------------------------------------
+// tile starts: row 0, a row whose start crosses a WIN_TNNZ boundary of the non-zero stream,
+// and every WIN_RMAX-th row (bounds a tile's x window); also counts the empty rows
+__global__ void k_tile_flags(const uint32_t* __restrict__ rp, int64_t rows,
+                             uint8_t* __restrict__ flag, unsigned long long* __restrict__ n_empty) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long ne = 0;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += stride) {
+    const uint32_t a = rp[r];
+    bool st = (r == 0) || (r % WIN_RMAX == 0);
+    if (!st) st = a / WIN_TNNZ != rp[r - 1] / WIN_TNNZ;
+    flag[r] = st ? 1 : 0;
+    ne += (rp[r + 1] == a) ? 1u : 0u;
+  }
+  for (int o = 16; o > 0; o >>= 1) ne += __shfl_down_sync(0xFFFFFFFFu, ne, o);
+  if ((threadIdx.x & 31) == 0 && ne) atomicAdd(n_empty, ne);
+}
+
+// bit rp[r] of the non-zero stream for every non-empty row r, plus a sentinel start at
+// nnz: the matrix's last row then closes like every other row (spmv_win.cu)
+__global__ void k_row_bits(const uint32_t* __restrict__ rp, int64_t rows,
+                           uint32_t* __restrict__ bits) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const uint32_t z = rp[rows];
+    atomicOr(bits + (z >> 5), 1u << (z & 31u));
+  }
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += stride) {
+    const uint32_t a = rp[r];
+    if (rp[r + 1] > a) atomicOr(bits + (a >> 5), 1u << (a & 31u));
+  }
+}
+
+// chunk_prev[c] = the row holding non-zero c * WIN_CH - 1 (the last r with rp[r] <= q)
+__global__ void k_chunk_prev(const uint32_t* __restrict__ rp, int64_t rows, int64_t nch,
+                             uint32_t* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nch; c += stride) {
+    if (c == 0) {
+      out[0] = 0xFFFFFFFFu;
+      continue;
+    }
+    const uint32_t q = (uint32_t)(c * WIN_CH - 1);
+    int64_t lo = 0, hi = rows;  // rp[lo] <= q < rp[hi] (q < nnz = rp[rows])
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (rp[mid] <= q)
+        lo = mid;
+      else
+        hi = mid;
+    }
+    out[c] = (uint32_t)lo;
+  }
+}
+
 static int grid_for(int64_t n, int threads, int dev) {
   int64_t g = (n + threads - 1) / threads;
   int64_t cap = (int64_t)num_sms(dev) * 8;
@@ -412,50 +547,60 @@ __global__ void k_group_stats(const uint32_t* __restrict__ rp, int64_t rows,
 
 static void choose_mode(Matrix& M) {
   // Row-walk needs every group staged (no heavy group) and little divergence between the
-  // 32 rows of a group; otherwise the strided-products kernel balances the load.
+  // 32 rows of a group; otherwise the window kernel (spmv_win.cu) balances the load.
+  // GSE_SPMV_MODE=sp|rw|win forces a kernel (A/B measurements).
   const char* env = getenv("GSE_SPMV_MODE");
   const bool rw_ok = M.heavy_groups == 0 && M.rows > 0 && M.ei_in_column;
-  int mode = (rw_ok && M.rw_efficiency >= 0.6) ? SPMV_RW : SPMV_SP;
+  int mode = (rw_ok && M.rw_efficiency >= 0.6) ? SPMV_RW : SPMV_WIN;
   if (env && !strcmp(env, "sp")) mode = SPMV_SP;
+  if (env && !strcmp(env, "win")) mode = SPMV_WIN;
   if (env && !strcmp(env, "rw") && rw_ok) mode = SPMV_RW;
   M.spmv_mode = mode;
 }
 
-// One host sync for the whole partition: the group statistics, the block-start selection
-// and (optionally) the caller's status word are read back together.
+// One host sync for the whole partition: the group statistics, both row selections (SP
+// warp blocks, window tiles), the empty-row count and (optionally) the caller's status word
+// are read back together.
 gse_status build_partition(Matrix& M, cudaStream_t s, const void* extra_d, void* extra_h,
                            size_t extra_bytes) {
   M.n_blocks = 0;
+  M.n_tiles = 0;
   M.n_groups = (M.rows + RW_ROWS - 1) / RW_ROWS;
   if (M.rows == 0) {
     choose_mode(M);
     M.blocks = dev_alloc_n<BlockDesc>(1, s);
-    if (!M.blocks) return GSE_ERR_OOM;
+    M.tiles = dev_alloc_n<BlockDesc>(1, s);
+    if (!M.blocks || !M.tiles) return GSE_ERR_OOM;
     BlockDesc h{0, 0};
     GSE_CUDA_TRY(cudaMemcpyAsync(M.blocks, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+    GSE_CUDA_TRY(cudaMemcpyAsync(M.tiles, &h, sizeof(h), cudaMemcpyHostToDevice, s));
     if (extra_bytes)
       GSE_CUDA_TRY(cudaMemcpyAsync(extra_h, extra_d, extra_bytes, cudaMemcpyDeviceToHost, s));
     GSE_CUDA_TRY(cudaStreamSynchronize(s));
     return GSE_OK;
   }
-  // acc: 5 group statistics, then the selected-block count
-  unsigned long long* acc = dev_alloc_n<unsigned long long>(6, s);
+  // acc: 5 group statistics, the empty-row count, then the two selection counts (int)
+  unsigned long long* acc = dev_alloc_n<unsigned long long>(8, s);
   uint8_t* flags = dev_alloc_n<uint8_t>(M.rows, s);
+  uint8_t* tflags = dev_alloc_n<uint8_t>(M.rows, s);
   uint32_t* starts = dev_alloc_n<uint32_t>(M.rows, s);
-  if (!acc || !flags || !starts) return GSE_ERR_OOM;
-  int* nsel = reinterpret_cast<int*>(acc + 5);
-  GSE_CUDA_TRY(cudaMemsetAsync(acc, 0, 48, s));
+  uint32_t* tstarts = dev_alloc_n<uint32_t>(M.rows, s);
+  if (!acc || !flags || !tflags || !starts || !tstarts) return GSE_ERR_OOM;
+  int* nsel = reinterpret_cast<int*>(acc + 6);
+  int* ntil = reinterpret_cast<int*>(acc + 7);
+  GSE_CUDA_TRY(cudaMemsetAsync(acc, 0, 64, s));
   k_group_stats<<<grid_for(M.n_groups * 32, 256, M.device), 256, 0, s>>>(M.row_ptr, M.rows,
                                                                          acc);
   k_block_flags<<<grid_for(M.rows, 256, M.device), 256, 0, s>>>(M.row_ptr, M.rows, flags);
-  thrust::counting_iterator<uint32_t> it(0);
-  size_t tmp_bytes = 0;
-  cub::DeviceSelect::Flagged(nullptr, tmp_bytes, it, flags, starts, nsel, (int)M.rows, s);
-  void* tmp = dev_alloc(tmp_bytes + 16, s);
-  if (!tmp) return GSE_ERR_OOM;
-  cub::DeviceSelect::Flagged(tmp, tmp_bytes, it, flags, starts, nsel, (int)M.rows, s);
-  unsigned long long h[6];
-  GSE_CUDA_TRY(cudaMemcpyAsync(h, acc, 48, cudaMemcpyDeviceToHost, s));
+  k_tile_flags<<<grid_for(M.rows, 256, M.device), 256, 0, s>>>(M.row_ptr, M.rows, tflags,
+                                                               acc + 5);
+  GSE_CUDA_TRY(cudaGetLastError());
+  gse_status rc = compact_flags(flags, M.rows, starts, nsel, s);
+  if (rc != GSE_OK) return rc;
+  rc = compact_flags(tflags, M.rows, tstarts, ntil, s);
+  if (rc != GSE_OK) return rc;
+  unsigned long long h[8];
+  GSE_CUDA_TRY(cudaMemcpyAsync(h, acc, 64, cudaMemcpyDeviceToHost, s));
   if (extra_bytes)
     GSE_CUDA_TRY(cudaMemcpyAsync(extra_h, extra_d, extra_bytes, cudaMemcpyDeviceToHost, s));
   GSE_CUDA_TRY(cudaStreamSynchronize(s));
@@ -464,18 +609,37 @@ gse_status build_partition(Matrix& M, cudaStream_t s, const void* extra_d, void*
   M.max_row_len = (int64_t)h[2];
   M.rw_span = (int64_t)h[3];
   M.rw_span2 = (int64_t)h[4];
+  M.n_empty_rows = (int64_t)h[5];
   choose_mode(M);
-  int nb = 0;
-  memcpy(&nb, &h[5], sizeof(int));
+  int nb = 0, nt = 0;
+  memcpy(&nb, &h[6], sizeof(int));
+  memcpy(&nt, &h[7], sizeof(int));
   M.n_blocks = nb;
+  M.n_tiles = nt;
   M.blocks = dev_alloc_n<BlockDesc>((size_t)nb + 1, s);
-  if (!M.blocks) return GSE_ERR_OOM;
+  M.tiles = dev_alloc_n<BlockDesc>((size_t)nt + 1, s);
+  if (!M.blocks || !M.tiles) return GSE_ERR_OOM;
   k_fill_desc<<<grid_for(nb + 1, 256, M.device), 256, 0, s>>>(starts, nsel, M.row_ptr, M.rows,
                                                               M.blocks);
+  k_fill_desc<<<grid_for(nt + 1, 256, M.device), 256, 0, s>>>(tstarts, ntil, M.row_ptr, M.rows,
+                                                              M.tiles);
   GSE_CUDA_TRY(cudaGetLastError());
-  dev_free(tmp, s);
+  // window-kernel row structure: 1 bit per non-zero (whole chunks, zero past nnz) and the
+  // row before every chunk
+  const int64_t nch = (M.nnz + WIN_CH - 1) / WIN_CH + 1;
+  const size_t words = (size_t)nch * (WIN_CH / 32) + 4;
+  M.rowbits = dev_alloc_n<uint32_t>(words, s);
+  M.chunk_prev = dev_alloc_n<uint32_t>((size_t)nch, s);
+  if (!M.rowbits || !M.chunk_prev) return GSE_ERR_OOM;
+  GSE_CUDA_TRY(cudaMemsetAsync(M.rowbits, 0, words * 4, s));
+  k_row_bits<<<grid_for(M.rows, 256, M.device), 256, 0, s>>>(M.row_ptr, M.rows, M.rowbits);
+  k_chunk_prev<<<grid_for(nch, 256, M.device), 256, 0, s>>>(M.row_ptr, M.rows, nch,
+                                                            M.chunk_prev);
+  GSE_CUDA_TRY(cudaGetLastError());
   dev_free(flags, s);
+  dev_free(tflags, s);
   dev_free(starts, s);
+  dev_free(tstarts, s);
   dev_free(acc, s);
   return GSE_OK;
 }

@@ -29,7 +29,20 @@ static_assert(CHUNK - 1 + LMAX <= WTILE, "short warp block must fit one pass");
 // group's planes staged into warp-private shared memory with 16-byte loads, lane = row.
 constexpr int RW_ROWS = 32;
 constexpr int RW_TILE = 1024;  // max staged span (8-aligned non-zeros) of a row-walk group
-enum SpmvMode : int { SPMV_SP = 0, SPMV_RW = 1 };
+// Window mode (irregular rows, e.g. the power-law config; spmv_win.cu): row-aligned tiles
+// of ~WIN_TNNZ non-zeros and <= WIN_RMAX rows; the CTA stages x[R0 - WIN_HALF, R1 + WIN_HALF)
+// in shared memory by one TMA bulk copy, warps walk 256-element chunks with 8 consecutive
+// non-zeros per lane, row starts come from a 1-bit-per-non-zero bitmap (encode-time).
+constexpr int WIN_EPT = 8;                  // consecutive non-zeros per lane and chunk
+constexpr int WIN_CH = 32 * WIN_EPT;        // non-zeros per warp chunk
+constexpr uint32_t WIN_HALF = 512;          // x window reaches this many columns past the rows
+constexpr uint32_t WIN_RMAX = 2048;         // rows per tile (bounds the window)
+#ifndef GSE_WIN_TNNZ
+#define GSE_WIN_TNNZ 16384
+#endif
+constexpr uint32_t WIN_TNNZ = GSE_WIN_TNNZ; // target non-zeros per tile
+constexpr uint32_t WIN_CAP = WIN_RMAX + 2 * WIN_HALF + 8;  // window buffer (elements)
+enum SpmvMode : int { SPMV_SP = 0, SPMV_RW = 1, SPMV_WIN = 2 };
 constexpr int NNZ_PAD = 8;  // plane allocations padded to a multiple of 8 elements (+8)
 
 struct BlockDesc {
@@ -71,6 +84,12 @@ struct Matrix {
   double* val = nullptr;        // [nnz_pad] FP64 kind
   BlockDesc* blocks = nullptr;  // [n_blocks + 1]
   int64_t n_blocks = 0;
+  // window mode (spmv_win.cu)
+  BlockDesc* tiles = nullptr;     // [n_tiles + 1] {first row, its row_ptr}
+  int64_t n_tiles = 0;
+  uint32_t* rowbits = nullptr;    // bit i of the stream: a non-empty row starts at non-zero i
+  uint32_t* chunk_prev = nullptr; // [n_chunks] row holding non-zero c * WIN_CH - 1 (~0 for c = 0)
+  int64_t n_empty_rows = 0;
   int spmv_mode = SPMV_SP;      // chosen at encode from the row-length statistics
   int64_t n_groups = 0;         // ceil(rows / 32)
   int64_t heavy_groups = 0;     // groups with > RW_TILE non-zeros

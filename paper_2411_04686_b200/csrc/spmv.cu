@@ -1,6 +1,7 @@
 // spmv.cu -- SpMV entry points: build the kernel parameters for the
 // requested level and dispatch to the kernel the encoder chose for this matrix
-// (Matrix::spmv_mode: spmv_rw.cu for regular rows, spmv_sp.cu otherwise).
+// (Matrix::spmv_mode: spmv_rw.cu for regular rows, spmv_win.cu otherwise; spmv_sp.cu on
+// request for A/B).
 // "SpMV kernel" for the design and profiles/ for the measurements behind it.
 #include <cstdlib>
 #include <cstring>
@@ -42,6 +43,12 @@ static SpmvParams<T> make_params(const Matrix& M, int level, const T* x, T* y,
   p.ticket = dot ? dot->ticket : nullptr;
   p.dot_result = dot ? dot->result : nullptr;
   p.stop = nullptr;
+  p.tiles = M.tiles;
+  p.rowbits = reinterpret_cast<const uint8_t*>(M.rowbits);
+  p.chunk_prev = M.chunk_prev;
+  p.n_tiles = (uint32_t)M.n_tiles;
+  p.cols = (uint32_t)dist_ext_cols(M);
+  p.win_on = ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) ? 1 : 0;
   const int L = level >= 1 && level <= 3 ? level : 3;
   for (int i = 0; i < 64; ++i) {
     p.d64[i] = M.htab.d64[L - 1][i];
@@ -52,14 +59,7 @@ static SpmvParams<T> make_params(const Matrix& M, int level, const T* x, T* y,
   return p;
 }
 
-static int mode_of(const Matrix& M) {
-  // A/B knob for measurements: GSE_SPMV_MODE=sp forces the strided-products kernel
-  static const int forced = [] {
-    const char* e = getenv("GSE_SPMV_MODE");
-    return (e && !strcmp(e, "sp")) ? 0 : -1;
-  }();
-  return forced == 0 ? (int)SPMV_SP : M.spmv_mode;
-}
+static int mode_of(const Matrix& M) { return M.spmv_mode; }
 
 template <class T>
 static void dispatch(const Matrix& M, int level, bool dot, const SpmvParams<T>& p,
@@ -67,8 +67,11 @@ static void dispatch(const Matrix& M, int level, bool dot, const SpmvParams<T>& 
   const int L = level >= 1 && level <= 3 ? level : 3;
   const bool fast = M.kind == GSE_KIND_GSE &&
                     (sizeof(T) == 8 ? M.htab.fast64[L - 1] : M.htab.fast32[L - 1]);
-  if (mode_of(M) == SPMV_RW)
+  const int mode = mode_of(M);
+  if (mode == SPMV_RW)
     launch_rw<T>(M, level, dot, fast, p, s);
+  else if (mode == SPMV_WIN)
+    launch_win<T>(M, level, dot, fast, p, s);
   else
     launch_sp<T>(M, level, dot, fast, p, s);
 }

@@ -18,6 +18,13 @@ __device__ __forceinline__ uint64_t l2_evict_first() {
   asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+// x (the SpMV operand) is re-read by every tile window and by the far gathers: its lines
+// carry evict-last so the streamed planes do not push it out of L2
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ uint32_t ld_nc_u32(const uint32_t* p) {
   uint32_t r;
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
@@ -59,6 +66,47 @@ __device__ __forceinline__ uint2 ld_nc_v2(const void* p) {
       : "=r"(r.x), "=r"(r.y)
       : "l"(p), "l"(l2_evict_first()));
   return r;
+}
+
+// ---- mbarrier + TMA bulk-copy helpers (row-walk stages, window-kernel x windows)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(l2_evict_first())
+      : "memory");
+}
+// the same with an evict-last hint (x windows: re-read by neighbouring tiles and gathers)
+__device__ __forceinline__ void bulk_g2s_keep(void* dst, const void* src, uint32_t bytes,
+                                              uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(l2_evict_last())
+      : "memory");
 }
 
 // Kernel "levels": 0 = FP64 CSR (a6), 1..3 = GSE segments (a5), and the 16-bit storage
@@ -107,6 +155,13 @@ struct SpmvParams {
   unsigned* ticket;
   double* dot_result;
   const int* stop;    // optional: skip the launch when *stop != 0 (GMRES cycle graphs)
+  // window mode (spmv_win.cu)
+  const BlockDesc* __restrict__ tiles;
+  const uint8_t* __restrict__ rowbits;
+  const uint32_t* __restrict__ chunk_prev;
+  uint32_t n_tiles;
+  uint32_t cols;
+  int win_on;         // x is 16-byte aligned: windows staged by TMA (else every gather is global)
   // CG p update fused into the SpMV (row walk, FP64; x is p_old): the operand is
   // r + beta p_old, p_new and x += alpha p_old are written for the launch's rows
   const double* fr;
@@ -240,6 +295,9 @@ void launch_sp(const Matrix& M, int level, bool dot, bool fast, const SpmvParams
 template <class T>
 void launch_rw(const Matrix& M, int level, bool dot, bool fast, const SpmvParams<T>& p,
                cudaStream_t s);
+template <class T>
+void launch_win(const Matrix& M, int level, bool dot, bool fast, const SpmvParams<T>& p,
+                cudaStream_t s);
 
 // persistent grid size for a kernel: resident CTAs per SM x SMs, capped by the work units
 template <class K>

@@ -25,37 +25,6 @@
 
 namespace gse {
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(l2_evict_first())
-      : "memory");
-}
-
 // bytes per staged element at level L (col_ei + requested planes; L = 0: FP64 values)
 template <int L>
 __host__ __device__ constexpr uint32_t rw_elem_bytes() {
@@ -186,44 +155,45 @@ __device__ __forceinline__ T sum_chunk(const SpmvParams<T>& p, const Chunk8<T>& 
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const bool ok = (uint32_t)q < nrem;
+    // slots past the row end take x = 0 (their decoded values are finite stored entries or
+    // the zero padding), so a NaN / Inf in x reaches only the rows that reference it
+    const T xq = ok ? xv[q] : (T)0;
     T prod;
     if constexpr (L == 0) {
-      prod = (T)__dmul_rn(ok ? v0[q] : 0.0, (double)xv[q]);
+      prod = (T)__dmul_rn(ok ? v0[q] : 0.0, (double)xq);  // (FP64 kind: values unchecked)
     } else if constexpr (is_half<L>()) {  // P:406 baselines: exact code value x x in FP64
-      prod = (T)__dmul_rn(ok ? half_value<L>(h[q]) : 0.0, (double)xv[q]);
+      prod = (T)__dmul_rn(ok ? half_value<L>(h[q]) : 0.0, (double)xq);  // (codes may be +-Inf)
     } else if constexpr (FAST) {
-      // scale index = EI | sign << ei_bits in one funnel shift (col's top bits are EI);
-      // a masked slot selects the zero entry
-      uint32_t idx = __funnelshift_rc(c[q], h[q] >> 15, p.ei_shift);
-      idx = ok ? idx : SSC_ZERO;
+      // scale index = EI | sign << ei_bits in one funnel shift (col's top bits are EI)
+      const uint32_t idx = __funnelshift_rc(c[q], h[q] >> 15, p.ei_shift);
       if constexpr (L == 1) {
         const uint32_t D = h[q] & 0x7FFFu;
         if constexpr (sizeof(T) == 8)
-          prod = __dmul_rn(__dmul_rn((double)D, ssc64[idx]), xv[q]);
+          prod = __dmul_rn(__dmul_rn((double)D, ssc64[idx]), xq);
         else
-          prod = __fmul_rn(__fmul_rn((float)D, ssc32[idx]), xv[q]);
+          prod = __fmul_rn(__fmul_rn((float)D, ssc32[idx]), xq);
       } else if constexpr (L == 2) {
         const uint32_t D = ((h[q] & 0x7FFFu) << 16) | t1[q];
         if constexpr (sizeof(T) == 8)
-          prod = __dmul_rn(__dmul_rn((double)D, ssc64[idx]), xv[q]);
+          prod = __dmul_rn(__dmul_rn((double)D, ssc64[idx]), xq);
         else
-          prod = __fmul_rn(__fmul_rn(__uint2float_rz(D), ssc32[idx]), xv[q]);
+          prod = __fmul_rn(__fmul_rn(__uint2float_rz(D), ssc32[idx]), xq);
       } else {
         const uint64_t D = ((uint64_t)(h[q] & 0x7FFFu) << 48) | ((uint64_t)t1[q] << 32) | t2[q];
         if constexpr (sizeof(T) == 8)
-          prod = __dmul_rn(__dmul_rn(__ull2double_rz(D), ssc64[idx]), xv[q]);
+          prod = __dmul_rn(__dmul_rn(__ull2double_rz(D), ssc64[idx]), xq);
         else
-          prod = __fmul_rn(__fmul_rn(__ull2float_rz(D), ssc32[idx]), xv[q]);
+          prod = __fmul_rn(__fmul_rn(__ull2float_rz(D), ssc32[idx]), xq);
       }
     } else {
       const uint32_t ei = __funnelshift_rc(c[q], 0u, p.ei_shift);
       const uint32_t tt1 = L >= 2 ? t1[q] : 0u, tt2 = L == 3 ? t2[q] : 0u;
       if constexpr (sizeof(T) == 8) {
         const double a = dec64<L, false>(h[q], tt1, tt2, sd64, sc64, ei);
-        prod = __dmul_rn(ok ? a : 0.0, xv[q]);
+        prod = __dmul_rn(a, xq);
       } else {
         const float a = dec32<L, false>(h[q], tt1, tt2, sd32, sc32, ei);
-        prod = __fmul_rn(ok ? a : 0.0f, xv[q]);
+        prod = __fmul_rn(a, xq);
       }
     }
     sum += prod;

@@ -188,11 +188,11 @@ def test_spmv_levels_parity(g, name):
 
 @pytest.mark.parametrize("k", [1, 2, 8, 16, 64])
 def test_spmv_k_sweep_parity(g, k):
-    """strided-products kernel: register scale table (k <= 8, exponent span < 256) and the
-    shared-memory table (k = 16, 64) at all levels, FP64 and FP32 accumulation"""
+    """window kernel (power-law rows): scale tables of 1..64 entries (1-6 EI bits) at all
+    levels, FP64 and FP32 accumulation"""
     A = gi.powerlaw_spd(20000, seed=11 + k)
     M, R = enc_both(g, A, k)
-    assert M.info["spmv_mode"] == 0
+    assert M.info["spmv_mode"] == 2
     x = gi.uniform_vec(A.cols, seed=5)
     for L in (1, 2, 3):
         yg = g.gse_spmv(M, x, segments=L)
@@ -219,7 +219,7 @@ def short_rows_matrix():
     return gi.Csr(rows, cols, rp, col, val, "short_rows")
 
 
-@pytest.mark.parametrize("mode", ["sp", "auto"])
+@pytest.mark.parametrize("mode", ["sp", "win", "auto"])
 def test_spmv_short_rows_and_sp_cg(g, mode, monkeypatch):
     A = short_rows_matrix()
     M, R = enc_both(g, A)
@@ -231,11 +231,11 @@ def test_spmv_short_rows_and_sp_cg(g, mode, monkeypatch):
         assert np.all(np.abs(yg - yo) <= bound), L
         assert np.all(yg[bound == 0] == 0.0)
     # CG through the strided kernel's fused dot (DOT variant) on an SPD stencil
-    if mode == "sp":
-        monkeypatch.setenv("GSE_SPMV_MODE", "sp")
+    if mode != "auto":
+        monkeypatch.setenv("GSE_SPMV_MODE", mode)
     B = gi.poisson3d(20, "varcoef")
     Mb, Rb = enc_both(g, B)
-    assert (Mb.info["spmv_mode"] == 0) == (mode == "sp")
+    assert Mb.info["spmv_mode"] == {"sp": 0, "win": 2, "auto": 1}[mode]
     b = gi.ones_rhs(B)
     _, rg = g.gse_solve_cg(Mb, b, tol=1e-10, sched=g.gse_default_schedule("cg", l=30, t=10, m=10))
     _, ro = O.cg(Rb, b, tol=1e-10, sched=O.schedule("cg", l=30, t=10, m=10))
@@ -289,6 +289,83 @@ def test_spmv_row_walk_rows_per_lane(g, name, rpl, monkeypatch):
     Fo = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
     Fa = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, np.abs(A.val))
     assert np.all(np.abs(yf - O.spmv_fp64(Fo, x)) <= 1e-12 * O.spmv_fp64(Fa, np.abs(x)))
+
+
+def window_edge_matrix(kind):
+    """window-kernel edges (spmv_win.cu): 'huge' -- one row of 70000 non-zeros (longer than a
+    tile, spans every warp of its CTA) among 1-entry rows (tiles capped at WIN_RMAX = 2048
+    rows); 'banded_empty' -- partners within the x window plus 10 % empty rows (row lookup
+    path); 'wide' -- 3000 rows x 400000 columns (window clipped, mostly global gathers)"""
+    rng = np.random.default_rng({"huge": 31, "banded_empty": 32, "wide": 33}[kind])
+    if kind == "huge":
+        lens = np.concatenate([np.ones(5000, np.int64), [70000], np.ones(3000, np.int64),
+                               rng.integers(1, 40, 3000)])
+        rows, cols = lens.size, 80000
+        col = [np.sort(rng.choice(cols, L, replace=False)) for L in lens]
+    elif kind == "banded_empty":
+        rows = cols = 60000
+        lens = rng.integers(1, 30, rows)
+        lens[rng.random(rows) < 0.1] = 0
+        col = []
+        for r, L in enumerate(lens):
+            c = np.unique(np.clip(r + rng.integers(-600, 600, L), 0, cols - 1))
+            col.append(c)
+        lens = np.array([c.size for c in col])
+    else:
+        rows, cols = 3000, 400000
+        lens = rng.integers(0, 60, rows)
+        col = [np.sort(rng.choice(cols, L, replace=False)) for L in lens]
+    rp = np.zeros(rows + 1, np.int64)
+    np.cumsum(lens, out=rp[1:])
+    colv = np.concatenate(col).astype(np.int32)
+    val = rng.uniform(-2, 2, rp[-1]) * np.ldexp(1.0, rng.integers(-8, 8, rp[-1]))
+    return gi.Csr(rows, cols, rp, colv, val, kind)
+
+
+@pytest.mark.parametrize("kind", ["huge", "banded_empty", "wide"])
+def test_spmv_window_edges(g, kind):
+    """window kernel against the oracle at every level, FP64 / FP32 accumulation, the
+    FP64-CSR comparator and an x that is not 16-byte aligned (window staging off)"""
+    A = window_edge_matrix(kind)
+    M, R = enc_both(g, A)
+    assert M.info["spmv_mode"] == 2
+    x = gi.uniform_vec(A.cols, seed=4)
+    buf = torch.empty(A.cols + 1, dtype=torch.float64, device="cuda")
+    xu = buf[1:]
+    xu.copy_(torch.from_numpy(x))
+    for L in (1, 2, 3):
+        yo = O.spmv_gse(R, x, L)
+        bound = spmv_bound(R, x, L, 1e-12)
+        for xin in (torch.from_numpy(x).cuda(), xu):
+            yg = g.gse_spmv(M, xin, segments=L).cpu().numpy()
+            bad = np.abs(yg - yo) > bound
+            assert not bad.any(), (kind, L, np.nonzero(bad)[0][:5])
+            assert np.all(yg[bound == 0] == 0.0)
+        yf = g.gse_spmv_f32acc(M, x.astype(np.float32), segments=L).astype(np.float64)
+        x32 = x.astype(np.float32).astype(np.float64)
+        assert np.all(np.abs(yf - O.spmv_gse(R, x32, L)) <= spmv_bound(R, x32, L, 1e-5)), L
+    F = g.gse_fp64_matrix(A.row_ptr, A.col, A.val, A.rows, A.cols)
+    yF = g.gse_spmv(F, x, segments=3)
+    yo = O.spmv_fp64(O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val), x)
+    absF = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, np.abs(A.val))
+    assert np.all(np.abs(yF - yo) <= 1e-12 * O.spmv_fp64(absF, np.abs(x)))
+
+
+def test_spmv_window_nan_isolation(g):
+    """a non-finite x entry reaches only the rows that reference its column (masked lanes
+    and slots never multiply it), in both irregular- and regular-row kernels"""
+    for A in (gi.powerlaw_spd(20000, seed=3), gi.poisson3d(24, "varcoef")):
+        M, R = enc_both(g, A)
+        x = gi.uniform_vec(A.cols, seed=9)
+        bad_col = A.cols // 2
+        x[bad_col] = np.nan
+        touched = np.zeros(A.rows, bool)
+        rr = np.repeat(np.arange(A.rows), np.diff(A.row_ptr))
+        touched[rr[A.col == bad_col]] = True
+        for L in (1, 3):
+            y = g.gse_spmv(M, x, segments=L)
+            assert np.all(np.isnan(y[touched])), L
+            assert np.all(np.isfinite(y[~touched])), (L, np.nonzero(~np.isfinite(y) & ~touched)[0][:5])
 
 
 def test_spmv_head_exact_poisson_bitwise(g):
@@ -632,7 +709,7 @@ def test_spmv_full_size_c3_sampled(g):
     O.set_threads(0)
     A = gi.powerlaw_spd(10_000_000, seed=42)
     M = _sampled_rows_parity(g, A, gi.uniform_vec(A.cols, seed=7), fp32=True, fp64_too=True)
-    assert M.info["spmv_mode"] == 0
+    assert M.info["spmv_mode"] == 2
 
 
 def test_spmv_full_size_c4_sampled_and_gmres(g):
