@@ -73,7 +73,7 @@ class OrcSchedule(C.Structure):
         ("l", C.c_int64), ("t", C.c_int64), ("m", C.c_int64),
         ("rsd_limit", C.c_double), ("ndec_limit", C.c_int64), ("reldec_limit", C.c_double),
         ("verify_at_full", C.c_int), ("level_floor", C.c_double * 2),
-        ("krylov_gse16", C.c_int),
+        ("krylov_gse16", C.c_int), ("perturb_c", C.c_double),
     ]
 
 
@@ -124,6 +124,7 @@ def _declare(L):
     L.orc_reldec.argtypes = [_p(dbl), i64]
     L.orc_reldec.restype = dbl
     L.orc_should_escalate.argtypes = [_p(dbl), i64, dbl, i64, dbl]
+    L.orc_perturbation_bounds.argtypes = [C.c_void_p, _p(dbl)]
     L.orc_default_schedule.argtypes = [i32, _p(OrcSchedule)]
     L.orc_default_schedule.restype = None
     L.orc_cg.argtypes = [_p(OrcMatrix), _p(dbl), _p(dbl), dbl, i64, _p(OrcSchedule),
@@ -458,6 +459,16 @@ def spmv_gse(A: GseCsr, x, level: int) -> np.ndarray:
     if st != OK:
         raise OracleError(st, "spmv_gse")
     return y
+
+
+def perturbation_bounds(A: GseCsr) -> tuple:
+    """R29: (eta_1, eta_2), eta_L = max_i sum_j |dec_3(a_ij) - dec_L(a_ij)|."""
+    m = A.orc()
+    eta = np.zeros(2)
+    st = lib().orc_perturbation_bounds(C.byref(m), _ptr(eta, C.c_double))
+    if st != 0:
+        raise OracleError(st, "perturbation_bounds")
+    return float(eta[0]), float(eta[1])
 
 
 def decode_all(A: GseCsr, level: int) -> np.ndarray:

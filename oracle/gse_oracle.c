@@ -566,6 +566,44 @@ int orc_apply(const orc_matrix* A, int level, const double* x, double* y) {
 }
 
 /* ------------------------------------------------------------------------------------
+ * R29 (build reading; the paper's switching rule is the monitor of P:258-294, whose
+ * defaults never fire before convergence on the BASELINE configs, R17): the level-L
+ * matrix A_L = A_3 - E_L differs from the full-precision one by the truncated tail bits,
+ * so the true residual of ANY iterate satisfies
+ *   ||b - A_3 x|| <= ||b - A_L x|| + ||E_L|| ||x||,
+ * and once the level-L residual falls below ~||E_L|| ||x|| / ||b|| further level-L
+ * iterations cannot lower the true residual (the attainable-accuracy floor of level L).
+ * eta_L = ||E_L||_inf = max_i sum_j |dec_3(a_ij) - dec_L(a_ij)| (a bound on ||E_L||_2 for
+ * symmetric E_L; a heuristic scale otherwise), row sums in storage order.
+ * ------------------------------------------------------------------------------------ */
+int orc_perturbation_bounds(const orc_matrix* A, double eta[2]) {
+  eta[0] = eta[1] = 0.0;
+  if (A->val || A->half_kind) return ORC_ERR_INVALID_ARG;
+  const int eb = A->ei_bits;
+  int bad = 0;
+  for (int64_t i = 0; i < A->rows; ++i) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int64_t j = A->row_ptr[i]; j < A->row_ptr[i + 1]; ++j) {
+      uint32_t c = A->col_ei[j];
+      int ei = A->ei_in_column ? (eb ? (int)(c >> (32 - eb)) : 0) : (int)A->side_ei[j];
+      double v3, v1, v2;
+      bad |= orc_decode(orc_assemble(A->head[j], A->tail1[j], A->tail2[j], 3), ei, A->table,
+                        A->table_len, &v3) != ORC_OK;
+      bad |= orc_decode(orc_assemble(A->head[j], A->tail1[j], A->tail2[j], 1), ei, A->table,
+                        A->table_len, &v1) != ORC_OK;
+      bad |= orc_decode(orc_assemble(A->head[j], A->tail1[j], A->tail2[j], 2), ei, A->table,
+                        A->table_len, &v2) != ORC_OK;
+      double e1 = fabs(v3 - v1), e2 = fabs(v3 - v2);
+      s1 = s1 + e1;
+      s2 = s2 + e2;
+    }
+    if (s1 > eta[0]) eta[0] = s1;
+    if (s2 > eta[1]) eta[1] = s2;
+  }
+  return bad ? ORC_ERR_INVALID_EXP_INDEX : ORC_OK;
+}
+
+/* ------------------------------------------------------------------------------------
  * c.1 step 9 -- residual monitor, window w[0..t] = resid[j-t .. j] (oldest first).
  * Eq. 3: RSD = sqrt((1/t) sum_{i=j-t}^{j-1} (resid[i]-avg)^2) / avg, avg over
  *   the same t values; 0 if avg < 1e-300.
@@ -658,10 +696,18 @@ static void ring_window(const ring_t* r, double* w) {
 /* check point rule: j >= l, (j - l) mod m == 0, window full; returns 1 to
  * escalate.  Level floors (R17) are an optional build heuristic, default off. */
 static int monitor_check(const orc_schedule* s, const ring_t* ring, double* wbuf, int64_t j,
-                         int level, double resid) {
+                         int level, double resid, const double* eta, double xx, double bnorm) {
   if (!s->enabled || level >= s->max_level) return 0;
   if (level <= 2 && s->level_floor[level - 1] > 0.0 && resid < s->level_floor[level - 1])
     return 1;
+  /* R29: the level's attainable-accuracy floor, with x the iterate before this iteration's
+   * update (CG) or at the start of the cycle (GMRES) */
+  if (level <= 2 && s->perturb_c > 0.0 && xx > 0.0) {
+    double thr = s->perturb_c * eta[level - 1];
+    thr = thr * sqrt(xx);
+    thr = thr / bnorm;
+    if (resid <= thr) return 1;
+  }
   if (j < s->l || ((j - s->l) % s->m) != 0 || ring->count < s->t + 1) return 0;
   ring_window(ring, wbuf);
   return orc_should_escalate(wbuf, s->t, s->rsd_limit, s->ndec_limit, s->reldec_limit);
@@ -669,6 +715,7 @@ static int monitor_check(const orc_schedule* s, const ring_t* ring, double* wbuf
 
 static int validate_sched(const orc_schedule* s) {
   if (s->start_level < 1 || s->start_level > 3) return 0;
+  if (!(s->perturb_c >= 0.0)) return 0;
   if (s->enabled) {
     if (s->max_level < s->start_level || s->max_level > 3) return 0;
     if (s->t < 1 || s->m < 1) return 0;
@@ -717,6 +764,8 @@ int orc_cg(const orc_matrix* A, const double* b, double* x, double tol, int64_t 
   ring.buf = (double*)malloc((size_t)(ring.cap ? ring.cap : 1) * sizeof(double));
   double* wbuf = (double*)malloc((size_t)(ring.cap ? ring.cap : 1) * sizeof(double));
   int status = ORC_NOT_CONVERGED;
+  double eta[2] = {0.0, 0.0};
+  if (stepped && sched->perturb_c > 0.0) orc_perturbation_bounds(A, eta);
 
   double bnorm = sqrt(vdot(n, b, b));
   if (bnorm == 0.0) { /* b = 0 -> x = 0 is exact */
@@ -753,6 +802,7 @@ int orc_cg(const orc_matrix* A, const double* b, double* x, double tol, int64_t 
     rep->iters_per_level[level - 1]++;
     double pq = vdot(n, p, q);
     if (!(pq > 0.0) || !isfinite(pq)) { status = ORC_NUMERICAL_ABORT; break; }
+    double xx = (stepped && sched->perturb_c > 0.0) ? vdot(n, x, x) : 0.0; /* R29: x_{j-1} */
     double alpha = rr / pq;
     for (int64_t i = 0; i < n; ++i) { double t2 = alpha * p[i]; x[i] = x[i] + t2; }
     for (int64_t i = 0; i < n; ++i) { double t2 = alpha * q[i]; r[i] = r[i] - t2; }
@@ -766,7 +816,7 @@ int orc_cg(const orc_matrix* A, const double* b, double* x, double tol, int64_t 
       if (!(stepped && level < 3 && sched->verify_at_full)) { status = ORC_OK; break; }
       if (true_resid(A, 3, b, x, q, bnorm, rep) <= tol) { status = ORC_OK; break; }
       escalate = 1; /* R16: converged at A_L but not at A -> one level up */
-    } else if (stepped && monitor_check(sched, &ring, wbuf, j, level, resid)) {
+    } else if (stepped && monitor_check(sched, &ring, wbuf, j, level, resid, eta, xx, bnorm)) {
       escalate = 1;
     }
     if (escalate) {
@@ -846,6 +896,8 @@ int orc_gmres(const orc_matrix* A, const double* b, double* x, double tol, int r
   double* wbuf = (double*)malloc((size_t)(ring.cap ? ring.cap : 1) * sizeof(double));
   int status = ORC_NOT_CONVERGED;
   int64_t jg = 0;
+  double eta[2] = {0.0, 0.0};
+  if (stepped && sched->perturb_c > 0.0) orc_perturbation_bounds(A, eta);
 
   double bnorm = sqrt(vdot(n, b, b));
   if (bnorm == 0.0) {
@@ -874,6 +926,7 @@ int orc_gmres(const orc_matrix* A, const double* b, double* x, double tol, int r
       break;
     }
     if (jg >= max_iters) { status = ORC_NOT_CONVERGED; break; }
+    double xx = (stepped && sched->perturb_c > 0.0) ? vdot(n, x, x) : 0.0; /* R29: cycle start */
     for (int64_t i = 0; i < n; ++i) V[i] = w[i] / beta;
     if (sched->krylov_gse16) compress16(n, V); /* NEXT-4 (R28) */
     for (int i = 0; i <= m; ++i) g[i] = 0.0;
@@ -918,7 +971,10 @@ int orc_gmres(const orc_matrix* A, const double* b, double* x, double tol, int r
       if (!isfinite(resid)) { status = ORC_NUMERICAL_ABORT; break; }
       if (stepped) ring_push(&ring, resid);
       if (resid <= tol || hn == 0.0) break; /* converged estimate / happy breakdown */
-      if (stepped && monitor_check(sched, &ring, wbuf, jg, level, resid)) { escalate = 1; break; }
+      if (stepped && monitor_check(sched, &ring, wbuf, jg, level, resid, eta, xx, bnorm)) {
+        escalate = 1;
+        break;
+      }
       if (jg >= max_iters) break;
       double* vn = V + (size_t)(jj + 1) * (size_t)n;
       for (int64_t q = 0; q < n; ++q) vn[q] = w[q] / hn;

@@ -108,6 +108,7 @@ typedef struct {
   int verify_at_full;
   double level_floor[2];
   int krylov_gse16; /* GMRES: Krylov basis stored as 16-bit GSE-SEM vectors (NEXT-4, R28) */
+  double perturb_c; /* R29: escalate at L < 3 when resid <= c * eta_L * ||x|| / ||b||; 0 = off */
 } orc_schedule;
 
 typedef struct {
@@ -120,6 +121,10 @@ typedef struct {
 } orc_report;
 
 void orc_default_schedule(int solver, orc_schedule* s);
+
+/* R29: eta[L-1] = max_i sum_j |dec_3(a_ij) - dec_L(a_ij)| (= ||A_3 - A_L||_inf) for
+ * L = 1, 2; row sums in storage order.  GSE matrices only. */
+int orc_perturbation_bounds(const orc_matrix* A, double eta[2]);
 
 /* ---- solvers ---- */
 int orc_cg(const orc_matrix* A, const double* b, double* x, double tol, int64_t max_iters,

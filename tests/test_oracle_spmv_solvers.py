@@ -318,3 +318,155 @@ def test_level_floors(solver):
     _, rf = run(G, b, tol=1e-10, sched=O.schedule(solver, level_floor=(1e-3, 1e-8)))
     assert rf.converged and rf.n_switches == 2 and rf.rel_residual_true <= 1e-10
     assert rf.switch_iter[0] < r0.switch_iter[0]  # before the head-only solve "converges"
+
+
+# ------------------------------------------------------------------ R29 perturbation trigger
+def _two_bit_rows_matrix(seed=4):
+    """rows holding a_i values +-(1 + 2^-20) and b_i values +-(1 + 2^-40): with the table
+    {1024} (d = 1) the head keeps 15 fraction bits and tail1 16 more, so per value
+    |dec_3 - dec_1| = 2^-20 (first kind) or 2^-40 (second), |dec_3 - dec_2| = 0 or 2^-40."""
+    rng = np.random.default_rng(seed)
+    rows = 40
+    a = rng.integers(0, 9, rows)
+    bb = rng.integers(0, 9, rows)
+    lens = a + bb
+    rp = np.zeros(rows + 1, np.int64)
+    np.cumsum(lens, out=rp[1:])
+    cols, vals = [], []
+    for i in range(rows):
+        c = np.sort(rng.choice(60, lens[i], replace=False))
+        v = np.concatenate([np.full(a[i], 1 + 2.0 ** -20), np.full(bb[i], 1 + 2.0 ** -40)])
+        v = rng.permutation(v) * rng.choice([-1.0, 1.0], lens[i])
+        cols.append(c)
+        vals.append(v)
+    A = gi.Csr(rows, 60, rp, np.concatenate(cols).astype(np.int32), np.concatenate(vals))
+    return A, a, bb
+
+
+def test_perturbation_bounds_closed_form():
+    """R29 eta_L = max_i sum_j |dec_3 - dec_L|: closed form on a matrix whose truncation
+    errors are known exactly per value; 0 on the head-exact Poisson stencil."""
+    A, a, bb = _two_bit_rows_matrix()
+    G = enc(A)
+    assert list(G.table) == [1024]
+    e1, e2 = O.perturbation_bounds(G)
+    assert e1 == max(a * 2.0 ** -20 + bb * 2.0 ** -40)
+    assert e2 == max(bb * 2.0 ** -40)
+    assert O.perturbation_bounds(enc(gi.poisson3d(6))) == (0.0, 0.0)
+
+
+def test_perturbation_bound_is_the_row_sum_of_the_level_gap():
+    """eta_L >= |(A_3 - A_L) s|_inf for every sign vector s (with equality for the row's own
+    signs), checked with the decoded values (dense) on a lossy matrix"""
+    A = gi.poisson2d(12, "varcoef")
+    G = enc(A)
+    eta = O.perturbation_bounds(G)
+    d3 = gi.Csr(A.rows, A.cols, A.row_ptr, A.col, O.decode_all(G, 3)).dense()
+    for L in (1, 2):
+        dL = gi.Csr(A.rows, A.cols, A.row_ptr, A.col, O.decode_all(G, L)).dense()
+        E = d3 - dL
+        assert np.all(E * np.sign(d3) >= 0)  # truncation toward zero
+        assert abs(np.abs(E).sum(axis=1).max() - eta[L - 1]) <= 1e-15 * eta[L - 1]
+        assert eta[L - 1] > 0
+
+
+@pytest.mark.parametrize("solver", ["cg", "gmres"])
+def test_perturbation_trigger_behaviour(solver):
+    """R29: c = 0 is the default solve; a huge c escalates at the first check where ||x|| > 0
+    (CG: iteration 2, then 3; GMRES: the first inner step of the second cycle, then the
+    next); c = 0.1 switches before the head-only solve 'converges' and still reaches 1e-10"""
+    A = gi.poisson3d(12, "varcoef") if solver == "cg" else gi.convdiff3d(10)
+    b = gi.ones_rhs(A)
+    G = enc(A)
+    run = O.cg if solver == "cg" else O.gmres
+    _, r0 = run(G, b, tol=1e-10, sched=O.schedule(solver))
+    _, rz = run(G, b, tol=1e-10, sched=O.schedule(solver, perturb_c=0.0))
+    assert (rz.iterations, rz.switch_iter) == (r0.iterations, r0.switch_iter)
+    _, rb = run(G, b, tol=1e-10, sched=O.schedule(solver, perturb_c=1e300))
+    first = 2 if solver == "cg" else 31
+    assert rb.switch_iter == (first, first + 1) and rb.switch_to_level == (2, 3)
+    assert rb.converged and rb.rel_residual_true <= 1e-10
+    _, rc = run(G, b, tol=1e-10, sched=O.schedule(solver, perturb_c=0.1))
+    assert rc.converged and rc.n_switches == 2 and rc.rel_residual_true <= 1e-10
+    assert rc.switch_iter[0] < r0.switch_iter[0]
+    assert rc.iterations < r0.iterations
+
+
+def test_perturbation_trigger_matches_independent_numpy_cg():
+    """The oracle's R29 switch points against a plain numpy CG on the decoded level
+    matrices (scipy CSR products, BLAS dots) with the same rule: escalate when
+    ||r||/||b|| <= c eta_L ||x_{j-1}|| / ||b||, restart r = b - A_new x, p = r."""
+    import scipy.sparse as sp
+    A = gi.poisson3d(10, "varcoef")
+    G = enc(A)
+    b = gi.ones_rhs(A)
+    c, tol = 0.1, 1e-10
+    eta = O.perturbation_bounds(G)
+    mats = {L: sp.csr_matrix((O.decode_all(G, L), A.col, A.row_ptr), shape=(A.rows, A.cols))
+            for L in (1, 2, 3)}
+    nb = np.linalg.norm(b)
+    x = np.zeros(A.rows)
+    L, r = 1, b.copy()
+    p, rr, sw, j = r.copy(), r @ r, [], 0
+    while j < 2000:
+        j += 1
+        q = mats[L] @ p
+        xx = x @ x
+        al = rr / (p @ q)
+        x = x + al * p
+        r = r - al * q
+        rn = r @ r
+        res = np.sqrt(rn) / nb
+        if res <= tol:
+            if L == 3 or np.linalg.norm(b - mats[3] @ x) / nb <= tol:
+                break
+            esc = True
+        else:
+            esc = L < 3 and xx > 0 and res <= c * eta[L - 1] * np.sqrt(xx) / nb
+        if esc:
+            L += 1
+            sw.append(j)
+            r = b - mats[L] @ x
+            p, rr = r.copy(), r @ r
+            continue
+        p = r + (rn / rr) * p
+        rr = rn
+    _, rep = O.cg(G, b, tol=tol, sched=O.schedule("cg", perturb_c=c))
+    assert len(sw) == rep.n_switches == 2
+    assert all(abs(a_ - b_) <= 1 for a_, b_ in zip(sw, rep.switch_iter))
+    assert abs(j - rep.iterations) <= 2
+
+
+# ------------------------------------------------------------------ independent iteration gauges
+@pytest.mark.parametrize("N,gauge", [(16, 46), (32, 93)])
+def test_cg_iteration_gauges(N, gauge):
+    """3D Poisson, b = A 1, tol 1e-10 -> 46 / 93 CG iterations at N = 16 / 32
+    (scratch gauge, unchanged under dot orders); scipy's CG agrees within 1."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+    A = gi.poisson3d(N)
+    b = gi.ones_rhs(A)
+    _, rep = O.cg(f64(A), b, tol=1e-10)
+    assert rep.iterations == gauge
+    its = []
+    S = sp.csr_matrix((A.val, A.col, A.row_ptr), shape=(A.rows, A.cols))
+    spla.cg(S, b, rtol=1e-10, atol=0.0, maxiter=5000, callback=lambda xk: its.append(1))
+    assert abs(len(its) - rep.iterations) <= 1
+
+
+@pytest.mark.parametrize("N,gauge", [(16, 135), (32, 363)])
+def test_gmres30_iteration_gauges(N, gauge):
+    """SURVEY 8(c.3) / S:381-383: conv-diff (beta = 64, 128, 192), b = A 1, GMRES(30) to
+    1e-10 takes 135 / 363 inner iterations at N = 16 / 32 (scipy gauge); scipy's
+    gmres(restart=30) counted here independently agrees within 3."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+    A = gi.convdiff3d(N)
+    b = gi.ones_rhs(A)
+    x, rep = O.gmres(f64(A), b, tol=1e-10, restart=30)
+    assert rep.converged and abs(rep.iterations - gauge) <= 3
+    S = sp.csr_matrix((A.val, A.col, A.row_ptr), shape=(A.rows, A.cols))
+    its = []
+    spla.gmres(S, b, rtol=1e-10, atol=0.0, restart=30, maxiter=1000,
+               callback=lambda pr: its.append(1), callback_type="pr_norm")
+    assert abs(len(its) - rep.iterations) <= 3
