@@ -1,32 +1,38 @@
 #!/usr/bin/env python
 """bench.py -- the driver's benchmark contract for the GSE-SEM hot path on B200.
 
-Workload (BASELINE.json configs[1]): 3D Poisson 7-point 128^3 (n = 2,097,152, nnz =
-14,581,760), b = A*1, x0 = 0.  One STEP = the whole hot path on that input: gse_encode
-(histogram, table, encode into head/tail1/tail2 planes, partition) followed by the stepped
-mixed-precision CG solve to a TRUE relative residual <= 1e-10 (paper-default schedule +
-verify_at_full).  value = solves / s.
+Workload (default, every N): BASELINE.json configs[4], 3D Poisson 7-point 512^3
+(n = 134,217,728, nnz = 937,951,232; 11.3 GB of GSE planes, far larger than the 126 MB L2),
+b = A*1, x0 = 0.  It is the largest single-GPU configuration in BASELINE.json and the
+scaling config.  One STEP = the whole hot path on it: gse_encode (histogram, table,
+encode into head/tail1/tail2 planes, row-walk partition) then the stepped mixed-precision
+CG solve to a TRUE relative residual <= 1e-10 (paper-default schedule + verify_at_full,
+R16).  value = solves / s.  Every timed step must report converged with a true residual
+<= tol, else the bench fails.
 
-N > 1 (torchrun, one process per GPU): the SAME problem is row-partitioned over the N
-GPUs (gse_encode_dist: global table by histogram allreduce, local renumbering; CG with
-NCCL halo exchange + allreduced dots) -> "scaling": "strong".  --workload c5 selects the
-512^3 Poisson of configs[4] (the multi-GPU config).
+N > 1 (torchrun, one process per GPU): the same 512^3 problem is row-partitioned over the
+N GPUs by z-slabs (gse_encode_dist: global table by histogram allreduce, local column
+renumbering; CG with the NCCL halo exchange overlapped with the interior rows and
+allreduced dots) -> "scaling": "strong".
 
-Also reported (N = 1): the SpMV segment sweep on C2 (GB/s, GFLOP/s, fraction of the measured
-HBM peak per segment count, FP64 / FP32 accumulation, FP64-CSR comparator, FP16 / BF16
-storage baselines; cold and back-to-back), the FP64-CSR / FP16 / BF16 CG time-to-1e-10 and
-the paper's GSE-SEM* projection (Eq. 7), the roofline of the dominant kernel, the configs[2]
-power-law SpMV segment sweep (`spmv_sweep_c3`), the configs[3] conv-diff 256^3 GMRES(30)
-times (`gmres_c4`, at 1e-10 and at the paper's 1e-6), the oracle CPU baseline, the
-end-to-end number through the C-ABI with host buffers, SM clocks.  About one minute.
+Also in the line (N = 1, rank 0): the C5 SpMV segment sweep (GB/s, GFLOP/s, fraction of
+the measured HBM peak per segment count, FP64 / FP32 accumulation, the CG's fused SpMV+dot
+kernel back to back as in the CG loop, FP64-CSR comparator), the FP64-CSR CG on the same
+GPU, the roofline of the dominant kernel, the end-to-end number through the C-ABI from
+pinned host buffers, the oracle CPU baseline, SM clocks; and compact sub-objects for
+configs[1] (C2 128^3 const: step, SpMV sweep), C2-shape varcoef stepped CG (where the
+solver switches levels), configs[2] (power-law 10M rows SpMV segment sweep) and configs[3]
+(conv-diff 256^3 GMRES(30)).  `--quick` skips the sub-objects.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gse|reference]
+                  [--workload c5|c2] [--quick]
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -40,6 +46,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = ("GSE SpMV GB/s & GFLOP/s (frac of HBM peak) per segment count; "
           "CG time-to-1e-10")
+WORKLOADS = {"c5": (512, "configs[4]"), "c2": (128, "configs[1]")}
+TOL = 1e-10
+R29_C = 0.1  # the R29 trigger constant of the stepped_r29 sub-results (R29)
 
 
 def unit_for(N):
@@ -52,18 +61,15 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gse", choices=["gse", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c2", "c5"])
+    ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
     ap.add_argument("--variant", default="const", choices=["const", "varcoef"])
-    ap.add_argument("--spmv-reps", type=int, default=20)
+    ap.add_argument("--quick", action="store_true",
+                    help="skip the configs[1]/[2]/[3] sub-objects")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
-    ap.add_argument("--no-c3", action="store_true",
-                    help="skip the configs[2] power-law SpMV segment sweep")
-    ap.add_argument("--cpu-iters", type=int, default=40,
-                    help="oracle CG iterations in the bounded CPU sample")
     a = ap.parse_args()
-    a.N = 128 if a.workload == "c2" else 512
+    a.N, a.cfg = WORKLOADS[a.workload]
     return a
 
 
@@ -73,6 +79,13 @@ def peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def r3(v):
+    """3 significant digits (keeps the JSON line short enough for the driver's tail)"""
+    if v is None or not isinstance(v, float) or v == 0 or not np.isfinite(v):
+        return v
+    return float(f"{v:.3g}") if abs(v) < 1000 else round(v, 1) if abs(v) < 1e5 else round(v)
 
 
 # ------------------------------------------------------------------ clocks sampler
@@ -168,84 +181,206 @@ def barrier(pg):
         pg.barrier()
 
 
-def partition(n, P):
-    return [round(i * n / P) for i in range(P + 1)]
+def slab_partition(N, P):
+    """z-slab row partition: rank i owns planes [round(iN/P), round((i+1)N/P))"""
+    return [round(i * N / P) * N * N for i in range(P + 1)]
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
 
 
 def _config(args, n, nnz, world):
-    return {"workload": f"3D Poisson 7-point {args.N}^3 ({args.variant}) stepped GSE CG to 1e-10 "
-                        f"({'configs[1]' if args.workload == 'c2' else 'configs[4]'})",
-            "n": int(n), "nnz": int(nnz), "k_max": 8, "tol": 1e-10,
-            "schedule": "paper default CG (l=3000,t=250,m=500) + verify_at_full",
-            "step": "gse_encode + gse_solve_cg (inputs resident in HBM)",
-            "l2": "flushed before every timed step (256 MiB write, then a read pass over it so no "
-                  "dirty lines are written back inside the timed region); per-step CUDA events",
-            "parallelism": (f"row-partitioned x{world} (NCCL halo + allreduce)" if world > 1
-                            else "single GPU")}
+    return {"workload": f"{args.cfg} 3D Poisson 7-point {args.N}^3 ({args.variant}): gse_encode + "
+                        f"stepped GSE CG to a true relative residual of 1e-10",
+            "n": int(n), "nnz": int(nnz), "k_max": 8, "tol": TOL,
+            "schedule": "paper default CG (l=3000,t=250,m=500) + verify_at_full (R16)",
+            "inputs": "CSR resident in HBM before the timed region",
+            "l2": ("inputs larger than L2 (planes 11.3 GB); L2 also flushed before every timed step"
+                   if args.N >= 256 else "flushed before every timed step (256 MiB write + read)"),
+            "parallelism": (f"row-partitioned x{world} z-slabs (NCCL halo + allreduce)"
+                            if world > 1 else "single GPU")}
+
+
+def l2_flush(buf, i):
+    """Evict L2: write a 256 MiB buffer (2x the 126 MB L2), then read it back once, so the
+    write-backs of the dirty lines happen here and not inside the next timed region."""
+    buf.fill_(float(i))
+    buf.sum()
+
+
+def time_cuda(fn, reps, stream, flush):
+    import torch
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(reps)]
+    for i in range(reps):
+        if flush is not None:
+            l2_flush(flush, i)
+        evs[i][0].record(stream)
+        fn()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    return [s.elapsed_time(e) for s, e in evs]
+
+
+def time_b2b(fn, reps, stream, flush):
+    """mean per call of `reps` back-to-back calls (after one flush), CUDA events"""
+    import torch
+    fn()
+    l2_flush(flush, 0)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+# ------------------------------------------------------------------ inputs on the device
+def device_poisson(args, r0, r1, dev, keep_host=False):
+    """rows [r0, r1) of the Poisson matrix (gse_inputs recipe, generated in chunks by a
+    thread pool) -> device CSR (row_ptr int32 local, col int32, val f64) and b = A*1."""
+    import torch
+    import gse_inputs as gi
+    rps, cols, vals, bs = [], [], [], []
+    base = 0
+    for _, A in gi.poisson3d_chunks(args.N, args.variant, r0, r1):
+        rps.append(torch.from_numpy((A.row_ptr[:-1] + base).astype(np.int32)).to(dev))
+        cols.append(torch.from_numpy(A.col).to(dev))
+        vals.append(torch.from_numpy(A.val).to(dev))
+        bs.append(torch.from_numpy(gi.ones_rhs(A)).to(dev))
+        base += A.nnz
+    rp = torch.cat(rps + [torch.tensor([base], dtype=torch.int32, device=dev)])
+    del rps
+    col, val, b = torch.cat(cols), torch.cat(vals), torch.cat(bs)
+    return rp, col, val, b
 
 
 # ------------------------------------------------------------------ reference arm (oracle)
-def oracle_sample(A, b, iters: int):
-    """Bounded oracle sample: oracle encode of the full matrix + `iters` CG iterations at
-    level 1 (the level the stepped solve runs at on this workload).  Returns seconds."""
-    import oracle as O
-    t0 = time.perf_counter()
-    R = O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
-    t1 = time.perf_counter()
+def oracle_iters(O, R, b, iters):
+    """`iters` level-1 CG iterations of the oracle (the level the stepped solve runs at on
+    this head-exact workload); returns seconds per iteration"""
     s = O.schedule("cg", verify_at_full=0)
+    t0 = time.perf_counter()
     _, rep = O.cg(R, b, tol=1e-300, max_iters=iters, sched=s)
-    t2 = time.perf_counter()
-    return t1 - t0, (t2 - t1) / max(rep.iterations, 1)
+    return (time.perf_counter() - t0) / max(rep.iterations, 1)
 
 
-def full_iterations(A, b):
-    # plain oracle CG count when cheap; else the 2.85 N rule measured for 3D Poisson
-    # (SURVEY 8(d), verified N = 16..64 in the oracle tests)
-    if A.rows <= 64 ** 3:
-        import oracle as O
-        F = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
-        return O.cg(F, b, tol=1e-10)[1].iterations
-    N = round(A.rows ** (1 / 3))
-    return int(round(2.85 * N))
+def oracle_count_c2(O, gi, variant):
+    """The oracle's own iteration count for the workload: the FP64 CG count at 128^3 (a full
+    oracle solve, seconds) scaled linearly with N (3D Poisson CG iterations grow ~ N: 2.85 N
+    measured N = 16..64)."""
+    A = gi.poisson3d(128, variant)
+    F = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+    return O.cg(F, gi.ones_rhs(A), tol=TOL)[1].iterations
+
+
+def host_poisson(args):
+    import gse_inputs as gi
+    parts = list(gi.poisson3d_chunks(args.N, args.variant))
+    nnz = sum(A.nnz for _, A in parts)
+    rp = np.zeros(args.N ** 3 + 1, np.int64)
+    col = np.empty(nnz, np.int32)
+    val = np.empty(nnz, np.float64)
+    b = np.empty(args.N ** 3)
+    o = 0
+    for r0, A in parts:
+        rp[r0:r0 + A.rows] = A.row_ptr[:-1] + o
+        col[o:o + A.nnz] = A.col
+        val[o:o + A.nnz] = A.val
+        b[r0:r0 + A.rows] = gi.ones_rhs(A)
+        o += A.nnz
+    rp[-1] = o
+    return gi.Csr(args.N ** 3, args.N ** 3, rp, col, val, "poisson"), b
 
 
 def run_reference(args, world, rank, pg):
+    """The oracle (plain C, OpenMP rows) on the host cores of rank 0 (other ranks exit).
+    Step = a bounded sample of the workload: k level-1 oracle CG iterations.  value = 1 /
+    (oracle encode + t_iteration x the oracle's iteration count for the workload);
+    ms_per_step = the measured sample time per step (what the timed region really ran)."""
     if rank != 0:
         return
     import gse_inputs as gi
     import oracle as O
     # all host cores (torchrun exports OMP_NUM_THREADS=1 to every rank; only rank 0 runs here)
     cores = O.set_threads(len(os.sched_getaffinity(0)))
-    A = gi.poisson3d(args.N, args.variant)
-    b = gi.ones_rhs(A)
-    iters_full = full_iterations(A, b)
-    k = max(4, args.cpu_iters // 4)
+    t0 = time.perf_counter()
+    if args.N == 128:
+        A = gi.poisson3d(128, args.variant)
+        b = gi.ones_rhs(A)
+    else:
+        A, b = host_poisson(args)
+    t_gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    R = O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+    t_enc = time.perf_counter() - t0
+    n128 = oracle_count_c2(O, gi, args.variant)
+    iters_full = int(round(n128 * args.N / 128))
+    t1 = oracle_iters(O, R, b, 1 if args.N > 256 else 8)
     times = []
-    for i in range(args.warmup + args.steps):
-        te, ti = oracle_sample(A, b, k)
-        if i >= args.warmup:
-            times.append(te + ti * iters_full)
-    t = statistics.mean(times)
-    value = 1.0 / t
+    if t_enc + t1 * iters_full < 30.0:
+        # a full oracle solve costs seconds: each step IS the workload (oracle encode +
+        # stepped CG to a true relative residual of 1e-10), nothing extrapolated
+        its = []
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            Ri = O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+            _, rep = O.cg(Ri, b, tol=TOL, sched=O.schedule("cg"))
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+                its.append(rep.iterations)
+        value = 1.0 / statistics.mean(times)
+        sample = (f"each step a full oracle solve: encode + stepped CG (paper defaults) to a true "
+                  f"relative residual of 1e-10 ({its[-1]} iterations)")
+    else:
+        # iterations per step: the whole (W + K)-step run takes ~2 minutes of CG work
+        k = max(1, min(50, int(120.0 / max(t1, 1e-6) / (args.warmup + args.steps))))
+        per_it = []
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            ti = oracle_iters(O, R, b, k)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+                per_it.append(ti)
+        t_it = statistics.mean(per_it)
+        value = 1.0 / (t_enc + t_it * iters_full)
+        sample = (f"per step {k} level-1 oracle CG iterations ({t_it * 1e3:.0f} ms each; "
+                  f"{k * args.steps} timed in all); value = 1 / (oracle encode {t_enc:.1f} s + "
+                  f"{iters_full} iterations), {iters_full} = the oracle's FP64 CG count at 128^3 "
+                  f"({n128}) x N/128")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": unit_for(args.N),
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": statistics.mean(times) * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {**_config(args, A.rows, A.nnz, world),
+            "config": {**_config(args, A.rows, A.nnz, world), "inputs": "host memory",
                        "parallelism": f"the plain CPU oracle on rank 0's host cores ({cores} threads)"},
             "cpu_baseline": {"value": value, "unit": unit_for(args.N), "cores": cores,
-                             "kind": "oracle",
-                             "sample": f"oracle encode + {k} CG iterations per step, extrapolated "
-                                       f"to {iters_full} iterations"},
+                             "kind": "oracle", "cpu": cpu_model(), "sample": sample,
+                             "generate_s": round(t_gen, 1)},
             "e2e": {"value": value, "unit": unit_for(args.N), "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ GSE arm
+def check_rep(rep, where):
+    if not (rep["converged"] and rep["rel_residual_true"] <= TOL * (1 + 1e-12)):
+        raise SystemExit(f"bench: {where} did not converge to {TOL}: {rep}")
+
+
 def run_gse(args, world, rank, local, pg):
     import torch
-    import gse_inputs as gi
     import paper_2411_04686_b200 as g
 
     torch.cuda.set_device(local)
@@ -253,17 +388,12 @@ def run_gse(args, world, rank, local, pg):
     stream = torch.cuda.current_stream(dev)
     hbm_peak, peak_src = peaks()
     n_glob = args.N ** 3
-    rr = partition(n_glob, world)
-    r0, r1 = rr[rank], rr[rank + 1]
-    A = gi.poisson3d(args.N, args.variant, row_begin=r0, row_end=r1)  # this rank's rows
     nnz_glob = 7 * args.N ** 3 - 6 * args.N ** 2
-    # b = A 1 on the rank's rows (row sums: input recipe)
-    b_h = gi.ones_rhs(A)
-    rp = torch.from_numpy(A.row_ptr.astype(np.int32)).to(dev)
-    col = torch.from_numpy(A.col).to(dev)
-    val = torch.from_numpy(A.val).to(dev)
-    b = torch.from_numpy(b_h).to(dev)
-    x = torch.zeros(A.rows, dtype=torch.float64, device=dev)
+    part = slab_partition(args.N, world)
+    r0, r1 = part[rank], part[rank + 1]
+    rp, col, val, b = device_poisson(args, r0, r1, dev)
+    n_loc = r1 - r0
+    x = torch.zeros(n_loc, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     sched = g.gse_default_schedule("cg")
 
@@ -278,18 +408,18 @@ def run_gse(args, world, rank, local, pg):
 
     def encode(rp_, col_, val_, **kw):
         if D is None:
-            return g.gse_encode(rp_, col_, val_, A.rows, A.cols, k_max=8, **kw)
+            return g.gse_encode(rp_, col_, val_, n_loc, n_glob, k_max=8, **kw)
         return g.gse_encode_dist(D, rp_, col_, val_, r0, n_glob, **kw)
 
     def step():
         M = encode(rp, col, val)
         x.zero_()
-        _, rep = g.gse_solve_cg(M, b, x, tol=1e-10, max_iters=20000, sched=sched)
+        _, rep = g.gse_solve_cg(M, b, x, tol=TOL, max_iters=20000, sched=sched)
         M.close()
         return rep
 
     for _ in range(args.warmup):
-        rep = step()
+        check_rep(step(), "warm-up step")
     torch.cuda.synchronize()
     barrier(pg)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -305,369 +435,401 @@ def run_gse(args, world, rank, local, pg):
             ev[i][1].record(stream)
         torch.cuda.synchronize()
     clocks = clk.summary()
+    for i, rep in enumerate(reps):  # every timed solve must have converged (true residual)
+        check_rep(rep, f"timed step {i}")
     step_ms = [s.elapsed_time(e) for s, e in ev]
     total_ms = max_over_ranks(sum(step_ms), pg, dev)
     barrier(pg)
     rep = reps[-1]
     value = args.steps / (total_ms * 1e-3)  # one (row-partitioned) problem per step
 
+    line = {
+        "metric": METRIC, "value": value, "unit": unit_for(args.N), "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (gse_inputs recipe, DESIGN.md 4)",
+        "config": _config(args, n_glob, nnz_glob, world)}
+    sub = {}
+    if world == 1 and rank == 0 and not args.quick and not args.no_sweep:
+        # the configs[1..3] sub-objects first (their GPU memory is freed before the C5 work)
+        sub = sub_workloads(dev, stream, flush, hbm_peak)
     extra = None
     if world == 1 and not args.no_sweep:
-        extra = spmv_and_cg_sweep(args, A, rp, col, val, b, dev, stream, flush, hbm_peak)
-    e2e = None if args.no_e2e else e2e_measure(args, A, b_h, dev, stream, encode, r0, n_glob)
+        extra = main_sweep(args, rp, col, val, b, n_loc, dev, stream, flush, hbm_peak)
+    e2e = None if args.no_e2e else e2e_measure(args, rp, col, val, b, dev, stream, encode)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, A, b_h, rep["iterations"])
+        del flush
+        cpu = cpu_baseline(args, rp, col, val, b, rep["iterations"])
     launches = estimate_launches(rep, world) * args.steps
     if D is not None:
         barrier(pg)
         D.close()
     if rank != 0:
         return
-    line = {
-        "metric": METRIC, "value": value, "unit": unit_for(args.N), "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": _config(args, n_glob, nnz_glob, world),
-        "solve": {"iterations": rep["iterations"], "iters_per_level": rep["iters_per_level"],
-                  "switch_iter": rep["switch_iter"],
-                  "rel_residual_true": rep["rel_residual_true"]},
-        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
-        "step_ms_each": [round(t, 3) for t in step_ms],
-    }
+    line.update(sub)
+    line["solve"] = {"iterations": rep["iterations"], "iters_per_level": rep["iters_per_level"],
+                     "switch_iter": rep["switch_iter"],
+                     "rel_residual_true": r3(rep["rel_residual_true"]),
+                     "step_ms_each": [round(t, 1) for t in step_ms]}
     if extra is not None:
-        dom = extra["spmv"]["L1"]
+        line["solve"]["fp64_csr_iterations"] = extra["cg_fp64_iters"]
         line["time_to_1e-10_ms"] = {
-            "stepped_gse_step": statistics.median(step_ms),
-            "stepped_gse_solve_only": extra["cg_gse_ms"], "encode": extra["encode_ms"],
-            "fp64_csr_cg": extra["cg_fp64_ms"],
-            "speedup_vs_fp64_csr": extra["cg_fp64_ms"] / extra["cg_gse_ms"]}
-        line["time_to_1e-10_ms"]["half_storage_cg"] = extra["cg_half"]
-        # P:534-537 Eq. 7: GSE-SEM* = TIME_FP16 / ITERS_FP16 x ITERS_GSE -- the stepped solve
-        # with the FP16 solver's per-iteration time, i.e. without the decode overhead
-        h16 = extra["cg_half"]["fp16"]
-        if h16["iterations"] > 0:
-            star = h16["ms"] / h16["iterations"] * rep["iterations"]
-            line["time_to_1e-10_ms"]["gse_sem_star_eq7_ms"] = star
-            line["time_to_1e-10_ms"]["gse_sem_star_speedup_vs_fp64_csr"] = extra["cg_fp64_ms"] / star
-        line["solve"]["fp64_iterations"] = extra["cg_fp64_iters"]
+            "stepped_gse_step": r3(statistics.median(step_ms)),
+            "stepped_gse_solve_only": r3(extra["cg_gse_ms"]), "encode": r3(extra["encode_ms"]),
+            "fp64_csr_cg": r3(extra["cg_fp64_ms"]),
+            "speedup_vs_fp64_csr": r3(extra["cg_fp64_ms"] / extra["cg_gse_ms"])}
         line["spmv_sweep"] = extra["spmv"]
-        line["spmv_sweep_steady"] = extra["spmv_steady"]
-        st = extra["spmv_steady"]["L1"]
+        dot = extra["dot_l1"]
         line["roofline"] = {
-            "bound": "hbm", "kernel": "k_spmv_rw<L=1> (level-1 GSE SpMV, row walk; the CG inner kernel)",
-            "achieved": st["GBps"], "peak": hbm_peak, "unit": "GB/s",
-            "frac": st["GBps"] / hbm_peak, "peak_source": peak_src,
-            "traffic": _profiled_traffic(), "algorithmic_bytes_per_launch": dom["bytes"],
-            "avg_launch_us": st["us"],
-            "timing": "CUDA events on the launching stream around back-to-back launches (as in "
-                      "the CG loop: no flush between SpMVs), average per launch",
-            "cold": {"achieved": dom["GBps"], "frac": dom["GBps"] / hbm_peak,
-                     "avg_launch_us": dom["us"],
-                     "timing": "one launch between CUDA events, L2 flushed before it"}}
-    if rank == 0 and world == 1 and not args.no_c3 and not args.no_sweep:
-        line["spmv_sweep_c3"] = c3_sweep(args, dev, stream, flush, hbm_peak)
-        line["gmres_c4"] = c4_gmres(dev, stream, flush)
-    print(json.dumps(line), flush=True)
+            "bound": "hbm", "achieved": r3(dot["GBps"]), "peak": hbm_peak, "unit": "GB/s",
+            "frac": r3(dot["GBps"] / hbm_peak), "traffic": _profiled_traffic(),
+            "kernel": "k_spmv_rw<L=1,DOT> (the CG's fused level-1 SpMV + p.q on C5)",
+            "algorithmic_bytes_per_launch": dot["bytes"], "avg_launch_us": r3(dot["us"]),
+            "peak_source": peak_src,
+            "timing": "gse_spmv_dot back to back (as in the CG loop), CUDA events on the "
+                      "launching stream, mean per launch"}
+    line["e2e"] = e2e
+    line["cpu_baseline"] = cpu
+    line["gpu_launches"] = launches
+    line["clocks"] = clocks
+    print(json.dumps(line, separators=(",", ":")), flush=True)
 
 
 def estimate_launches(rep, world):
-    """Kernels launched per step: encode (rowptr, hist, select, encode, flags, group stats,
-    2 CUB select kernels, fill_desc = 9), CG setup (dot, spmv, residual = 3), per iteration
-    3 (single GPU, graph while-loop body) or 5 (+ pack + events, distributed), verify /
-    final residual (2 each).  The single-GPU graph body holds 8 iterations (GSE_CG_UNROLL):
-    the kernels of the pass that sees the event still launch (and return at once), so each
+    """Kernels launched per step: encode (rowptr, hist, select, encode, flags, compaction,
+    group stats, fill_desc = 9), CG setup (dot, spmv, residual = 3), per iteration 3
+    (single GPU, graph while-loop body) or 5 (+ pack + events, distributed), verify / final
+    residual (2 each).  The single-GPU graph body holds 8 iterations (GSE_CG_UNROLL): the
+    kernels of the pass that sees the event still launch (and return at once), so each
     level's count rounds up to a multiple of 8."""
     if world == 1:
         u = int(os.environ.get("GSE_CG_UNROLL", "8"))
         u = min(max(u, 1), 32)
         its = sum(-(-i // u) * u for i in rep["iters_per_level"] if i > 0)
-        # outside the graph: 9 encode + 3 SpMV + 3 residual kernels (ncu launch list of
-        # scripts/count_launches.py; ncu does not list the conditional body's kernels)
         return 9 + 6 + 2 * rep["n_switches"] + 3 * its
     return 9 + 3 + 5 * rep["iterations"] + 2 * (1 + rep["n_switches"]) + 2
 
 
 def _profiled_traffic():
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full
+    summary (profiles/ncu_summary_c5_*.json), or None"""
     import glob
-    found = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_summary_r*.json")))
-    p = found[-1] if found else ""
-    if p and os.path.exists(p):
+    found = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_summary_c5_r*.json")))
+    if found:
         try:
-            return json.load(open(p)).get("k_spmv_L1", {}).get("dram_bytes_per_launch")
+            return json.load(open(found[-1])).get("k_spmv_dot_L1", {}).get("dram_bytes_per_launch")
         except Exception:
             return None
     return None
 
 
-def l2_flush(buf, i):
-    """Evict L2: write a 256 MiB buffer (2x the 126 MB L2), then read it back once, so the
-    write-backs of the dirty lines happen here and not inside the next timed region."""
-    buf.fill_(float(i))
-    buf.sum()
+def spmv_entry(byt, nnz, us, peak):
+    t = us * 1e-6
+    return {"us": r3(us), "GBps": r3(byt / t / 1e9), "GFLOPs": r3(2 * nnz / t / 1e9),
+            "frac": r3(byt / t / 1e9 / peak)}
 
 
-def time_cuda(fn, reps, stream, flush):
-    import torch
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(reps)]
-    for i in range(reps):
-        l2_flush(flush, i)
-        evs[i][0].record(stream)
-        fn()
-        evs[i][1].record(stream)
-    torch.cuda.synchronize()
-    return [s.elapsed_time(e) for s, e in evs]
-
-
-def spmv_and_cg_sweep(args, A, rp, col, val, b, dev, stream, flush, hbm_peak):
+def main_sweep(args, rp, col, val, b, n, dev, stream, flush, hbm_peak):
+    """C5 (or C2) on one GPU: SpMV per segment count (cold: one launch after an L2 flush),
+    FP32 accumulation, the CG's fused SpMV+dot back to back, FP64-CSR; CG solve-only times."""
     import torch
     import paper_2411_04686_b200 as g
-    n, nnz = A.rows, A.nnz
-    M = g.gse_encode(rp, col, val, A.rows, A.cols)
-    F = g.gse_fp64_matrix(rp, col, val, A.rows, A.cols)
+    nnz = int(col.numel())
+    M = g.gse_encode(rp, col, val, n, n)
     x = torch.rand(n, dtype=torch.float64, device=dev)
     y = torch.empty(n, dtype=torch.float64, device=dev)
     x32, y32 = x.float(), torch.empty(n, dtype=torch.float32, device=dev)
-    for _ in range(3):
-        g.gse_spmv(M, x, y, segments=1)
+    dd = torch.empty(1, dtype=torch.float64, device=dev)
     out = {}
-    rows_bytes = 4 * (n + 1)
+    rows_b = 4 * (n + 1)
+    reps = 5 if n > 2 ** 24 else 20
 
-    def rec(key, fn, byt):
-        fn()  # first launch of the kernel (module load) outside the timing
-        t = statistics.mean(time_cuda(fn, args.spmv_reps, stream, flush)) * 1e-3
-        out[key] = {"bytes": byt, "us": t * 1e6, "GBps": byt / t / 1e9,
-                    "GFLOPs": 2 * nnz / t / 1e9, "frac_hbm": byt / t / 1e9 / hbm_peak}
-
-    for L, s_l in ((1, 2), (2, 4), (3, 8)):
-        rec(f"L{L}", lambda: g.gse_spmv(M, x, y, segments=L), nnz * (4 + s_l) + rows_bytes + 16 * n)
-    for L, s_l in ((1, 2), (2, 4), (3, 8)):
-        rec(f"L{L}_f32acc", lambda: g.gse_spmv_f32acc(M, x32, y32, segments=L),
-            nnz * (4 + s_l) + rows_bytes + 8 * n)
-    rec("fp64_csr", lambda: g.gse_spmv(F, x, y, segments=3), nnz * 12 + rows_bytes + 16 * n)
-    # the paper's 16-bit storage baselines (P:406): FP16 / BF16 values, FP64 products and sums
-    H = {k: g.gse_half_matrix(rp, col, val, A.rows, A.cols, kind=k) for k in ("fp16", "bf16")}
-    for k, Hm in H.items():
-        rec(k, lambda: g.gse_spmv(Hm, x, y, segments=3), nnz * 6 + rows_bytes + 16 * n)
-    # steady state, as inside the CG loop: back-to-back launches, no flush in between
-    steady = {}
-    for L in (1, 2, 3):
-        fn = lambda: g.gse_spmv(M, x, y, segments=L)
+    def cold(fn):
         fn()
-        l2_flush(flush, 0)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        reps = 4 * args.spmv_reps
-        e0.record(stream)
-        for _ in range(reps):
-            fn()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        t = e0.elapsed_time(e1) * 1e-3 / reps
-        byt = out[f"L{L}"]["bytes"]
-        steady[f"L{L}"] = {"us": t * 1e6, "GBps": byt / t / 1e9, "frac_hbm": byt / t / 1e9 / hbm_peak}
-    # CG solve only (no encode), stepped GSE vs FP64-CSR
+        return statistics.mean(time_cuda(fn, reps, stream, flush))
+
+    for L, s_l in ((1, 2), (2, 4), (3, 8)):
+        byt = nnz * (4 + s_l) + rows_b + 16 * n
+        out[f"L{L}"] = spmv_entry(byt, nnz, 1e3 * cold(lambda: g.gse_spmv(M, x, y, segments=L)), hbm_peak)
+    for L, s_l in ((1, 2), (2, 4), (3, 8)):
+        byt = nnz * (4 + s_l) + rows_b + 8 * n
+        out[f"L{L}_f32acc"] = spmv_entry(
+            byt, nnz, 1e3 * cold(lambda: g.gse_spmv_f32acc(M, x32, y32, segments=L)), hbm_peak)
+    b1 = nnz * 6 + rows_b + 16 * n
+    us_dot = 1e3 * time_b2b(lambda: g.gse_spmv_dot(M, x, y, segments=1, dot=dd), 4 * reps,
+                            stream, flush)
+    out["L1_dot_cg_loop"] = spmv_entry(b1, nnz, us_dot, hbm_peak)
+    dot = {"bytes": b1, "us": us_dot, "GBps": b1 / (us_dot * 1e-6) / 1e9}
+    del x32, y32
+    F = g.gse_fp64_matrix(rp, col, val, n, n)
+    out["fp64_csr"] = spmv_entry(nnz * 12 + rows_b + 16 * n, nnz,
+                                 1e3 * cold(lambda: g.gse_spmv(F, x, y, segments=3)), hbm_peak)
+    del x, y
     xs = torch.zeros(n, dtype=torch.float64, device=dev)
     sched = g.gse_default_schedule("cg")
 
-    def cg_gse():
+    def solve(A, s):
         xs.zero_()
-        return g.gse_solve_cg(M, b, xs, tol=1e-10, sched=sched)[1]
+        rep = g.gse_solve_cg(A, b, xs, tol=TOL, max_iters=20000, sched=s)[1]
+        check_rep(rep, "sweep solve")
+        return rep
 
-    def cg_f64():
-        xs.zero_()
-        return g.gse_solve_cg(F, b, xs, tol=1e-10)[1]
-
-    cg_gse()
-    cg_f64()
-    t_gse = statistics.median(time_cuda(cg_gse, 3, stream, flush))
-    t_f64 = statistics.median(time_cuda(cg_f64, 3, stream, flush))
-    rf = cg_f64()
-    half_cg = {}
-    for k, Hm in H.items():
-        def cg_h(Hm=Hm):
-            xs.zero_()
-            return g.gse_solve_cg(Hm, b, xs, tol=1e-10)[1]
-        rh = cg_h()
-        half_cg[k] = {"ms": statistics.median(time_cuda(cg_h, 3, stream, flush)),
-                      "iterations": rh["iterations"], "status": rh["status"],
-                      "rel_residual_true_vs_rounded_matrix": rh["rel_residual_true"]}
-        Hm.close()
-
-    def enc():
-        m = g.gse_encode(rp, col, val, A.rows, A.cols)
-        m.close()
-
-    t_enc = statistics.median(time_cuda(enc, 3, stream, flush))
+    solve(M, sched)
+    t_gse = statistics.median(time_cuda(lambda: solve(M, sched), 2, stream, flush))
+    rf = solve(F, None)
+    t_f64 = statistics.median(time_cuda(lambda: solve(F, None), 2, stream, flush))
     M.close()
     F.close()
-    return {"spmv": out, "spmv_steady": steady, "cg_gse_ms": t_gse, "cg_fp64_ms": t_f64,
-            "cg_fp64_iters": rf["iterations"], "encode_ms": t_enc, "cg_half": half_cg}
+
+    def enc():
+        g.gse_encode(rp, col, val, n, n).close()
+
+    t_enc = statistics.median(time_cuda(enc, 3, stream, flush))
+    torch.cuda.empty_cache()
+    return {"spmv": out, "dot_l1": dot, "cg_gse_ms": t_gse, "cg_fp64_ms": t_f64,
+            "cg_fp64_iters": rf["iterations"], "encode_ms": t_enc}
 
 
-def c3_sweep(args, dev, stream, flush, hbm_peak):
-    """configs[2]: the power-law SPD (10M rows, ~200M nnz; recipe in DESIGN.md) SpMV segment
-    sweep -- the strided-products kernel -- per level and accumulation, the FP64-CSR
-    comparator and the FP16 / BF16 baselines.  Cold launches (L2 flushed before each)."""
+# ------------------------------------------------------------------ sub-workloads (N = 1)
+def _dev_csr(A, dev):
+    import torch
+    return (torch.from_numpy(A.row_ptr.astype(np.int32)).to(dev), torch.from_numpy(A.col).to(dev),
+            torch.from_numpy(A.val).to(dev))
+
+
+def _solve_ms(g, stream, flush, solver, M, b, x, sched, tol=TOL):
+    """one warm solve (graphs built), then one timed solve after an L2 flush"""
+    import torch
+    fn = g.gse_solve_cg if solver == "cg" else g.gse_solve_gmres
+    x.zero_()
+    fn(M, b, x, tol=tol, sched=sched)
+    x.zero_()
+    l2_flush(flush, 0)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    rep = fn(M, b, x, tol=tol, sched=sched)[1]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1), rep
+
+
+def sub_workloads(dev, stream, flush, peak):
+    import torch
+    out = {}
+    out["c2"] = sub_c2(dev, stream, flush, peak)
+    torch.cuda.empty_cache()
+    out["c2_varcoef_cg"] = sub_c2_varcoef(dev, stream, flush)
+    torch.cuda.empty_cache()
+    out["c3_spmv"] = sub_c3(dev, stream, flush, peak)
+    torch.cuda.empty_cache()
+    out["c4_gmres"] = sub_c4(dev, stream, flush)
+    torch.cuda.empty_cache()
+    return out
+
+
+def sub_c2(dev, stream, flush, peak):
+    """configs[1] (3D Poisson 128^3 const): step (encode + stepped CG) and SpMV sweep"""
     import torch
     import gse_inputs as gi
     import paper_2411_04686_b200 as g
-    t0 = time.time()
-    A = gi.powerlaw_spd(10_000_000, seed=42)
-    gen_s = time.time() - t0
+    A = gi.poisson3d(128)
+    rp, col, val = _dev_csr(A, dev)
+    b = torch.from_numpy(gi.ones_rhs(A)).to(dev)
     n, nnz = A.rows, A.nnz
-    rp = torch.from_numpy(A.row_ptr.astype(np.int32)).to(dev)
-    col = torch.from_numpy(A.col).to(dev)
-    val = torch.from_numpy(A.val).to(dev)
+    x = torch.zeros(n, dtype=torch.float64, device=dev)
+    sched = g.gse_default_schedule("cg")
+
+    def step():
+        M = g.gse_encode(rp, col, val, n, n)
+        x.zero_()
+        rep = g.gse_solve_cg(M, b, x, tol=TOL, sched=sched)[1]
+        M.close()
+        return rep
+
+    step()
+    t = statistics.median(time_cuda(step, 5, stream, flush))
+    M = g.gse_encode(rp, col, val, n, n)
+    F = g.gse_fp64_matrix(rp, col, val, n, n)
+    t64, r64 = _solve_ms(g, stream, flush, "cg", F, b, x, None)
+    tg, rg = _solve_ms(g, stream, flush, "cg", M, b, x, sched)
+    xv = torch.rand(n, dtype=torch.float64, device=dev)
+    y = torch.empty(n, dtype=torch.float64, device=dev)
+    dd = torch.empty(1, dtype=torch.float64, device=dev)
+    sw = {}
+    for L, s_l in ((1, 2), (2, 4), (3, 8)):
+        byt = nnz * (4 + s_l) + 4 * (n + 1) + 16 * n
+        fn = lambda: g.gse_spmv(M, xv, y, segments=L)
+        fn()
+        sw[f"L{L}"] = spmv_entry(byt, nnz, 1e3 * statistics.mean(time_cuda(fn, 20, stream, flush)), peak)
+    b1 = nnz * 6 + 4 * (n + 1) + 16 * n
+    sw["L1_dot_cg_loop"] = spmv_entry(b1, nnz, 1e3 * time_b2b(
+        lambda: g.gse_spmv_dot(M, xv, y, segments=1, dot=dd), 80, stream, flush), peak)
+    fn = lambda: g.gse_spmv(F, xv, y, segments=3)
+    fn()
+    sw["fp64_csr"] = spmv_entry(nnz * 12 + 4 * (n + 1) + 16 * n, nnz,
+                                1e3 * statistics.mean(time_cuda(fn, 20, stream, flush)), peak)
+    M.close()
+    F.close()
+    return {"solves_per_s": r3(1e3 / t), "step_ms": r3(t), "cg_ms": r3(tg), "iters": rg["iterations"],
+            "fp64_csr_cg_ms": r3(t64), "fp64_iters": r64["iterations"],
+            "speedup_vs_fp64_csr": r3(t64 / tg), "spmv": sw}
+
+
+def sub_c2_varcoef(dev, stream, flush):
+    """C2 shape with varcoef values (head-lossy: the stepped solver switches levels): time
+    to 1e-10 for the paper-default schedule, the level floors (R17), the R29 perturbation
+    trigger and FP64-CSR"""
+    import torch
+    import gse_inputs as gi
+    import paper_2411_04686_b200 as g
+    A = gi.poisson3d(128, "varcoef")
+    rp, col, val = _dev_csr(A, dev)
+    b = torch.from_numpy(gi.ones_rhs(A)).to(dev)
+    n = A.rows
+    x = torch.zeros(n, dtype=torch.float64, device=dev)
+    M = g.gse_encode(rp, col, val, n, n)
+    F = g.gse_fp64_matrix(rp, col, val, n, n)
+    out = {}
+    t64, r64 = _solve_ms(g, stream, flush, "cg", F, b, x, None)
+    out["fp64_csr"] = {"ms": r3(t64), "it": r64["iterations"]}
+    for name, s in (("stepped_default", g.gse_default_schedule("cg")),
+                    ("stepped_floors", g.gse_default_schedule("cg", level_floor=(1e-3, 1e-8))),
+                    ("stepped_r29", g.gse_default_schedule("cg", perturb_c=R29_C))):
+        t, r = _solve_ms(g, stream, flush, "cg", M, b, x, s)
+        out[name] = {"ms": r3(t), "it": r["iterations"], "per_level": r["iters_per_level"],
+                     "res": r3(r["rel_residual_true"]), "x_fp64": r3(t64 / t)}
+    M.close()
+    F.close()
+    return out
+
+
+def sub_c3(dev, stream, flush, peak):
+    """configs[2]: power-law SPD (10M rows, ~200M nnz; DESIGN.md recipe) SpMV segment sweep
+    (window kernel), FP64 and FP32 accumulation, FP64-CSR; cold launches"""
+    import torch
+    import gse_inputs as gi
+    import paper_2411_04686_b200 as g
+    A = gi.powerlaw_spd(10_000_000, seed=42)
+    n, nnz = A.rows, A.nnz
+    rp, col, val = _dev_csr(A, dev)
     del A
     x = torch.from_numpy(gi.uniform_vec(n, seed=7)).to(dev)
     y = torch.empty(n, dtype=torch.float64, device=dev)
     x32, y32 = x.float(), torch.empty(n, dtype=torch.float32, device=dev)
-    out = {"n": n, "nnz": int(nnz), "generate_s": round(gen_s, 1)}
+    out = {"n": n, "nnz": nnz}
 
     def rec(key, fn, byt):
         fn()
-        t = statistics.mean(time_cuda(fn, 10, stream, flush)) * 1e-3
-        out[key] = {"us": round(t * 1e6, 1), "GBps": round(byt / t / 1e9, 1),
-                    "GFLOPs": round(2 * nnz / t / 1e9, 1), "frac_hbm": round(byt / t / 1e9 / hbm_peak, 3)}
+        out[key] = spmv_entry(byt, nnz, 1e3 * statistics.mean(time_cuda(fn, 10, stream, flush)), peak)
 
     M = g.gse_encode(rp, col, val, n, n)
     rows_b = 4 * (n + 1)
     for L, s_l in ((1, 2), (2, 4), (3, 8)):
         rec(f"L{L}", lambda: g.gse_spmv(M, x, y, segments=L), nnz * (4 + s_l) + rows_b + 16 * n)
+    for L, s_l in ((1, 2), (2, 4), (3, 8)):
         rec(f"L{L}_f32acc", lambda: g.gse_spmv_f32acc(M, x32, y32, segments=L),
             nnz * (4 + s_l) + rows_b + 8 * n)
-    out["spmv_mode"] = "strided products" if M.info["spmv_mode"] == 0 else "row walk"
     M.close()
     F = g.gse_fp64_matrix(rp, col, val, n, n)
     rec("fp64_csr", lambda: g.gse_spmv(F, x, y, segments=3), nnz * 12 + rows_b + 16 * n)
     F.close()
-    for k in ("fp16", "bf16"):
-        H = g.gse_half_matrix(rp, col, val, n, n, kind=k)
-        rec(k, lambda: g.gse_spmv(H, x, y, segments=3), nnz * 6 + rows_b + 16 * n)
-        H.close()
-    del rp, col, val
-    torch.cuda.empty_cache()
     return out
 
 
-def c4_gmres(dev, stream, flush):
-    """configs[3]: conv-diff 256^3, restarted GMRES(30) to a true relative residual of 1e-10
-    (one solve per variant, CUDA events, L2 flushed before each): FP64-CSR, stepped GSE with
-    the paper-default schedule, with the R17 level floors, and with the 16-bit Krylov basis
-    (NEXT-4)."""
+def sub_c4(dev, stream, flush):
+    """configs[3]: conv-diff 256^3 restarted GMRES(30) to a true relative residual of 1e-10
+    (and the paper's 1e-6): FP64-CSR vs stepped GSE (paper defaults, level floors, R29)"""
     import torch
     import gse_inputs as gi
     import paper_2411_04686_b200 as g
     A = gi.convdiff3d(256)
     n = A.rows
-    rp = torch.from_numpy(A.row_ptr.astype(np.int32)).to(dev)
-    col = torch.from_numpy(A.col).to(dev)
-    val = torch.from_numpy(A.val).to(dev)
+    rp, col, val = _dev_csr(A, dev)
     b = torch.from_numpy(gi.ones_rhs(A)).to(dev)
     del A
     x = torch.zeros(n, dtype=torch.float64, device=dev)
-    out = {"n": n, "tol": 1e-10, "restart": 30}
-    k16 = g.gse_default_schedule("gmres", level_floor=(1e-3, 1e-8))
-    k16.krylov_gse16 = 1
-    runs = [("fp64_csr", "fp64", None),
-            ("stepped_default", "gse", g.gse_default_schedule("gmres")),
-            ("stepped_floors", "gse", g.gse_default_schedule("gmres", level_floor=(1e-3, 1e-8))),
-            ("stepped_floors_krylov16", "gse", k16)]
-    for name, kind, sched in runs:
-        M = (g.gse_fp64_matrix(rp, col, val, n, n) if kind == "fp64"
-             else g.gse_encode(rp, col, val, n, n))
-        x.zero_()
-        g.gse_solve_gmres(M, b, x, tol=1e-10, sched=sched)  # graphs built outside the timing
-        x.zero_()
-        l2_flush(flush, 0)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        rep = g.gse_solve_gmres(M, b, x, tol=1e-10, sched=sched)[1]
-        e1.record(stream)
-        torch.cuda.synchronize()
-        t = e0.elapsed_time(e1)
-        out[name] = {"ms": round(t, 1), "iterations": rep["iterations"],
-                     "iters_per_level": rep["iters_per_level"],
-                     "rel_residual_true": rep["rel_residual_true"]}
-        M.close()
-    f = out["fp64_csr"]["ms"]
-    for name, _, _ in runs[1:]:
-        out[name]["speedup_vs_fp64_csr"] = round(f / out[name]["ms"], 3)
-    # the paper's own tolerance (P:299: 1e-6): FP64-CSR vs stepped GSE (paper defaults)
-    t6 = {}
-    for name, kind, sched in runs[:2]:
-        M = (g.gse_fp64_matrix(rp, col, val, n, n) if kind == "fp64"
-             else g.gse_encode(rp, col, val, n, n))
-        x.zero_()
-        g.gse_solve_gmres(M, b, x, tol=1e-6, sched=sched)
-        x.zero_()
-        l2_flush(flush, 0)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        rep = g.gse_solve_gmres(M, b, x, tol=1e-6, sched=sched)[1]
-        e1.record(stream)
-        torch.cuda.synchronize()
-        t6[name] = {"ms": round(e0.elapsed_time(e1), 1), "iterations": rep["iterations"],
-                    "iters_per_level": rep["iters_per_level"],
-                    "rel_residual_true": rep["rel_residual_true"]}
-        M.close()
-    t6["stepped_default"]["speedup_vs_fp64_csr"] = round(t6["fp64_csr"]["ms"] /
-                                                         t6["stepped_default"]["ms"], 3)
-    out["tol_1e-6"] = t6
-    del rp, col, val
-    torch.cuda.empty_cache()
+    M = g.gse_encode(rp, col, val, n, n)
+    F = g.gse_fp64_matrix(rp, col, val, n, n)
+    out = {}
+    for tol, tag in ((1e-10, ""), (1e-6, "_tol1e-6")):
+        t64, r64 = _solve_ms(g, stream, flush, "gmres", F, b, x, None, tol)
+        out["fp64_csr" + tag] = {"ms": r3(t64), "it": r64["iterations"]}
+        runs = [("stepped_default", g.gse_default_schedule("gmres"))]
+        if tol == 1e-10:
+            runs.append(("stepped_floors", g.gse_default_schedule("gmres", level_floor=(1e-3, 1e-8))))
+            runs.append(("stepped_r29", g.gse_default_schedule("gmres", perturb_c=R29_C)))
+        for name, s in runs:
+            t, r = _solve_ms(g, stream, flush, "gmres", M, b, x, s, tol)
+            out[name + tag] = {"ms": r3(t), "it": r["iterations"], "per_level": r["iters_per_level"],
+                               "x_fp64": r3(t64 / t)}
+    M.close()
+    F.close()
     return out
 
 
-def e2e_measure(args, A, b_h, dev, stream, encode, r0, n_glob):
-    """Same step through the C-ABI with HOST (pinned) buffers: H2D of the CSR and b inside
-    the calls, D2H of x at the end."""
+# ------------------------------------------------------------------ end to end, CPU baseline
+def e2e_measure(args, rp, col, val, b, dev, stream, encode):
+    """The same step through the C-ABI with HOST (pinned) buffers: H2D of the CSR, b and x0
+    inside the calls, D2H of x at the end (host wall clock around the synchronous calls)."""
     import torch
     import paper_2411_04686_b200 as g
-    rp = torch.from_numpy(A.row_ptr.astype(np.int32)).pin_memory()
-    col = torch.from_numpy(A.col).pin_memory()
-    val = torch.from_numpy(A.val).pin_memory()
-    b = torch.from_numpy(b_h).pin_memory()
-    x = torch.zeros(A.rows, dtype=torch.float64).pin_memory()
+    hp = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t)
+    rp_h, col_h, val_h, b_h = hp(rp), hp(col), hp(val), hp(b)
+    x = torch.zeros(b_h.numel(), dtype=torch.float64).pin_memory()
     sched = g.gse_default_schedule("cg")
     s = stream.cuda_stream
 
     def step():
-        M = encode(rp, col, val, stream=s)
+        M = encode(rp_h, col_h, val_h, stream=s)
         x.zero_()
-        g.gse_solve_cg(M, b, x, tol=1e-10, max_iters=20000, sched=sched, stream=s)
+        rep = g.gse_solve_cg(M, b_h, x, tol=TOL, max_iters=20000, sched=sched, stream=s)[1]
         M.close()
+        check_rep(rep, "e2e step")
 
     step()
     ts = []
-    for _ in range(max(2, args.steps // 2)):
+    for _ in range(2):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         step()
         torch.cuda.synchronize()
         ts.append(time.perf_counter() - t0)
     t = statistics.median(ts)
-    h2d = rp.numel() * 4 + col.numel() * 4 + val.numel() * 8 + b.numel() * 8 + x.numel() * 8
+    h2d = rp_h.numel() * 4 + col_h.numel() * 4 + val_h.numel() * 8 + b_h.numel() * 8 + x.numel() * 8
     return {"value": 1.0 / t, "unit": unit_for(args.N), "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(x.numel() * 8), "ms_per_step": t * 1e3,
+            "d2h_bytes_per_step": int(x.numel() * 8), "ms_per_step": r3(t * 1e3),
             "timer": "host wall clock around the synchronous C-ABI calls (rank 0)"}
 
 
-def cpu_baseline(args, A, b_h, iters_full):
+def cpu_baseline(args, rp, col, val, b, iters_gpu):
+    """The oracle as it stands on the host cores: oracle encode of the whole matrix + a
+    bounded number of level-1 CG iterations (~20 s), extrapolated to the GPU solve's
+    iteration count; plus the single-thread time per iteration."""
+    import torch
+    import gse_inputs as gi
     import oracle as O
+    del torch
+    A = gi.Csr(int(b.numel()), int(b.numel()), rp.cpu().numpy().astype(np.int64),
+               col.cpu().numpy(), val.cpu().numpy())
+    bh = b.cpu().numpy()
     cores = O.set_threads(len(os.sched_getaffinity(0)))
-    # bounded sample (~20 s of CPU work): 2 iterations first, more when they are cheap
-    te, ti = oracle_sample(A, b_h, 2)
-    k = 2
-    if ti * args.cpu_iters < 20.0:
-        k = args.cpu_iters
-        te, ti = oracle_sample(A, b_h, k)
-    t = te + ti * iters_full
+    t0 = time.perf_counter()
+    R = O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+    te = time.perf_counter() - t0
+    t1 = oracle_iters(O, R, bh, 1)
+    k = max(2, min(200, int(20.0 / max(t1, 1e-6))))
+    ti = oracle_iters(O, R, bh, k)
+    O.set_threads(1)
+    t_single = oracle_iters(O, R, bh, 1 if t1 * cores > 2.0 else 3)
+    O.set_threads(cores)
+    t = te + ti * iters_gpu
     return {"value": 1.0 / t, "unit": unit_for(args.N), "cores": cores, "kind": "oracle",
-            "sample": f"oracle encode of the full matrix ({te:.2f} s) + {k} level-1 "
-                      f"CG iterations ({ti * 1e3:.1f} ms each), extrapolated to the GPU run's "
-                      f"{iters_full} iterations; OpenMP rows in SpMV/encode, sequential dots"}
+            "cpu": cpu_model(),
+            "sample": f"oracle encode of the whole matrix ({te:.1f} s) + {k} level-1 CG iterations "
+                      f"({ti * 1e3:.0f} ms each), extrapolated to the GPU solve's {iters_gpu} "
+                      f"iterations; OpenMP rows in SpMV/encode, sequential dots",
+            "single_thread_ms_per_iteration": r3(t_single * 1e3)}
 
 
 def main():

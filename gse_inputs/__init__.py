@@ -149,6 +149,37 @@ def poisson3d(N: int, variant: str = "const", seed: int = 42, row_begin: int = 0
     return _stencil(dims, _OFF3, fn, row_begin, row_end, name=f"poisson3d_{N}_{variant}")
 
 
+def poisson3d_chunks(N: int, variant: str = "const", row_begin: int = 0,
+                     row_end: int | None = None, planes: int = 8, workers: int | None = None):
+    """poisson3d's rows [row_begin, row_end) as consecutive row chunks of <= `planes` x-y
+    planes each, generated by a thread pool and yielded in row order as (r0, Csr): the same
+    matrix, without one 938M-non-zero temporary for C5 (bench.py streams the chunks to the
+    GPU).  Each chunk's row_ptr starts at 0."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    n = N ** 3
+    row_end = n if row_end is None else row_end
+    step = planes * N * N
+    bounds = [(a, min(a + step, row_end)) for a in range(row_begin, row_end, step)]
+    kappa = None if variant == "const" else _kappa(n, 42)
+    dims = (N, N, N)
+    if variant == "const":
+        fn = lambda idx, k, ok: np.full(idx.size, 6.0 if k == 3 else -1.0)
+    else:
+        fn = _varcoef_fn(dims, _OFF3, kappa)
+    work = lambda ab: (ab[0], _stencil(dims, _OFF3, fn, ab[0], ab[1], name=f"poisson3d_{N}_{variant}"))
+    workers = workers or min(16, os.cpu_count() or 1)
+    with ThreadPoolExecutor(workers) as ex:
+        # bounded look-ahead: at most 2 x workers chunks in host memory
+        pending = [ex.submit(work, ab) for ab in bounds[:2 * workers]]
+        nxt = len(pending)
+        while pending:
+            yield pending.pop(0).result()
+            if nxt < len(bounds):
+                pending.append(ex.submit(work, bounds[nxt]))
+                nxt += 1
+
+
 def convdiff3d(N: int, beta=(64.0, 128.0, 192.0), row_begin: int = 0,
                row_end: int | None = None) -> Csr:
     """C4 (N=256): first-order upwind convection-diffusion, per dimension the unscaled

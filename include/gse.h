@@ -180,6 +180,16 @@ gse_status gse_spmv(gse_matrix A, const double* x, double* y, int segments, void
  * GSE_ERR_FP32_RANGE if the table can represent values >= 2^128. */
 gse_status gse_spmv_f32acc(gse_matrix A, const float* x, float* y, int segments, void* stream);
 
+/* y = A_L x and dot = x . y in ONE launch: the fused SpMV + dot kernel the CG iteration runs
+ * (q = A p, p . q).  Single-GPU matrices only (a distributed CG sums
+ * its dots with an allreduce).  x[cols], y[rows] FP64 host or device; dot: ONE double, host
+ * or device.  The dot is the deterministic fixed-order reduction of per-CTA partials, so
+ * repeated calls give bit-identical results.  Uses the matrix's solver workspace: do not
+ * run concurrently with a solve or another gse_spmv_dot on the same matrix.
+ * GSE_ERR_WRONG_FORMAT for a distributed matrix. */
+gse_status gse_spmv_dot(gse_matrix A, const double* x, double* y, int segments, double* dot,
+                        void* stream);
+
 /* ---------------------------------------------------------------------------------------
  * Stepped mixed-precision solvers (P:217-294 [3.4]).
  * ------------------------------------------------------------------------------------- */
@@ -197,6 +207,13 @@ typedef struct {
                                 * significand bits; a table per basis vector; NEXT-4, R28):
                                 * the Arnoldi steps and the solution update read the decoded
                                 * 16-bit values; 0 = FP64 basis (default)                    */
+  double perturb_c;            /* R29 (build reading, single GPU): escalate at L < 3 when the
+                                * monitored residual <= perturb_c * eta_L * ||x|| / ||b||,
+                                * eta_L = ||A_3 - A_L||_inf (gse_perturbation_bounds): the
+                                * residual level below which level-L iterations cannot lower
+                                * the true residual.  x = the iterate before the current CG
+                                * iteration's update / at the start of the GMRES cycle.
+                                * 0 = off (default, the paper's monitor only); must be >= 0 */
 } gse_step_schedule;
 
 typedef struct {
@@ -210,6 +227,12 @@ typedef struct {
   double seconds;                 /* device time of the solve (CUDA events)                 */
   int64_t spmv_count[3];          /* SpMVs issued per level (incl. replacement / verify)    */
 } gse_solve_report;
+
+/* R29: eta[L-1] = ||A_3 - A_L||_inf = max_i sum_j |dec_3(a_ij) - dec_L(a_ij)|, L = 1, 2
+ * (row sums in storage order: bit-identical to the oracle), computed once per matrix and
+ * cached.  eta: two doubles, host memory.  Synchronises the stream.  GSE matrices only
+ * (GSE_ERR_WRONG_FORMAT otherwise). */
+gse_status gse_perturbation_bounds(gse_matrix A, double* eta, void* stream);
 
 /* Paper defaults (P:433, P:441 [4.4.1]): CG l=3000 t=250 m=500 0.50/130/0.45; GMRES
  * l=9000 t=300 m=1500 0.03/80/0.08; enabled, start 1, max 3, verify_at_full 1, floors 0. */

@@ -33,7 +33,7 @@ GSE_KIND_GSE, GSE_KIND_FP64, GSE_KIND_FP16, GSE_KIND_BF16 = 0, 1, 2, 3
 
 ABI_SYMBOLS = (
     "gse_encode", "gse_fp64_matrix", "gse_half_matrix", "gse_matrix_get_info", "gse_matrix_copy_planes",
-    "gse_decode", "gse_spmv", "gse_spmv_f32acc", "gse_default_schedule", "gse_solve_cg",
+    "gse_decode", "gse_spmv", "gse_spmv_f32acc", "gse_spmv_dot", "gse_perturbation_bounds", "gse_default_schedule", "gse_solve_cg",
     "gse_solve_gmres", "gse_matrix_free", "gse_status_string", "gse_last_error_detail",
     "gse_set_allocator", "gse_nccl_unique_id", "gse_dist_create", "gse_encode_dist",
     "gse_dist_free", "gse_dist_thread_group_create", "gse_dist_thread_group_free",
@@ -87,7 +87,8 @@ class StepSchedule(C.Structure):
                 ("l", C.c_int64), ("t", C.c_int64), ("m", C.c_int64),
                 ("rsd_limit", C.c_double), ("ndec_limit", C.c_int64),
                 ("reldec_limit", C.c_double), ("verify_at_full", C.c_int),
-                ("level_floor", C.c_double * 2), ("krylov_gse16", C.c_int)]
+                ("level_floor", C.c_double * 2), ("krylov_gse16", C.c_int),
+                ("perturb_c", C.c_double)]
 
 
 class SolveReport(C.Structure):
@@ -108,6 +109,8 @@ def _declare(L):
     L.gse_decode.argtypes = [vp, i32, vp, vp]
     L.gse_spmv.argtypes = [vp, vp, vp, i32, vp]
     L.gse_spmv_f32acc.argtypes = [vp, vp, vp, i32, vp]
+    L.gse_spmv_dot.argtypes = [vp, vp, vp, i32, vp, vp]
+    L.gse_perturbation_bounds.argtypes = [vp, vp, vp]
     L.gse_default_schedule.argtypes = [i32, C.POINTER(StepSchedule)]
     L.gse_default_schedule.restype = None
     L.gse_solve_cg.argtypes = [vp, vp, vp, dbl, i64, C.POINTER(StepSchedule),
@@ -362,6 +365,19 @@ def gse_spmv(A: Matrix, x, y=None, segments: int = 3, stream=None):
     return y
 
 
+def gse_spmv_dot(A: Matrix, x, y=None, segments: int = 3, dot=None, stream=None):
+    """a7's fused kernel: y = A_L x and x . y in one launch.  `dot` (one float64, host numpy
+    or device tensor) receives the dot; returns (y, dot)."""
+    if y is None:
+        y = _like(x, A.info["rows"], np.float64)
+    if dot is None:
+        dot = _like(x, 1, np.float64)
+    assert _dtype_ok(x, np.float64) and _dtype_ok(y, np.float64) and _dtype_ok(dot, np.float64)
+    _check(_lib.gse_spmv_dot(A.handle, _addr(x), _addr(y), segments, _addr(dot),
+                             _stream(x, y, stream=stream)), "gse_spmv_dot")
+    return y, dot
+
+
 def gse_spmv_f32acc(A: Matrix, x, y=None, segments: int = 3, stream=None):
     """y = A_L x with FP32 accumulation (R20)."""
     if y is None:
@@ -370,6 +386,14 @@ def gse_spmv_f32acc(A: Matrix, x, y=None, segments: int = 3, stream=None):
     _check(_lib.gse_spmv_f32acc(A.handle, _addr(x), _addr(y), segments,
                                 _stream(x, y, stream=stream)), "gse_spmv_f32acc")
     return y
+
+
+def gse_perturbation_bounds(A: Matrix, stream=None) -> tuple:
+    """R29: (eta_1, eta_2), eta_L = ||A_3 - A_L||_inf."""
+    eta = np.zeros(2)
+    _check(_lib.gse_perturbation_bounds(A.handle, eta.ctypes.data,
+                                        _stream(stream=stream)), "gse_perturbation_bounds")
+    return float(eta[0]), float(eta[1])
 
 
 def gse_default_schedule(solver: str = "cg", **overrides) -> StepSchedule:

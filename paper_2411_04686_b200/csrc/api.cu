@@ -2,6 +2,7 @@
 // pointer staging, device selection, error detail, allocator hook.  No arithmetic of the
 // method lives here; every step runs in the kernels of encode.cu / spmv.cu / solvers.cu.
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <string>
 
@@ -265,6 +266,10 @@ static gse_status check_sched(const gse_step_schedule* sc) {
       return GSE_ERR_INVALID_ARG;
     }
   }
+  if (!(sc->perturb_c >= 0.0) || !std::isfinite(sc->perturb_c)) {
+    set_error("perturb_c must be finite and >= 0 (0 = off)");
+    return GSE_ERR_INVALID_ARG;
+  }
   return GSE_OK;
 }
 
@@ -476,6 +481,61 @@ gse_status gse_spmv(gse_matrix A, const double* x, double* y, int segments, void
   return st.finish();
 }
 
+gse_status gse_spmv_dot(gse_matrix A, const double* x, double* y, int segments, double* dot,
+                        void* stream) {
+  if (!A || segments < 1 || segments > 3 || !dot) {
+    set_error("invalid matrix, segments (must be 1, 2 or 3) or NULL dot");
+    return GSE_ERR_INVALID_ARG;
+  }
+  Matrix& M = A->m;
+  if (M.kind != GSE_KIND_GSE && segments != 3) {
+    set_error("an FP64 / FP16 / BF16 CSR matrix is read at full precision only (segments = 3)");
+    return GSE_ERR_WRONG_FORMAT;
+  }
+  if (M.dist) {
+    set_error("gse_spmv_dot is single-GPU (a distributed dot needs the allreduce of a solve)");
+    return GSE_ERR_WRONG_FORMAT;
+  }
+  if (M.rows != M.cols) {
+    set_error("x . y needs a square matrix");
+    return GSE_ERR_DIM_MISMATCH;
+  }
+  if ((M.cols > 0 && !x) || (M.rows > 0 && !y)) {
+    set_error("x or y is NULL");
+    return GSE_ERR_INVALID_ARG;
+  }
+  DeviceGuard g(M.device);
+  cudaStream_t s = (cudaStream_t)stream;
+  Staging st(s);
+  const double* dx = nullptr;
+  double* dy = nullptr;
+  double* dd = nullptr;
+  gse_status rc = st.in(x, (size_t)M.cols, M.device, &dx);
+  if (rc == GSE_OK) rc = st.out(y, (size_t)M.rows, M.device, false, &dy);
+  if (rc == GSE_OK) rc = st.out(dot, 1, M.device, false, &dd);
+  if (rc != GSE_OK) return rc;
+  rc = spmv_dot_ws(M, segments, dx, dy, dd, s);
+  if (rc != GSE_OK) return rc;
+  rc = st.out_done(y, dy, (size_t)M.rows);
+  if (rc == GSE_OK) rc = st.out_done(dot, dd, 1);
+  if (rc != GSE_OK) return rc;
+  return st.finish();
+}
+
+gse_status gse_perturbation_bounds(gse_matrix A, double* eta, void* stream) {
+  if (!A || !eta) {
+    set_error("NULL matrix or eta");
+    return GSE_ERR_INVALID_ARG;
+  }
+  Matrix& M = A->m;
+  DeviceGuard g(M.device);
+  gse_status rc = perturbation_bounds(M, (cudaStream_t)stream);
+  if (rc != GSE_OK) return rc;
+  eta[0] = M.eta[0];
+  eta[1] = M.eta[1];
+  return GSE_OK;
+}
+
 gse_status gse_spmv_f32acc(gse_matrix A, const float* x, float* y, int segments, void* stream) {
   if (!A || segments < 1 || segments > 3) {
     set_error("invalid matrix or segments (must be 1, 2 or 3)");
@@ -539,6 +599,10 @@ static gse_status solve_common(gse_matrix A, const double* b, double* x, double 
   }
   gse_status rc = check_sched(&sc);
   if (rc != GSE_OK) return rc;
+  if (M.dist && sc.enabled && sc.perturb_c > 0.0) {
+    set_error("the R29 perturbation trigger (perturb_c) is single-GPU only");
+    return GSE_ERR_WRONG_FORMAT;
+  }
   gse_solve_report r;
   memset(&r, 0, sizeof(r));
   DeviceGuard g(M.device);

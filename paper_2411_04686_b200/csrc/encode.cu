@@ -1015,4 +1015,60 @@ gse_status decode_all(const Matrix& M, int level, double* out, cudaStream_t s) {
   return GSE_OK;
 }
 
+// R29: one thread per row sums |dec_3 - dec_1| and |dec_3 - dec_2| in storage order (the
+// oracle's order: bit-identical sums); the maxima of the non-negative sums by atomicMax on
+// their bit patterns (order-free)
+__global__ void k_perturb_eta(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ col_ei,
+                              const uint8_t* __restrict__ side, const uint16_t* __restrict__ head,
+                              const uint16_t* __restrict__ tail1,
+                              const uint32_t* __restrict__ tail2, int64_t rows, int ei_bits,
+                              const DecodeTable* __restrict__ dt,
+                              unsigned long long* __restrict__ eta_bits) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int sh = 32 - ei_bits;
+  double m1 = 0.0, m2 = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += stride) {
+    double s1 = 0.0, s2 = 0.0;
+    for (uint32_t j = rp[i]; j < rp[i + 1]; ++j) {
+      const unsigned ei = side ? side[j] : __funnelshift_rc(col_ei[j], 0u, sh);
+      const uint32_t h = head[j], t1 = tail1[j];
+      const double v3 = decode_l3(h, t1, tail2[j], dt->d64[2][ei]);
+      const double v1 = decode_l1(h, dt->d64[0][ei]);
+      const double v2 = decode_l2(h, t1, dt->d64[1][ei]);
+      s1 = __dadd_rn(s1, fabs(__dsub_rn(v3, v1)));
+      s2 = __dadd_rn(s2, fabs(__dsub_rn(v3, v2)));
+    }
+    m1 = fmax(m1, s1);
+    m2 = fmax(m2, s2);
+  }
+  if (m1 > 0.0) atomicMax(eta_bits, (unsigned long long)__double_as_longlong(m1));
+  if (m2 > 0.0) atomicMax(eta_bits + 1, (unsigned long long)__double_as_longlong(m2));
+}
+
+gse_status perturbation_bounds(Matrix& M, cudaStream_t s) {
+  if (M.eta_ok) return GSE_OK;
+  if (M.kind != GSE_KIND_GSE) {
+    set_error("perturbation bounds are defined for GSE matrices");
+    return GSE_ERR_WRONG_FORMAT;
+  }
+  unsigned long long* d = dev_alloc_n<unsigned long long>(2, s);
+  if (!d) return GSE_ERR_OOM;
+  GSE_CUDA_TRY(cudaMemsetAsync(d, 0, 16, s));
+  if (M.rows > 0) {
+    const int g = grid_for(M.rows, 256, M.device);
+    const uint8_t* side = M.ei_in_column ? nullptr : M.side_ei;
+    k_perturb_eta<<<g, 256, 0, s>>>(M.row_ptr, M.col_ei, side, M.head, M.tail1, M.tail2, M.rows,
+                                    M.ei_bits, M.dtab, d);
+    GSE_CUDA_TRY(cudaGetLastError());
+  }
+  unsigned long long h[2] = {0, 0};
+  GSE_CUDA_TRY(cudaMemcpyAsync(h, d, 16, cudaMemcpyDeviceToHost, s));
+  GSE_CUDA_TRY(cudaStreamSynchronize(s));
+  dev_free(d, s);
+  memcpy(&M.eta[0], &h[0], 8);
+  memcpy(&M.eta[1], &h[1], 8);
+  M.eta_ok = 1;
+  return GSE_OK;
+}
+
 }  // namespace gse

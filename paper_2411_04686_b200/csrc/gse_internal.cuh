@@ -35,8 +35,14 @@ constexpr int RW_TILE = 1024;  // max staged span (8-aligned non-zeros) of a row
 // non-zeros per lane, row starts come from a 1-bit-per-non-zero bitmap (encode-time).
 constexpr int WIN_EPT = 8;                  // consecutive non-zeros per lane and chunk
 constexpr int WIN_CH = 32 * WIN_EPT;        // non-zeros per warp chunk
-constexpr uint32_t WIN_HALF = 512;          // x window reaches this many columns past the rows
-constexpr uint32_t WIN_RMAX = 2048;         // rows per tile (bounds the window)
+#ifndef GSE_WIN_HALF
+#define GSE_WIN_HALF 512
+#endif
+#ifndef GSE_WIN_RMAX
+#define GSE_WIN_RMAX 2048
+#endif
+constexpr uint32_t WIN_HALF = GSE_WIN_HALF;  // x window reaches this many columns past the rows
+constexpr uint32_t WIN_RMAX = GSE_WIN_RMAX;  // rows per tile (bounds the window)
 #ifndef GSE_WIN_TNNZ
 #define GSE_WIN_TNNZ 16384
 #endif
@@ -100,6 +106,8 @@ struct Matrix {
   DecodeTable* dtab = nullptr;  // device copy
   DecodeTable htab;             // host copy
   SolverWs* ws = nullptr;
+  double eta[2] = {0.0, 0.0};   // R29 ||A_3 - A_L||_inf, L = 1, 2 (valid when eta_ok)
+  int eta_ok = 0;
   DistCtx* dist = nullptr;      // non-null for a row-partitioned matrix
   int64_t n_local_cols = 0;     // dist: owned + halo columns
 };
@@ -187,6 +195,9 @@ gse_status fp64_matrix(Matrix& M, const void* d_row_ptr, int rp64, const int32_t
                        const double* d_val, cudaStream_t s, int kind = GSE_KIND_FP64);
 void build_decode_table(Matrix& M);
 gse_status decode_all(const Matrix& M, int level, double* out, cudaStream_t s);
+// R29: M.eta = max_i sum_j |dec_3(a_ij) - dec_L(a_ij)| (row sums in storage order, bit-exact
+// with the oracle), computed once per matrix (synchronises s)
+gse_status perturbation_bounds(Matrix& M, cudaStream_t s);
 
 // spmv.cu
 struct DotOut {
@@ -194,9 +205,6 @@ struct DotOut {
   unsigned* ticket = nullptr;   // last-block counter (reset by the last block)
   double* result = nullptr;     // deterministic sum of partials
 };
-gse_status launch_spmv_cgp(const Matrix& M, int level, const double* p_old, const double* r,
-                           double* p_new, double* x, const double* alpha, const double* beta,
-                           double* q, const DotOut* dot, cudaStream_t s, const int* stop);
 gse_status launch_spmv(const Matrix& M, int level, const double* x, double* y,
                        const DotOut* dot, cudaStream_t s, const int* stop = nullptr);
 gse_status launch_spmv_guarded(const Matrix& M, int level, const double* x, double* y,
@@ -214,6 +222,9 @@ gse_status solve_gmres(Matrix& M, const double* b, double* x, double tol, int re
                        int64_t max_iters, const gse_step_schedule& sched,
                        gse_solve_report& rep, cudaStream_t s);
 void free_solver_ws(Matrix& M);
+// y = A_L x and *dot = x . y (device pointers) with the CG's fused SpMV + dot kernel
+gse_status spmv_dot_ws(Matrix& M, int level, const double* x, double* y, double* dot,
+                       cudaStream_t s);
 
 // dist.cu
 gse_status dist_halo_exchange(const Matrix& M, double* x_local_ext, cudaStream_t s);

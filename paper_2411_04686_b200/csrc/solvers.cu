@@ -47,8 +47,9 @@ struct SolveCtrl {
   double dot;  // scratch reduction target
   double rr_part;  // distributed CG: this rank's r.r partial (allreduced before k_cg_events)
   double alpha;    // CG: step of the current iteration, applied to x by k_cg_xpay (0: none)
-  double pend_alpha;  // CG with the p update in the SpMV: last alpha and the buffer of its p
-  long long pend_buf;  // (applied to x by k_cg_xfin after the loop)
+  double perturb_c, eta[2];  // R29 trigger: c and ||A_3 - A_L||_inf (L = 1, 2); c = 0: off
+  double xx;       // R29: ||x||^2 of the latest iterate (CG: after the previous iteration's
+                   // x update; GMRES: at the start of the cycle)
   int upd_ok;
   long long iter, max_iters;
   int level, event, stop, stepped, max_level;
@@ -66,7 +67,6 @@ struct SolverWs {
   int64_t n = 0;
   int vgrid = 0;
   double *x = nullptr, *r = nullptr, *p = nullptr, *q = nullptr, *b = nullptr, *tmp = nullptr;
-  double* p2 = nullptr;  // second p buffer of the fused CG graph (p_old / p_new alternate)
   double* V = nullptr;  // GMRES basis (restart + 1) x n
   int V_cols = 0;
   // 16-bit Krylov basis (NEXT-4): words, per-vector tables, histogram, decoded current vector
@@ -90,6 +90,7 @@ struct SolverWs {
   cudaGraphExec_t gm_exec[3] = {nullptr, nullptr, nullptr};
   cudaGraph_t gm_graph[3] = {nullptr, nullptr, nullptr};
   int gm_restart = 0;
+  int cg_xx = 0;  // the CG graphs compute ||x||^2 in k_cg_xpay (R29 trigger on)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
@@ -181,6 +182,13 @@ __device__ void ring_push(SolveCtrl* c, double* ring, double v) {
 __device__ int monitor_check(const SolveCtrl* c, const double* ring, long long j, double resid) {
   if (!c->stepped || c->level >= c->max_level) return 0;
   if (c->level <= 2 && c->floor_[c->level - 1] > 0.0 && resid < c->floor_[c->level - 1]) return 1;
+  // R29: the level's attainable-accuracy floor c eta_L ||x|| / ||b|| (oracle's operation order)
+  if (c->level <= 2 && c->perturb_c > 0.0 && c->xx > 0.0) {
+    double thr = __dmul_rn(c->perturb_c, c->eta[c->level - 1]);
+    thr = __dmul_rn(thr, sqrt(c->xx));
+    thr = thr / c->bnorm;
+    if (resid <= thr) return 1;
+  }
   const long long t = c->t, cap = t + 1;
   if (j < c->l || ((j - c->l) % c->m) != 0 || c->ring_count < cap) return 0;
   auto w = [&](long long i) { return ring[(c->ring_head + i) % cap]; };
@@ -281,7 +289,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_update(SolveCtrl* __restrict__ c,
                                                    const double* __restrict__ q, int64_t n,
                                                    double* partials, unsigned* ticket,
                                                    cudaGraphConditionalHandle handle,
-                                                   int in_graph, int defer, int pbuf) {
+                                                   int in_graph, int defer) {
   pdl_wait();
   pdl_trigger();
   __shared__ unsigned long long sctrl[CTRL_HEAD_WORDS];
@@ -335,8 +343,6 @@ __global__ void __launch_bounds__(256, 4) k_cg_update(SolveCtrl* __restrict__ c,
   if (grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0) {
     SolveCtrl* sc = reinterpret_cast<SolveCtrl*>(sctrl);
     sc->alpha = ok ? alpha : 0.0;
-    sc->pend_alpha = sc->alpha;
-    sc->pend_buf = pbuf;
     if (defer) {  // distributed: r.r is this rank's partial; k_cg_events runs after the allreduce
       sc->rr_part = tot;
       sc->upd_ok = ok ? 1 : 0;
@@ -355,96 +361,20 @@ __global__ void k_cg_events(SolveCtrl* __restrict__ c, double* ring) {
   cg_events(c, ring, c->rr_part, c->upd_ok != 0, 0, 0);
 }
 
-// Fused CG tail (single GPU): x += alpha p, r -= alpha q, r.r -> ONE grid barrier ->
-// residual / monitor / events (CTA 0) and p = r + beta p with the new r still in registers.
-// Cooperative launch (all CTAs co-resident); each thread owns elements i0 + k*stride,
-// k < FUSE_K.  Saves the separate xpay pass (r read again) and one kernel boundary per
-// iteration.  The p update runs even when an event fires: every event either stops the
-// solve or restarts it with p = r (R15), so p is never used stale.
-constexpr int FUSE_K = 16;
-
-__global__ void __launch_bounds__(256, 4) k_cg_fused(SolveCtrl* __restrict__ c, double* ring,
-                                                  double* __restrict__ x, double* __restrict__ r,
-                                                  double* __restrict__ p,
-                                                  const double* __restrict__ q, int64_t n,
-                                                  double* partials,
-                                                  cudaGraphConditionalHandle handle,
-                                                  int in_graph) {
-  __shared__ double red[8];
-  __shared__ double s_tot;
-  if (c->event != EV_NONE) return;  // uniform: written only before this launch
-  const double pq = c->pq, rr = c->rr;
-  const bool ok = (pq > 0.0) && isfinite(pq);
-  const double alpha = rr / pq;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  double rv[FUSE_K];
-  double acc = 0.0;
-#pragma unroll
-  for (int k = 0; k < FUSE_K; ++k) {
-    const int64_t j = i0 + k * stride;
-    rv[k] = 0.0;
-    if (ok && j < n) {
-      const double xv = x[j], pv = p[j], rj = r[j], qv = q[j];
-      x[j] = __dadd_rn(xv, __dmul_rn(alpha, pv));
-      rv[k] = __dsub_rn(rj, __dmul_rn(alpha, qv));
-      r[j] = rv[k];
-      acc = __dadd_rn(acc, __dmul_rn(rv[k], rv[k]));
-    }
-  }
-  acc = warp_sum_d(acc);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-    partials[blockIdx.x] = s;
-  }
-  __threadfence();
-  cooperative_groups::this_grid().sync();
-  // every CTA sums the partials in the same fixed order -> identical total everywhere
-  if (threadIdx.x < 32) {
-    double s = 0.0;
-    for (unsigned i = threadIdx.x; i < gridDim.x; i += 32) s += __ldcg(partials + i);
-    s = warp_sum_d(s);
-    if (threadIdx.x == 0) s_tot = s;
-  }
-  __syncthreads();
-  const double tot = s_tot;
-  if (blockIdx.x == 0 && threadIdx.x == 0) cg_events(c, ring, tot, ok, handle, in_graph);
-  if (!ok) return;
-  const double beta = tot / rr;
-#pragma unroll
-  for (int k = 0; k < FUSE_K; ++k) {
-    const int64_t j = i0 + k * stride;
-    if (j < n) p[j] = __dadd_rn(rv[k], __dmul_rn(beta, p[j]));
-  }
-}
-
-// After the fused CG graph's loop: the x update of the last iteration (its SpMV, which
-// would have applied it, was stopped by the event): x += pend_alpha p[pend_buf]
-__global__ void __launch_bounds__(256) k_cg_xfin(const SolveCtrl* __restrict__ c,
-                                                 double* __restrict__ x,
-                                                 const double* __restrict__ p0,
-                                                 const double* __restrict__ p1, int64_t n) {
-  const double a = c->pend_alpha;
-  if (a == 0.0) return;
-  const double* pp = c->pend_buf ? p1 : p0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-    x[i] = __dadd_rn(x[i], __dmul_rn(a, pp[i]));
-}
-
 // x += alpha p (the update deferred by k_cg_update) ; p = r + beta p (skipped when an event
-// is pending: the host restarts / stops).  Both read the old p.
-__global__ void __launch_bounds__(256, 4) k_cg_xpay(const SolveCtrl* __restrict__ c,
+// is pending: the host restarts / stops).  Both read the old p.  XX (R29 trigger on): also
+// ||x_new||^2 -> c->xx (deterministic grid sum; x unchanged -> xx kept).
+template <bool XX>
+__global__ void __launch_bounds__(256, 4) k_cg_xpay(SolveCtrl* __restrict__ c,
                                                  double* __restrict__ x, double* __restrict__ p,
-                                                 const double* __restrict__ r, int64_t n) {
+                                                 const double* __restrict__ r, int64_t n,
+                                                 double* partials, unsigned* ticket) {
   pdl_wait();
   pdl_trigger();
   const double alpha = c->alpha, beta = c->beta;
   const bool do_x = alpha != 0.0, do_p = c->event == EV_NONE;
   if (!do_x && !do_p) return;
+  double acc = 0.0;
   const int64_t n2 = n >> 1;
   double2* __restrict__ x2 = reinterpret_cast<double2*>(x);
   double2* __restrict__ p2 = reinterpret_cast<double2*>(p);
@@ -470,6 +400,10 @@ __global__ void __launch_bounds__(256, 4) k_cg_xpay(const SolveCtrl* __restrict_
           o.x = __dadd_rn(xv[k].x, __dmul_rn(alpha, pv[k].x));
           o.y = __dadd_rn(xv[k].y, __dmul_rn(alpha, pv[k].y));
           x2[j] = o;
+          if constexpr (XX) {
+            acc = __dadd_rn(acc, __dmul_rn(o.x, o.x));
+            acc = __dadd_rn(acc, __dmul_rn(o.y, o.y));
+          }
         }
         if (do_p) {
           double2 o;
@@ -483,8 +417,15 @@ __global__ void __launch_bounds__(256, 4) k_cg_xpay(const SolveCtrl* __restrict_
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
     const int64_t j = n - 1;
     const double pv = p[j];
-    if (do_x) x[j] = __dadd_rn(x[j], __dmul_rn(alpha, pv));
+    if (do_x) {
+      x[j] = __dadd_rn(x[j], __dmul_rn(alpha, pv));
+      if constexpr (XX) acc = __dadd_rn(acc, __dmul_rn(x[j], x[j]));
+    }
     if (do_p) p[j] = __dadd_rn(r[j], __dmul_rn(beta, pv));
+  }
+  if constexpr (XX) {
+    double tot;
+    if (do_x && grid_sum(acc, partials, ticket, &tot) && threadIdx.x == 0) c->xx = tot;
   }
 }
 
@@ -1328,7 +1269,6 @@ static gse_status ensure_ws(Matrix& M, int64_t ring_t, int gm_restart, cudaStrea
     // p is gathered by the SpMV: distributed -> owned + halo entries
     ws->p = dev_alloc_n<double>((size_t)dist_ext_cols(M) + 1, s);
     ws->q = dev_alloc_n<double>(nn, s);
-    if (!M.dist) ws->p2 = dev_alloc_n<double>((size_t)dist_ext_cols(M) + 1, s);
     ws->b = dev_alloc_n<double>(nn, s);
     ws->tmp = dev_alloc_n<double>(nn, s);
     const int64_t np = (M.n_blocks > 2 * ws->vgrid ? M.n_blocks : 2 * ws->vgrid) + 1;
@@ -1386,7 +1326,7 @@ void free_solver_ws(Matrix& M) {
     if (ws->gm_exec[L]) cudaGraphExecDestroy(ws->gm_exec[L]);
     if (ws->gm_graph[L]) cudaGraphDestroy(ws->gm_graph[L]);
   }
-  for (double* p : {ws->x, ws->r, ws->p, ws->p2, ws->q, ws->b, ws->tmp, ws->V, ws->partials,
+  for (double* p : {ws->x, ws->r, ws->p, ws->q, ws->b, ws->tmp, ws->V, ws->partials,
                     ws->ring, ws->vcur})
     if (p) dev_free(p, s);
   for (void* p : {(void*)ws->V16, (void*)ws->vtab, (void*)ws->vlen, (void*)ws->vhist,
@@ -1425,6 +1365,14 @@ static DotOut dot_to(SolverWs* ws, double* target) {
   return d;
 }
 
+gse_status spmv_dot_ws(Matrix& M, int level, const double* x, double* y, double* dot,
+                       cudaStream_t s) {
+  gse_status rc = ensure_ws(M, 0, 0, s);
+  if (rc != GSE_OK) return rc;
+  DotOut d = dot_to(M.ws, dot);
+  return launch_spmv(M, level, x, y, &d, s, nullptr);
+}
+
 // GSE_NO_GRAPH=1: drive solver iterations from the host instead of CUDA graphs (ncu cannot
 // profile kernel nodes of graphs with conditional nodes; also a fallback)
 static bool no_graph() {
@@ -1435,39 +1383,23 @@ static bool no_graph() {
   return v;
 }
 
-// cooperative grid for k_cg_fused: all CTAs resident and n <= FUSE_K x threads; 0 -> use
-// the unfused update + xpay kernels (also when GSE_CG_UNFUSED=1, for A/B measurements)
-static int fused_grid(const Matrix& M) {
-  // opt-in (GSE_CG_FUSED=1): on C2 the register-resident tail spills and ran at 89 us per
-  // iteration vs 64 us for update + xpay (profiles/README.md), so it is off by default
-  static const bool off = [] {
-    const char* e = getenv("GSE_CG_FUSED");
-    return !(e && e[0] == '1');
-  }();
-  if (off) return 0;
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_fused, 256, 0) != cudaSuccess) {
-    cudaGetLastError();
-    return 0;
-  }
-  const int64_t cap = (int64_t)per_sm * num_sms(M.device);
-  int64_t want = (M.rows + 255) / 256;
-  if (want > cap) want = cap;
-  const bool fits = want >= 1 && M.rows <= (int64_t)FUSE_K * want * 256;
-  if (getenv("GSE_DEBUG"))
-    fprintf(stderr, "[gse] k_cg_fused: %d CTAs/SM, grid %lld, rows %lld -> %s\n", per_sm,
-            (long long)want, (long long)M.rows, fits ? "fused" : "unfused");
-  return fits ? (int)want : 0;
+// x += alpha p ; p = r + beta p (+ ||x||^2 when the R29 trigger is on: ws->cg_xx)
+static void launch_xpay(SolverWs* ws, cudaStream_t s, int64_t n) {
+  if (ws->cg_xx)
+    launch_k(k_cg_xpay<true>, ws->vgrid, 256, 0, s, ws->ctrl, ws->x, ws->p, (const double*)ws->r,
+             n, ws->partials, ws->ticket);
+  else
+    launch_k(k_cg_xpay<false>, ws->vgrid, 256, 0, s, ws->ctrl, ws->x, ws->p, (const double*)ws->r,
+             n, ws->partials, ws->ticket);
 }
 
-// The CG p update fused into the next SpMV (launch_spmv_cgp): row-walk matrices, single
-// GPU, graph path; opt-in (GSE_CG_FUSEP=1, read when a graph is built).  Results are
-// bitwise those of the separate xpay kernel, but the second gathered vector (r and p_old
-// instead of p) costs more than the pass it saves: C2 stepped CG 56.5 vs 46.2 us per
-// iteration (64^3: 17.2 vs 17.7), profiles/ab_cg_fusep_r01.txt.
-static bool cg_fuse_p(const Matrix& M) {
-  const char* e = getenv("GSE_CG_FUSEP");
-  return e && atoi(e) == 1 && M.spmv_mode == SPMV_RW && M.rows > 0 && M.ws && M.ws->p2;
+static void drop_cg_graphs(SolverWs* ws) {
+  for (int L = 0; L < 3; ++L) {
+    if (ws->cg_exec[L]) cudaGraphExecDestroy(ws->cg_exec[L]);
+    if (ws->cg_graph[L]) cudaGraphDestroy(ws->cg_graph[L]);
+    ws->cg_exec[L] = nullptr;
+    ws->cg_graph[L] = nullptr;
+  }
 }
 
 // ---------------------------------------------------------------- CG graph per level
@@ -1499,66 +1431,28 @@ static gse_status build_cg_graph(Matrix& M, int level) {
     const int u = e ? atoi(e) : 8;
     return u < 1 ? 1 : (u > 32 ? 32 : u);
   }();
-  const int fg = fused_grid(M);
-  const bool fp = fg == 0 && cg_fuse_p(M);
-  // fused p update: p_old / p_new alternate between ws->p and ws->p2, so the body holds an
-  // even number of iterations (every pass starts with p in ws->p)
-  const int nu = fp ? (unroll + 1) & ~1 : unroll;
   gse_status rc = GSE_OK;
-  for (int u = 0; u < nu && rc == GSE_OK; ++u) {
-  if (fp) {
-    double* po = (u & 1) ? ws->p2 : ws->p;
-    double* pn = (u & 1) ? ws->p : ws->p2;
-    rc = launch_spmv_cgp(M, level, po, ws->r, pn, ws->x, &ws->ctrl->alpha, &ws->ctrl->beta,
-                         ws->q, &d, cs, &ws->ctrl->event);
-    if (rc == GSE_OK)
-      launch_k(k_cg_update, ws->vgrid, 256, 0, cs, ws->ctrl, ws->ring, ws->r,
-               (const double*)ws->q, n, ws->partials, ws->ticket, h, 1, 0, (u + 1) & 1);
-    continue;
-  }
-  rc = launch_spmv(M, level, ws->p, ws->q, &d, cs, &ws->ctrl->event);
-  if (fg > 0) {
-    // cooperative fused tail (one grid barrier), see k_cg_fused
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(fg);
-    cfg.blockDim = dim3(256);
-    cfg.stream = cs;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    cudaError_t le = cudaLaunchKernelEx(&cfg, k_cg_fused, ws->ctrl, ws->ring, ws->x, ws->r,
-                                        ws->p, (const double*)ws->q, n, ws->partials, h, 1);
-    if (le != cudaSuccess) {
-      cudaStreamEndCapture(cs, nullptr);
-      return cuda_status(le, "cooperative k_cg_fused");
-    }
-  } else {
-    launch_k(k_cg_update, ws->vgrid, 256, 0, cs, ws->ctrl, ws->ring, ws->r, ws->q, n, ws->partials,
-                                           ws->ticket, h, 1, 0, 0);
-    launch_k(k_cg_xpay, ws->vgrid, 256, 0, cs, ws->ctrl, ws->x, ws->p, ws->r, n);
-  }
+  for (int u = 0; u < unroll && rc == GSE_OK; ++u) {
+    rc = launch_spmv(M, level, ws->p, ws->q, &d, cs, &ws->ctrl->event);
+    launch_k(k_cg_update, ws->vgrid, 256, 0, cs, ws->ctrl, ws->ring, ws->r, ws->q, n,
+             ws->partials, ws->ticket, h, 1, 0);
+    launch_xpay(ws, cs, n);
   }
   cudaGraph_t captured;
   cudaError_t e = cudaStreamEndCapture(cs, &captured);
   if (rc != GSE_OK) return rc;
   GSE_CUDA_TRY(e);
-  if (fp) {  // after the loop: the last iteration's x update
-    GSE_CUDA_TRY(cudaStreamBeginCaptureToGraph(cs, g, &node, nullptr, 1,
-                                               cudaStreamCaptureModeRelaxed));
-    launch_k(k_cg_xfin, ws->vgrid, 256, 0, cs, (const SolveCtrl*)ws->ctrl, ws->x,
-             (const double*)ws->p, (const double*)ws->p2, n);
-    e = cudaStreamEndCapture(cs, &captured);
-    GSE_CUDA_TRY(e);
-  }
   GSE_CUDA_TRY(cudaGraphInstantiate(&ws->cg_exec[level - 1], g, 0));
   ws->cg_graph[level - 1] = g;
   return GSE_OK;
 }
 
-static void fill_sched(SolveCtrl* h, const gse_step_schedule& sc, int stepped) {
+static void fill_sched(SolveCtrl* h, const gse_step_schedule& sc, int stepped, const Matrix& M) {
   h->stepped = stepped;
+  h->perturb_c = (stepped && M.eta_ok) ? sc.perturb_c : 0.0;
+  h->eta[0] = M.eta[0];
+  h->eta[1] = M.eta[1];
+  h->xx = 0.0;
   h->max_level = sc.max_level;
   h->l = sc.l;
   h->t = sc.t;
@@ -1628,6 +1522,15 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
   gse_status rc = ensure_ws(M, stepped ? sched.t : 0, 0, s);
   if (rc != GSE_OK) return rc;
   SolverWs* ws = M.ws;
+  const bool xx_on = stepped && sched.perturb_c > 0.0;
+  if (xx_on) {
+    rc = perturbation_bounds(M, s);  // once per matrix (R29)
+    if (rc != GSE_OK) return rc;
+  }
+  if ((int)xx_on != ws->cg_xx) {  // the graphs' xpay variant follows the trigger
+    drop_cg_graphs(ws);
+    ws->cg_xx = xx_on ? 1 : 0;
+  }
   GSE_CUDA_TRY(cudaEventRecord(ws->ev0, s));
   GSE_CUDA_TRY(cudaMemcpyAsync(ws->b, b, n * 8, cudaMemcpyDeviceToDevice, s));
   GSE_CUDA_TRY(cudaMemcpyAsync(ws->x, x, n * 8, cudaMemcpyDeviceToDevice, s));
@@ -1684,10 +1587,12 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
     hc->max_iters = max_iters;
     hc->level = level;
     hc->event = EV_NONE;
-    hc->alpha = hc->beta = hc->pend_alpha = 0.0;  // fused p update: p_1 = r_0 + 0 p_0
-    hc->pend_buf = 0;
-    fill_sched(hc, sched, stepped);
+    hc->alpha = hc->beta = 0.0;
+    fill_sched(hc, sched, stepped, M);
     GSE_CUDA_TRY(cudaMemcpyAsync(ws->ctrl, hc, sizeof(SolveCtrl), cudaMemcpyHostToDevice, s));
+    if (xx_on)  // R29: ||x0||^2 for the first iteration's check
+      launch_k(k_dot, ws->vgrid, 256, 0, s, (const double*)ws->x, (const double*)ws->x, n,
+               ws->partials, ws->ticket, &ws->ctrl->xx);
   }
   int64_t last_iter = 0;
   while (!done) {
@@ -1706,11 +1611,11 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
           rc = dist_allreduce_sum(M, &ws->ctrl->pq, 1, s);
           if (rc != GSE_OK) return rc;
           launch_k(k_cg_update, ws->vgrid, 256, 0, s, ws->ctrl, ws->ring, ws->r, ws->q, n,
-                                                ws->partials, ws->ticket, 0, 0, 1, 0);
+                   ws->partials, ws->ticket, 0, 0, 1);
           rc = dist_allreduce_sum(M, &ws->ctrl->rr_part, 1, s);
           if (rc != GSE_OK) return rc;
           launch_k(k_cg_events, 1, 32, 0, s, ws->ctrl, ws->ring);
-          launch_k(k_cg_xpay, ws->vgrid, 256, 0, s, ws->ctrl, ws->x, ws->p, ws->r, n);
+          launch_xpay(ws, s, n);
         }
         GSE_CUDA_TRY(cudaGetLastError());
         rc = read_ctrl(ws, s);
@@ -1724,8 +1629,8 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
           rc = launch_spmv(M, level, ws->p, ws->q, &d, s, &ws->ctrl->event);
           if (rc != GSE_OK) return rc;
           launch_k(k_cg_update, ws->vgrid, 256, 0, s, ws->ctrl, ws->ring, ws->r, ws->q, n,
-                                                ws->partials, ws->ticket, 0, 0, 0, 0);
-          launch_k(k_cg_xpay, ws->vgrid, 256, 0, s, ws->ctrl, ws->x, ws->p, ws->r, n);
+                   ws->partials, ws->ticket, 0, 0, 0);
+          launch_xpay(ws, s, n);
         }
         GSE_CUDA_TRY(cudaGetLastError());
         rc = read_ctrl(ws, s);
@@ -1780,7 +1685,7 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
       if (rc != GSE_OK) return rc;
       rc = set_field(ws, &SolveCtrl::event, (int)EV_NONE, s);
       if (rc != GSE_OK) return rc;
-      for (double SolveCtrl::*f : {&SolveCtrl::alpha, &SolveCtrl::beta, &SolveCtrl::pend_alpha}) {
+      for (double SolveCtrl::*f : {&SolveCtrl::alpha, &SolveCtrl::beta}) {
         rc = set_field(ws, f, 0.0, s);
         if (rc != GSE_OK) return rc;
       }
@@ -1880,6 +1785,10 @@ static gse_status build_gm_graph(Matrix& M, int level, int restart, int k16) {
   SolveCtrl* c = ws->ctrl;
   double* w = ws->tmp;
   GSE_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+  // R29: ||x||^2 at the start of the cycle (one vector read per cycle; read only when the
+  // perturbation trigger is on)
+  launch_k(k_dot, ws->vgrid, 256, 0, cs, (const double*)ws->x, (const double*)ws->x, n,
+           ws->partials, ws->ticket, &c->xx);
   gse_status rc = launch_spmv(M, level, ws->x, w, nullptr, cs);
   launch_pdl(k_gm_restart, ws->vgrid, 256, 0, cs, c, ws->b, w, n, ws->partials, ws->ticket, 0);
   if (k16) {
@@ -2042,6 +1951,10 @@ gse_status solve_gmres(Matrix& M, const double* b, double* x, double tol, int re
   gse_status rc = ensure_ws(M, stepped ? sched.t : 0, restart, s, k16);
   if (rc != GSE_OK) return rc;
   SolverWs* ws = M.ws;
+  if (stepped && sched.perturb_c > 0.0) {
+    rc = perturbation_bounds(M, s);  // once per matrix (R29)
+    if (rc != GSE_OK) return rc;
+  }
   GSE_CUDA_TRY(cudaEventRecord(ws->ev0, s));
   GSE_CUDA_TRY(cudaMemcpyAsync(ws->b, b, n * 8, cudaMemcpyDeviceToDevice, s));
   GSE_CUDA_TRY(cudaMemcpyAsync(ws->x, x, n * 8, cudaMemcpyDeviceToDevice, s));
@@ -2068,7 +1981,7 @@ gse_status solve_gmres(Matrix& M, const double* b, double* x, double tol, int re
   hc->stop = 0;
   hc->restart = restart;
   hc->k = 0;
-  fill_sched(hc, sched, stepped);
+  fill_sched(hc, sched, stepped, M);
   GSE_CUDA_TRY(cudaMemcpyAsync(ws->ctrl, hc, sizeof(SolveCtrl), cudaMemcpyHostToDevice, s));
   gse_status status = GSE_NOT_CONVERGED;
   int64_t last_iter = 0, iter = 0;

@@ -14,11 +14,6 @@ template <class T>
 static SpmvParams<T> make_params(const Matrix& M, int level, const T* x, T* y,
                                  const DotOut* dot) {
   SpmvParams<T> p;
-  p.fr = nullptr;
-  p.fpn = nullptr;
-  p.fx = nullptr;
-  p.falpha = nullptr;
-  p.fbeta = nullptr;
   p.blocks = M.blocks;
   p.row_ptr = M.row_ptr;
   p.col_ei = M.col_ei;
@@ -47,6 +42,7 @@ static SpmvParams<T> make_params(const Matrix& M, int level, const T* x, T* y,
   p.rowbits = reinterpret_cast<const uint8_t*>(M.rowbits);
   p.chunk_prev = M.chunk_prev;
   p.n_tiles = (uint32_t)M.n_tiles;
+  p.nnz_pad = (uint32_t)padded(M.nnz);
   p.cols = (uint32_t)dist_ext_cols(M);
   p.win_on = ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) ? 1 : 0;
   const int L = level >= 1 && level <= 3 ? level : 3;
@@ -78,28 +74,6 @@ static void dispatch(const Matrix& M, int level, bool dot, const SpmvParams<T>& 
 
 static bool empty_matrix(const Matrix& M) {
   return M.kind == GSE_KIND_GSE ? M.rows == 0 : M.rows == 0;
-}
-
-// CG iteration with the p update fused in (row-walk matrices only): operand r + beta p_old,
-// writes p_new and x += alpha p_old for every row, q = A p_new, dot p_new . q
-gse_status launch_spmv_cgp(const Matrix& M, int level, const double* p_old, const double* r,
-                           double* p_new, double* x, const double* alpha, const double* beta,
-                           double* q, const DotOut* dot, cudaStream_t s, const int* stop) {
-  if (M.spmv_mode != SPMV_RW || M.rows == 0 || !dot) {
-    set_error("internal: the fused CG SpMV needs a non-empty row-walk matrix and a dot");
-    return GSE_ERR_INVALID_ARG;
-  }
-  SpmvParams<double> p = make_params<double>(M, level, p_old, q, dot);
-  p.stop = stop;
-  p.fr = r;
-  p.fpn = p_new;
-  p.fx = x;
-  p.falpha = alpha;
-  p.fbeta = beta;
-  const int L = level >= 1 && level <= 3 ? level : 3;
-  launch_rw<double>(M, level, true, M.kind == GSE_KIND_GSE && M.htab.fast64[L - 1], p, s);
-  GSE_CUDA_TRY(cudaGetLastError());
-  return GSE_OK;
 }
 
 gse_status launch_spmv(const Matrix& M, int level, const double* x, double* y,

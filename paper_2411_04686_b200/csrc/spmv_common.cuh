@@ -160,15 +160,9 @@ struct SpmvParams {
   const uint8_t* __restrict__ rowbits;
   const uint32_t* __restrict__ chunk_prev;
   uint32_t n_tiles;
+  uint32_t nnz_pad;   // allocated (padded) plane length: bulk copies never read past it
   uint32_t cols;
   int win_on;         // x is 16-byte aligned: windows staged by TMA (else every gather is global)
-  // CG p update fused into the SpMV (row walk, FP64; x is p_old): the operand is
-  // r + beta p_old, p_new and x += alpha p_old are written for the launch's rows
-  const double* fr;
-  double* fpn;
-  double* fx;
-  const double* falpha;
-  const double* fbeta;
   long long d64[64];  // decode deltas of the launched level (integer form, FP64)
   int d32[64];        // (integer form, FP32)
   double sc64[64];    // multiply-form scales when the table allows it (FAST)

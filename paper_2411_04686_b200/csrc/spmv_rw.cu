@@ -89,9 +89,9 @@ struct Chunk8 {
 };
 
 // the 8 staged slots from j on and their gathered operands (all gathers issued here)
-template <int L, class T, bool FUSE>
+template <int L, class T>
 __device__ __forceinline__ void load_chunk(const SpmvParams<T>& p, const Stage<L>& st,
-                                           uint32_t j, Chunk8<T>& K, double fbeta) {
+                                           uint32_t j, Chunk8<T>& K) {
   uint32_t* c = K.c;
   uint32_t* h = K.h;
   uint32_t* t1 = K.t1;
@@ -110,20 +110,6 @@ __device__ __forceinline__ void load_chunk(const SpmvParams<T>& p, const Stage<L
     if constexpr (has_t2<L>()) t2[q] = st.tail2[j + q];
   }
   // all 8 gathers issued before any product (ld.global.nc, volatile asm keeps the order)
-  if constexpr (FUSE) {  // operand r + beta p_old (the CG p update, same rounding)
-    double rv[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const uint32_t cc = c[q] & p.col_mask;
-      double v, w;
-      asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p.fr + cc));
-      asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(w) : "l"(p.x + cc));
-      rv[q] = v;
-      xv[q] = (T)w;
-    }
-#pragma unroll
-    for (int q = 0; q < 8; ++q) xv[q] = (T)__dadd_rn(rv[q], __dmul_rn(fbeta, (double)xv[q]));
-  } else {
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const T* a = p.x + (c[q] & p.col_mask);
@@ -136,7 +122,6 @@ __device__ __forceinline__ void load_chunk(const SpmvParams<T>& p, const Stage<L
       asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(a));
       xv[q] = v;
     }
-  }
   }
 }
 
@@ -202,16 +187,15 @@ __device__ __forceinline__ T sum_chunk(const SpmvParams<T>& p, const Chunk8<T>& 
 }
 
 // sum of one row, elements [j0, j1) of the stage, in storage order
-template <int L, bool FAST, class T, bool FUSE = false>
+template <int L, bool FAST, class T>
 __device__ __forceinline__ T walk_row(const SpmvParams<T>& p, const Stage<L>& st, uint32_t j0,
                                       uint32_t j1, const double* ssc64, const float* ssc32,
                                       const long long* sd64, const int* sd32,
-                                      const double* sc64, const float* sc32,
-                                      double fbeta = 0.0) {
+                                      const double* sc64, const float* sc32) {
   T sum = 0;
   for (uint32_t j = j0; j < j1; j += 8) {
     Chunk8<T> K;
-    load_chunk<L, T, FUSE>(p, st, j, K, fbeta);
+    load_chunk<L, T>(p, st, j, K);
     sum = sum_chunk<L, FAST, T>(p, K, j1 - j, sum, ssc64, ssc32, sd64, sd32, sc64, sc32);
   }
   return sum;
@@ -228,7 +212,7 @@ __device__ __forceinline__ T walk_row(const SpmvParams<T>& p, const Stage<L>& st
 #else
 #define RW_MINB(L) 3
 #endif
-template <int L, int RPL, bool DOT, bool FAST, class T, bool FUSE>
+template <int L, int RPL, bool DOT, bool FAST, class T>
 __global__ void __launch_bounds__(SPMV_THREADS, RW_MINB(L)) k_spmv_rw(const SpmvParams<T> p) {
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t bars[SPMV_WARPS][2];
@@ -298,11 +282,6 @@ __global__ void __launch_bounds__(SPMV_THREADS, RW_MINB(L)) k_spmv_rw(const Spmv
     return;
   }
   pdl_trigger();
-  double fa = 0.0, fb = 0.0;
-  if constexpr (FUSE) {
-    fa = *p.falpha;
-    fb = *p.fbeta;
-  }
   uint32_t it = 0;
   for (; g < ng; g += W, ++it) {
     const uint32_t cur = it & 1u;
@@ -336,8 +315,8 @@ __global__ void __launch_bounds__(SPMV_THREADS, RW_MINB(L)) k_spmv_rw(const Spmv
       const uint32_t n0 = ea[0] - cur_b.a[0], n1 = ea[1] - cur_b.a[1];
       if (__all_sync(0xFFFFFFFFu, n0 <= 8u && n1 <= 8u)) {
         Chunk8<T> K0, K1;
-        load_chunk<L, T, FUSE>(p, st, cur_b.a[0] - base, K0, fb);
-        load_chunk<L, T, FUSE>(p, st, cur_b.a[1] - base, K1, fb);
+        load_chunk<L, T>(p, st, cur_b.a[0] - base, K0);
+        load_chunk<L, T>(p, st, cur_b.a[1] - base, K1);
         sums[0] = n0 ? sum_chunk<L, FAST, T>(p, K0, n0, T(0), ssc64, ssc32, sd64, sd32, sc64,
                                              sc32)
                      : T(0);
@@ -351,8 +330,8 @@ __global__ void __launch_bounds__(SPMV_THREADS, RW_MINB(L)) k_spmv_rw(const Spmv
     if (!paired) {
 #pragma unroll
       for (int k = 0; k < RPL; ++k)
-        sums[k] = walk_row<L, FAST, T, FUSE>(p, st, cur_b.a[k] - base, ea[k] - base, ssc64,
-                                             ssc32, sd64, sd32, sc64, sc32, fb);
+        sums[k] = walk_row<L, FAST, T>(p, st, cur_b.a[k] - base, ea[k] - base, ssc64, ssc32,
+                                       sd64, sd32, sc64, sc32);
     }
 #pragma unroll
     for (int k = 0; k < RPL; ++k) {
@@ -360,15 +339,7 @@ __global__ void __launch_bounds__(SPMV_THREADS, RW_MINB(L)) k_spmv_rw(const Spmv
       const uint32_t row = r0 + 32 * k + lane;
       if (row < rows) {
         p.y[row] = sa;
-        if constexpr (FUSE) {
-          const double po = p.x[row];
-          const double pn = __dadd_rn(p.fr[row], __dmul_rn(fb, po));
-          p.fpn[row] = pn;
-          p.fx[row] = __dadd_rn(p.fx[row], __dmul_rn(fa, po));
-          dacc += pn * (double)sa;
-        } else if (DOT) {
-          dacc += (double)p.xd[row] * (double)sa;
-        }
+        if constexpr (DOT) dacc += (double)p.xd[row] * (double)sa;
       }
     }
     __syncwarp();
@@ -388,13 +359,13 @@ struct RwLaunchCache {
   std::map<std::pair<int, size_t>, int> grid;  // (device, smem) -> resident CTAs x SMs
 };
 
-template <int L, int RPL, bool DOT, bool FAST, class T, bool FUSE>
+template <int L, int RPL, bool DOT, bool FAST, class T>
 static void go_rpl(const Matrix& M, const SpmvParams<T>& p, cudaStream_t s) {
   static RwLaunchCache lc;
   const int dev = M.device < 64 ? M.device : 0;
   const uint32_t N = RPL == 1 ? p.rw_stage : p.rw_stage2;
   const size_t smem = (size_t)SPMV_WARPS * 2 * N * rw_elem_bytes<L>();
-  auto kern = k_spmv_rw<L, RPL, DOT, FAST, T, FUSE>;
+  auto kern = k_spmv_rw<L, RPL, DOT, FAST, T>;
   int cap = 0;
   {
     std::lock_guard<std::mutex> lk(lc.mu);
@@ -435,49 +406,47 @@ static int rw_rpl(const Matrix& M, uint32_t rw_stage2) {
   return (M.rows + 2 * RW_ROWS - 1) / (2 * RW_ROWS) >= 32 * warps ? 2 : 1;
 }
 
-template <int L, bool DOT, bool FAST, class T, bool FUSE>
+template <int L, bool DOT, bool FAST, class T>
 static void go(const Matrix& M, const SpmvParams<T>& p, cudaStream_t s) {
   if (rw_rpl<L>(M, p.rw_stage2) == 2)
-    go_rpl<L, 2, DOT, FAST, T, FUSE>(M, p, s);
+    go_rpl<L, 2, DOT, FAST, T>(M, p, s);
   else
-    go_rpl<L, 1, DOT, FAST, T, FUSE>(M, p, s);
+    go_rpl<L, 1, DOT, FAST, T>(M, p, s);
 }
 
-template <int L, bool DOT, class T, bool FUSE>
+template <int L, bool DOT, class T>
 static void go_l(const Matrix& M, bool fast, const SpmvParams<T>& p, cudaStream_t s) {
   if (fast)
-    go<L, DOT, true, T, FUSE>(M, p, s);
+    go<L, DOT, true, T>(M, p, s);
   else
-    go<L, DOT, false, T, FUSE>(M, p, s);
+    go<L, DOT, false, T>(M, p, s);
 }
 
-template <bool DOT, class T, bool FUSE = false>
+template <bool DOT, class T>
 static void go_dot(const Matrix& M, int level, bool fast, const SpmvParams<T>& p,
                    cudaStream_t s) {
   if (M.kind == GSE_KIND_FP64) {
-    go<0, DOT, false, T, FUSE>(M, p, s);
+    go<0, DOT, false, T>(M, p, s);
   } else if (M.kind == GSE_KIND_FP16 || M.kind == GSE_KIND_BF16) {
     if constexpr (sizeof(T) == 8) {  // FP64 accumulation only
       if (M.kind == GSE_KIND_FP16)
-        go<L_FP16, DOT, false, T, FUSE>(M, p, s);
+        go<L_FP16, DOT, false, T>(M, p, s);
       else
-        go<L_BF16, DOT, false, T, FUSE>(M, p, s);
+        go<L_BF16, DOT, false, T>(M, p, s);
     }
   } else if (level == 1) {
-    go_l<1, DOT, T, FUSE>(M, fast, p, s);
+    go_l<1, DOT, T>(M, fast, p, s);
   } else if (level == 2) {
-    go_l<2, DOT, T, FUSE>(M, fast, p, s);
+    go_l<2, DOT, T>(M, fast, p, s);
   } else {
-    go_l<3, DOT, T, FUSE>(M, fast, p, s);
+    go_l<3, DOT, T>(M, fast, p, s);
   }
 }
 
 template <>
 void launch_rw<double>(const Matrix& M, int level, bool dot, bool fast,
                        const SpmvParams<double>& p, cudaStream_t s) {
-  if (p.fr)  // the CG p update fused in (launch_spmv_cgp; always with the dot)
-    go_dot<true, double, true>(M, level, fast, p, s);
-  else if (dot)
+  if (dot)
     go_dot<true, double>(M, level, fast, p, s);
   else
     go_dot<false, double>(M, level, fast, p, s);

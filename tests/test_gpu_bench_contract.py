@@ -13,7 +13,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_bench_json_line():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3",
-                          "--warmup", "3", "--no-sweep", "--no-cpu-baseline"],
+                          "--warmup", "3", "--workload", "c2", "--quick", "--no-sweep",
+                           "--no-cpu-baseline"],
                          capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]

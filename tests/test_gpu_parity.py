@@ -186,6 +186,35 @@ def test_spmv_levels_parity(g, name):
         assert np.all(yg[bound == 0] == 0.0)
 
 
+@pytest.mark.parametrize("name", ["poisson2d_varcoef", "poisson3d_40", "powerlaw_30k", "convdiff_20"])
+def test_spmv_dot_parity(g, name):
+    """gse_spmv_dot (the CG's fused SpMV + p.q kernel, row walk or window): y within the SpMV
+    bound, the dot within sum_i |x_i| bound_i + 1e-13 sum_i |x_i y_i|, repeat bit-identical;
+    the FP64-CSR matrix the same way"""
+    A = MATS[name]()
+    M, R = enc_both(g, A)
+    x = gi.uniform_vec(A.cols, seed=13)
+    xt = torch.from_numpy(x).cuda()
+    for L in (1, 2, 3):
+        yt, dt = g.gse_spmv_dot(M, xt, segments=L)
+        yg, dg = yt.cpu().numpy(), float(dt.item())
+        yo = O.spmv_gse(R, x, L)
+        bound = spmv_bound(R, x, L, 1e-12)
+        assert np.all(np.abs(yg - yo) <= bound), L
+        do = float(np.dot(x, yo))
+        assert abs(dg - do) <= float(np.abs(x) @ bound) + 1e-13 * float(np.abs(x) @ np.abs(yo)), L
+        _, d2 = g.gse_spmv_dot(M, xt, segments=L)
+        assert float(d2.item()) == dg
+    F = g.gse_fp64_matrix(A.row_ptr, A.col, A.val, A.rows, A.cols)
+    hd = np.zeros(1)
+    yf, _ = g.gse_spmv_dot(F, x, segments=3, dot=hd)  # host x, y and dot
+    yo = O.spmv_fp64(O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val), x)
+    Fa = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, np.abs(A.val))
+    bound = 1e-12 * O.spmv_fp64(Fa, np.abs(x))
+    assert np.all(np.abs(yf - yo) <= bound)
+    assert abs(hd[0] - x @ yo) <= float(np.abs(x) @ bound) + 1e-13 * float(np.abs(x) @ np.abs(yo))
+
+
 @pytest.mark.parametrize("k", [1, 2, 8, 16, 64])
 def test_spmv_k_sweep_parity(g, k):
     """window kernel (power-law rows): scale tables of 1..64 entries (1-6 EI bits) at all
@@ -489,41 +518,39 @@ def test_cg_parity_c1(g, variant, mode):
     assert rg["converged"] and rg["rel_residual_true"] <= 1e-10
 
 
-@pytest.mark.parametrize("mode", ["stepped_scaled", "fixed3", "fp64"])
-def test_cg_fused_p_update(g, mode, monkeypatch):
-    """opt-in GSE_CG_FUSEP=1 (the p update inside the row-walk SpMV, p double-buffered, the
-    last x update after the graph loop): oracle parity, and for GSE matrices bitwise the
-    solution of the separate-xpay graph (same rounding), across escalations"""
-    A = gi.poisson3d(24, "varcoef")
+@pytest.mark.parametrize("name", ["poisson2d_varcoef", "powerlaw_30k", "random_mixed", "random_wide"])
+def test_perturbation_bounds_bit_exact(g, name):
+    """R29 eta_L = ||A_3 - A_L||_inf: bit-identical to the oracle (row sums in storage order)"""
+    A = MATS[name]()
+    M, R = enc_both(g, A)
+    assert g.gse_perturbation_bounds(M) == O.perturbation_bounds(R)
+    assert g.gse_perturbation_bounds(enc_both(g, gi.poisson3d(12))[0]) == (0.0, 0.0)
+
+
+@pytest.mark.parametrize("solver", ["cg", "gmres"])
+@pytest.mark.parametrize("c", [0.1, 1.0, 1e300])
+def test_perturbation_trigger_parity(g, solver, c):
+    """R29 trigger on the GPU (||x||^2 from the CG's xpay kernel / at the GMRES cycle start)
+    against the oracle: iterations +-2, switch points +-2, residual ratio; the same handle
+    then solves without the trigger exactly as before (graphs rebuilt)"""
+    A = gi.poisson3d(16, "varcoef") if solver == "cg" else gi.convdiff3d(12)
     b = gi.ones_rhs(A)
-    if mode == "fp64":
-        mk = lambda: g.gse_fp64_matrix(A.row_ptr, A.col, A.val, A.rows, A.cols)
-        Rm = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
-        sg, so = None, None
-    else:
-        mk = lambda: g.gse_encode(A.row_ptr, A.col, A.val, A.rows, A.cols)
-        Rm = O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
-        if mode == "fixed3":
-            sg, so = g.fixed_schedule(3), O.fixed_schedule(3)
-        else:
-            sg = g.gse_default_schedule("cg", l=30, t=10, m=10)
-            so = O.schedule("cg", l=30, t=10, m=10)
-    M0 = mk()
-    assert M0.info["spmv_mode"] == 1  # row walk: the fused kernel applies
-    x0, r0 = g.gse_solve_cg(M0, b, tol=1e-10, max_iters=5000, sched=sg)
-    monkeypatch.setenv("GSE_CG_FUSEP", "1")
-    M1 = mk()
-    x1, r1 = g.gse_solve_cg(M1, b, tol=1e-10, max_iters=5000, sched=sg)
-    # a second solve on the same handle reuses the graph (fresh alpha / beta / pending x)
-    x2, r2 = g.gse_solve_cg(M1, b, tol=1e-10, max_iters=5000, sched=sg)
-    xo, ro = O.cg(Rm, b, tol=1e-10, max_iters=5000, sched=so)
-    _cmp_reports(r1, ro)
-    assert r1["converged"] and r1["rel_residual_true"] <= 1e-10
-    assert r1["iterations"] == r2["iterations"] and np.array_equal(x1, x2)
-    if mode != "fp64":
-        assert r1["iterations"] == r0["iterations"]
-        assert r1["switch_iter"] == r0["switch_iter"]
-        assert np.array_equal(x1.view(np.uint64), x0.view(np.uint64))
+    M, R = enc_both(g, A)
+    run_g = g.gse_solve_cg if solver == "cg" else g.gse_solve_gmres
+    run_o = O.cg if solver == "cg" else O.gmres
+    _, r_plain = run_g(M, b, tol=1e-10, sched=g.gse_default_schedule(solver))
+    _, rg = run_g(M, b, tol=1e-10, sched=g.gse_default_schedule(solver, perturb_c=c))
+    _, ro = run_o(R, b, tol=1e-10, sched=O.schedule(solver, perturb_c=c))
+    _cmp_reports(rg, ro)
+    assert rg["n_switches"] == ro.n_switches == 2
+    if c == 1e300:
+        assert rg["switch_iter"] == ro.switch_iter
+    for a_, b_ in zip(rg["switch_iter"], ro.switch_iter):
+        assert abs(a_ - b_) <= 2
+    assert rg["converged"] and rg["rel_residual_true"] <= 1e-10
+    _, r_again = run_g(M, b, tol=1e-10, sched=g.gse_default_schedule(solver))
+    assert (r_again["iterations"], r_again["switch_iter"]) == (r_plain["iterations"],
+                                                               r_plain["switch_iter"])
 
 
 @pytest.mark.parametrize("mode", ["stepped_scaled", "stepped", "fp64"])

@@ -30,6 +30,23 @@ def test_poisson3d_shape_and_row_range(N):
     assert np.array_equal(part.col, A.col[A.row_ptr[5]:A.row_ptr[20]])
 
 
+@pytest.mark.parametrize("variant", ["const", "varcoef"])
+def test_poisson3d_chunks_concatenate_to_the_matrix(variant):
+    """bench.py's chunked C5 generation yields exactly poisson3d's rows"""
+    N = 9
+    A = gi.poisson3d(N, variant)
+    r0, r1 = 2 * N * N + 5, A.rows - 7
+    parts = list(gi.poisson3d_chunks(N, variant, r0, r1, planes=2, workers=3))
+    assert [p[0] for p in parts] == sorted(p[0] for p in parts) and parts[0][0] == r0
+    assert sum(p[1].rows for p in parts) == r1 - r0
+    col = np.concatenate([p[1].col for p in parts])
+    val = np.concatenate([p[1].val for p in parts])
+    s, e = A.row_ptr[r0], A.row_ptr[r1]
+    assert np.array_equal(col, A.col[s:e]) and np.array_equal(val, A.val[s:e])
+    lens = np.concatenate([np.diff(p[1].row_ptr) for p in parts])
+    assert np.array_equal(lens, np.diff(A.row_ptr)[r0:r1])
+
+
 def test_c2_c5_sizes_by_formula():
     # 7-point stencil nnz = 7 N^3 - 6 N^2 (SURVEY 8(a): 14,581,760 and 937,951,232)
     assert 7 * 128 ** 3 - 6 * 128 ** 2 == 14581760
