@@ -102,7 +102,14 @@ int orc_build_table_emax(const uint64_t* hist, int k_max, int e_max_true, uint16
   int take = n < k_max ? n : k_max;
   int have_max = 0;
   for (int i = 0; i < take; ++i) have_max |= (es[i] == e_max);
-  if (!have_max) es[take - 1] = e_max;
+  /* R27b: a free slot (fewer than k_max sampled exponents) takes e_max; otherwise it
+   * replaces the least frequent selected entry (R5) */
+  if (!have_max) {
+    if (take < k_max)
+      es[take++] = e_max;
+    else
+      es[take - 1] = e_max;
+  }
   for (int i = 0; i < take; ++i) table[i] = (uint16_t)(es[i] + 1);
   *table_len = take;
   return ORC_OK;
@@ -786,7 +793,10 @@ int orc_cg(const orc_matrix* A, const double* b, double* x, double tol, int64_t 
   if (resid <= tol) {
     if (!(stepped && level < 3 && sched->verify_at_full)) { status = ORC_OK; goto out; }
     if (true_resid(A, 3, b, x, q, bnorm, rep) <= tol) { status = ORC_OK; goto out; }
-    level = 3; /* x0 already converged at A_L but not at A: finish at full precision */
+    /* x0 already converged at A_L but not at A: finish at the highest allowed level (R16;
+     * capped by max_level: no higher level allowed -> not converged) */
+    if (level >= sched->max_level) { status = ORC_NOT_CONVERGED; goto out; }
+    level = sched->max_level;
     log_switch(rep, 0, level);
     orc_apply(A, level, x, q);
     rep->spmv_count[level - 1]++;
@@ -815,7 +825,9 @@ int orc_cg(const orc_matrix* A, const double* b, double* x, double tol, int64_t 
     if (resid <= tol) {
       if (!(stepped && level < 3 && sched->verify_at_full)) { status = ORC_OK; break; }
       if (true_resid(A, 3, b, x, q, bnorm, rep) <= tol) { status = ORC_OK; break; }
-      escalate = 1; /* R16: converged at A_L but not at A -> one level up */
+      /* R16: converged at A_L but not at A -> one level up, within max_level */
+      if (level >= sched->max_level) { status = ORC_NOT_CONVERGED; break; }
+      escalate = 1;
     } else if (stepped && monitor_check(sched, &ring, wbuf, j, level, resid, eta, xx, bnorm)) {
       escalate = 1;
     }
@@ -918,6 +930,7 @@ int orc_gmres(const orc_matrix* A, const double* b, double* x, double tol, int r
       if (stepped && level < 3 && sched->verify_at_full) {
         double rt = true_resid(A, 3, b, x, w, bnorm, rep);
         if (rt <= tol) { status = ORC_OK; break; }
+        if (level >= sched->max_level) { status = ORC_NOT_CONVERGED; break; } /* capped */
         level++;
         log_switch(rep, jg, level);
         continue; /* restart with an explicit residual at the new level */

@@ -113,7 +113,8 @@ def test_sampled_histogram_is_the_sampled_rows(seed, B):
 @pytest.mark.parametrize("seed", range(30))
 def test_table_emax_brute_force(seed):
     """selection on a sample with the TRUE e_max forced: maximal sample coverage among
-    subsets of size min(k, #distinct sampled) containing e_max_true"""
+    subsets containing e_max_true of size min(k, #distinct sampled), or one more when e_max
+    was not sampled and a slot is free (R27b)"""
     rng = np.random.default_rng(seed)
     nd = int(rng.integers(1, 7))
     exps = rng.choice(np.arange(1, 2000), nd, replace=False)
@@ -125,11 +126,22 @@ def test_table_emax_brute_force(seed):
     k = int(rng.choice([1, 2, 4]))
     table = [int(t) for t in O.build_table_emax(hist, k, e_true)]
     sel = [t - 1 for t in table]
-    assert e_true in sel and len(set(sel)) == len(sel) == min(k, nd)
+    sampled_max = e_true in set(int(e) for e in exps)
+    size = min(k, nd) if (sampled_max or nd >= k) else nd + 1
+    assert e_true in sel and len(set(sel)) == len(sel) == size
     pool = sorted(set(int(e) for e in exps) | {e_true})
     best = max(sum(int(hist[e]) for e in c) for c in itertools.combinations(pool, len(sel))
                if e_true in c)
     assert sum(int(hist[e]) for e in sel) == best
+
+
+def test_free_slot_takes_the_true_max():
+    """R27b (advisor finding): a sample {1023} with the true e_max 1030 and k = 8 keeps the
+    sampled class and appends 1031 instead of overwriting it"""
+    hist = np.zeros(2048, np.uint64)
+    hist[1023] = 5
+    assert list(O.build_table_emax(hist, 8, 1030)) == [1024, 1031]
+    assert list(O.build_table_emax(hist, 1, 1030)) == [1031]
 
 
 def test_empty_sample_gives_forced_entry_only():

@@ -470,3 +470,21 @@ def test_gmres30_iteration_gauges(N, gauge):
     spla.gmres(S, b, rtol=1e-10, atol=0.0, restart=30, maxiter=1000,
                callback=lambda pr: its.append(1), callback_type="pr_norm")
     assert abs(len(its) - rep.iterations) <= 3
+
+
+@pytest.mark.parametrize("solver", ["cg", "gmres"])
+def test_verify_respects_max_level(solver):
+    """R16 within max_level (advisor finding): a schedule capped at level 2 on a head-lossy
+    matrix never runs at level 3; when the level-2 recurrence converges but A_3's residual
+    does not, the solve reports NOT_CONVERGED (it may not escalate) -- unless level 2 alone
+    reaches tol against A_3."""
+    A = gi.poisson2d(16, "varcoef") if solver == "cg" else gi.convdiff3d(8)
+    b = gi.ones_rhs(A)
+    G = enc(A)
+    run = O.cg if solver == "cg" else O.gmres
+    _, r1 = run(G, b, tol=1e-10, sched=O.schedule(solver, max_level=1))
+    assert r1.status == O.NOT_CONVERGED and r1.n_switches == 0 and r1.iters_per_level[1:] == (0, 0)
+    assert r1.rel_residual_true > 1e-10
+    _, r2 = run(G, b, tol=1e-13, sched=O.schedule(solver, max_level=2))
+    assert r2.iters_per_level[2] == 0 and max(r2.switch_to_level, default=1) <= 2
+    assert r2.status == (O.OK if r2.rel_residual_true <= 1e-13 else O.NOT_CONVERGED)
