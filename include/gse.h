@@ -278,7 +278,11 @@ const char* gse_status_string(gse_status s);
 const char* gse_last_error_detail(void);
 
 /* Route library device allocations (planes, workspaces) through a caller allocator, e.g.
- * torch's caching allocator.  NULL alloc restores cudaMallocAsync / cudaFreeAsync. */
+ * torch's caching allocator.  NULL alloc restores cudaMallocAsync / cudaFreeAsync.  The
+ * allocator must return 256-byte aligned device memory (cudaMalloc's guarantee: the SpMV
+ * kernels stage planes with TMA bulk copies); a misaligned block is handed back to free_
+ * and the calling entry point fails with GSE_ERR_OOM and a detail message.  A size may be
+ * rounded up to a multiple of 256 bytes. */
 gse_status gse_set_allocator(void* (*alloc)(size_t bytes, void* stream, void* ctx),
                              void (*free_)(void* ptr, void* stream, void* ctx), void* ctx);
 

@@ -20,6 +20,11 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "gse_oracle.c")
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
+# ORACLE_SANITIZE=1: an ASan + UBSan build (scripts/oracle_sanitize.sh; run with libasan
+# preloaded) in a separate file, so the normal build is untouched
+_SANITIZE = os.environ.get("ORACLE_SANITIZE") == "1"
+if _SANITIZE:
+    _LIB_PATH = os.path.join(_HERE, "liboracle_san.so")
 
 OK, NOT_CONVERGED, NUMERICAL_ABORT = 0, 2, 3
 ERR_INVALID_ARG, ERR_DIM, ERR_NONFINITE, ERR_NO_VALUES = 10, 11, 12, 13
@@ -32,9 +37,11 @@ def build(force: bool = False) -> str:
         os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "gse_oracle.h"))
     ):
         tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        san = ["-fsanitize=address,undefined", "-fno-sanitize-recover=undefined",
+               "-fno-omit-frame-pointer", "-g"] if _SANITIZE else []
         subprocess.check_call(
             ["gcc", "-std=c99", "-O2", "-fPIC", "-ffp-contract=off", "-fno-fast-math",
-             "-fopenmp", "-shared", "-o", tmp, _SRC, "-lm"]
+             "-fopenmp", *san, "-shared", "-o", tmp, _SRC, "-lm"]
         )
         os.replace(tmp, _LIB_PATH)
     return _LIB_PATH

@@ -124,6 +124,7 @@ def _declare(L):
     L.gse_last_error_detail.argtypes = []
     L.gse_last_error_detail.restype = C.c_char_p
     L.gse_nccl_unique_id.argtypes = [vp]
+    L.gse_set_allocator.argtypes = [vp, vp, vp]
     L.gse_dist_create.argtypes = [vp, i32, i32, i32, C.POINTER(vp)]
     L.gse_dist_thread_group_create.argtypes = [i32, C.POINTER(vp)]
     L.gse_dist_thread_group_free.argtypes = [vp]
@@ -487,6 +488,41 @@ def gse_decode_vector16(words, table, ei_bits: int = 3, stream=None):
                                     ei_bits, _addr(out), _stream(words, stream=stream)),
            "gse_decode_vector16")
     return out
+
+
+_ALLOC_T = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+_FREE_T = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
+_alloc_keep = None  # the installed ctypes callbacks must outlive every allocation
+
+
+def gse_set_allocator(alloc=None, free=None):
+    """Route the library's device allocations through Python callables alloc(bytes,
+    stream) -> int pointer and free(ptr, stream) (both None: back to cudaMallocAsync)."""
+    global _alloc_keep
+    if (alloc is None) != (free is None):
+        raise ValueError("alloc and free must both be set or both be None")
+    if alloc is None:
+        _check(_lib.gse_set_allocator(None, None, None), "gse_set_allocator")
+        _alloc_keep = None
+        return
+    a = _ALLOC_T(lambda nbytes, stream, ctx: alloc(int(nbytes), stream) or None)
+    f = _FREE_T(lambda ptr, stream, ctx: free(int(ptr), stream))
+    _check(_lib.gse_set_allocator(C.cast(a, C.c_void_p), C.cast(f, C.c_void_p), None),
+           "gse_set_allocator")
+    _alloc_keep = (a, f)
+
+
+def torch_allocator():
+    """(alloc, free) callables over torch's caching allocator, for gse_set_allocator."""
+    import torch
+
+    def alloc(nbytes, stream):
+        return torch.cuda.caching_allocator_alloc(nbytes, stream=stream or 0)
+
+    def free(ptr, stream):
+        torch.cuda.caching_allocator_delete(ptr)
+
+    return alloc, free
 
 
 def gse_matrix_free(A: Matrix):

@@ -44,7 +44,20 @@ static void keep_pool_cached() {
 void* dev_alloc(size_t bytes, cudaStream_t s) {
   if (bytes == 0) bytes = 16;
   bytes = (bytes + 255) & ~(size_t)255;
-  if (g_alloc) return g_alloc(bytes, (void*)s, g_ctx);
+  if (g_alloc) {
+    void* p = g_alloc(bytes, (void*)s, g_ctx);
+    if (!p) {
+      set_error("the caller allocator returned NULL for " + std::to_string(bytes) + " bytes");
+      return nullptr;
+    }
+    // TMA bulk copies and 16-byte vector loads of the planes need aligned bases
+    if (reinterpret_cast<uintptr_t>(p) & 255u) {
+      g_free(p, (void*)s, g_ctx);
+      set_error("the caller allocator must return 256-byte aligned memory (as cudaMalloc does)");
+      return nullptr;
+    }
+    return p;
+  }
   keep_pool_cached();
   void* p = nullptr;
   if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) {
@@ -208,7 +221,7 @@ static void destroy_matrix(Matrix& M) {
 
 gse_status create_from_csr(const gse_csr_f64* A, int kind, int k_max, int device,
                            gse_matrix* out, cudaStream_t s, Matrix** mout, Comm* comm,
-                           const int32_t* local_col_host, int64_t sample_block_rows,
+                           const int32_t* local_col, int64_t sample_block_rows,
                            uint64_t sample_seed, int shard_table) {
   gse_status rc = check_csr(A);
   if (rc != GSE_OK) return rc;
@@ -228,7 +241,7 @@ gse_status create_from_csr(const gse_csr_f64* A, int kind, int k_max, int device
   else
     rc = st.in((const int*)A->row_ptr, (size_t)A->rows + 1, dev, (const int**)&rp);
   if (rc == GSE_OK)
-    rc = st.in(local_col_host ? local_col_host : A->col_idx, (size_t)A->nnz, dev, &col);
+    rc = st.in(local_col ? local_col : A->col_idx, (size_t)A->nnz, dev, &col);
   if (rc == GSE_OK) rc = st.in(A->values, (size_t)A->nnz, dev, &val);
   if (rc != GSE_OK) return rc;
   gse_matrix h = new gse_matrix_s();

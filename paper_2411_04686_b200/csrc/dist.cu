@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "gse_internal.cuh"
+#include "scan.cuh"
 
 namespace gse {
 
@@ -332,28 +333,19 @@ struct DistCtx {
   unsigned* part_ticket = nullptr;
 };
 
-// first row / end of the longest run of rows whose columns are all owned (< n_local),
-// aligned inward to 64 rows; empty when shorter than max(4096, n_local / 8)
-static void interior_range(int64_t n_local, const std::vector<int64_t>& rp,
-                           const std::vector<int32_t>& local_col, int64_t* i0, int64_t* i1) {
-  int64_t best0 = 0, best1 = 0, run0 = 0;
-  for (int64_t r = 0; r <= n_local; ++r) {
-    bool interior = false;
-    if (r < n_local) {
-      interior = true;
-      for (int64_t j = rp[r]; j < rp[r + 1]; ++j)
-        if (local_col[(size_t)j] >= n_local) {
-          interior = false;
-          break;
-        }
+// first row / end of the longest run of rows whose columns are all owned (< n_local), given
+// the ascending list of the rows that read halo columns; aligned inward to 64 rows; empty
+// when shorter than max(4096, n_local / 8)
+static void interior_from_halo_rows(int64_t n_local, const std::vector<uint32_t>& hrows,
+                                    int64_t* i0, int64_t* i1) {
+  int64_t best0 = 0, best1 = 0, prev = -1;
+  for (size_t k = 0; k <= hrows.size(); ++k) {
+    const int64_t r = k < hrows.size() ? (int64_t)hrows[k] : n_local;
+    if (r - (prev + 1) > best1 - best0) {
+      best0 = prev + 1;
+      best1 = r;
     }
-    if (!interior) {
-      if (r - run0 > best1 - best0) {
-        best0 = run0;
-        best1 = r;
-      }
-      run0 = r + 1;
-    }
+    prev = r;
   }
   int64_t a = (best0 + 63) / 64 * 64, b = best1 / 64 * 64;
   const int64_t min_len = n_local / 8 > 4096 ? n_local / 8 : 4096;
@@ -370,6 +362,124 @@ __global__ void k_add_parts(const double* a, const double* b, const double* c, i
     if (use_c) s += *c;
     *out = s;
   }
+}
+
+static int plan_grid(int64_t n, int dev) {
+  int64_t g = (n + 255) / 256;
+  const int64_t cap = (int64_t)num_sms(dev) * 8;
+  if (g > cap) g = cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+// ---------------------------------------------------------------- plan (device)
+// The local renumbering of gse_encode_dist on the GPU (the host version build_plan_host is
+// kept for gse_dist_plan and the CPU tests): a bitmap over the GLOBAL columns marks the
+// non-owned columns the rank references; its set bits in ascending order ARE the sorted,
+// duplicate-free halo list, and a column's halo position is the number of set bits before
+// it (per-word exclusive prefix + popcount).  C5 at P = 2: 469M columns renumbered without
+// leaving the device (the host loops took seconds per encode).
+constexpr int PLAN_THREADS = 256, PLAN_ITEMS = 16, PLAN_TILE = PLAN_THREADS * PLAN_ITEMS;
+
+__global__ void k_plan_mark(const int32_t* __restrict__ col, int64_t nnz, int64_t rb,
+                            int64_t re, int64_t gcols, uint32_t* __restrict__ bm,
+                            unsigned long long* __restrict__ bad) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += stride) {
+    const int64_t c = col[i];
+    if (c < 0 || c >= gcols) {
+      atomicMin(bad, (unsigned long long)i);
+    } else if (c < rb || c >= re) {
+      const uint32_t b = 1u << (c & 31);
+      if (!(bm[c >> 5] & b)) atomicOr(&bm[c >> 5], b);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(PLAN_THREADS) k_plan_bcount(const uint32_t* __restrict__ bm,
+                                                              int64_t nw,
+                                                              uint32_t* __restrict__ bcnt) {
+  const int64_t base = (int64_t)blockIdx.x * PLAN_TILE + (int64_t)threadIdx.x * PLAN_ITEMS;
+  uint32_t c = 0;
+  for (int i = 0; i < PLAN_ITEMS; ++i) c += base + i < nw ? __popc(bm[base + i]) : 0u;
+  uint32_t tot;
+  block_excl_scan(c, &tot);
+  if (threadIdx.x == 0) bcnt[blockIdx.x] = tot;
+}
+
+// per-word exclusive prefix of the set bits, and the halo list (ascending columns)
+__global__ void __launch_bounds__(PLAN_THREADS) k_plan_words(const uint32_t* __restrict__ bm,
+                                                             int64_t nw,
+                                                             const uint32_t* __restrict__ boff,
+                                                             uint32_t* __restrict__ wpre,
+                                                             int32_t* __restrict__ halo) {
+  const int64_t base = (int64_t)blockIdx.x * PLAN_TILE + (int64_t)threadIdx.x * PLAN_ITEMS;
+  uint32_t c = 0;
+  for (int i = 0; i < PLAN_ITEMS; ++i) c += base + i < nw ? __popc(bm[base + i]) : 0u;
+  uint32_t tot;
+  uint32_t o = boff[blockIdx.x] + block_excl_scan(c, &tot);
+  for (int i = 0; i < PLAN_ITEMS && base + i < nw; ++i) {
+    uint32_t w = bm[base + i];
+    wpre[base + i] = o;
+    while (w) {
+      const int b = __ffs(w) - 1;
+      halo[o++] = (int32_t)((base + i) * 32 + b);
+      w &= w - 1u;
+    }
+  }
+}
+
+__global__ void k_plan_renumber(const int32_t* __restrict__ col, int64_t nnz, int64_t rb,
+                                int64_t re, int64_t n_local, const uint32_t* __restrict__ bm,
+                                const uint32_t* __restrict__ wpre,
+                                int32_t* __restrict__ local_col) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += stride) {
+    const int64_t c = col[i];
+    if (c >= rb && c < re) {
+      local_col[i] = (int32_t)(c - rb);
+    } else {
+      const uint32_t below = bm[c >> 5] & ((1u << (c & 31)) - 1u);
+      local_col[i] = (int32_t)(n_local + wpre[c >> 5] + __popc(below));
+    }
+  }
+}
+
+// 1 for rows that read a halo column (local id >= n_local)
+template <class RP>
+__global__ void k_plan_rowflag(const RP* __restrict__ rp, int64_t n_local,
+                               const int32_t* __restrict__ local_col, uint8_t* __restrict__ f) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n_local; r += stride) {
+    uint8_t h = 0;
+    for (int64_t j = rp[r]; j < rp[r + 1]; ++j)
+      if (local_col[j] >= n_local) {
+        h = 1;
+        break;
+      }
+    f[r] = h;
+  }
+}
+
+// a device view of a caller array (host arrays are copied; *owned is then freed by the caller)
+template <class T>
+static gse_status device_view(const T* p, size_t n, int dev, cudaStream_t s, const T** out,
+                              void** owned) {
+  *owned = nullptr;
+  int d = -1;
+  if (n == 0 || p == nullptr || is_device_ptr(p, &d)) {
+    if (p && n && d != dev) {
+      set_error("device array lives on another device than the rank's");
+      return GSE_ERR_INVALID_ARG;
+    }
+    *out = p;
+    return GSE_OK;
+  }
+  T* b = static_cast<T*>(dev_alloc(n * sizeof(T), s));
+  if (!b) return GSE_ERR_OOM;
+  GSE_CUDA_TRY(cudaMemcpyAsync(b, p, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  *owned = b;
+  *out = b;
+  return GSE_OK;
 }
 
 }  // namespace gse
@@ -432,6 +542,14 @@ gse_status dist_spmv(const Matrix& M, int level, double* xe, double* y, const Do
     GSE_CUDA_TRY(cudaGetLastError());
   }
   return GSE_OK;
+}
+
+bool dist_capturable(const Matrix& M) {
+  static const bool off = [] {
+    const char* e = getenv("GSE_DIST_NO_GRAPH");
+    return e && e[0] == '1';
+  }();
+  return M.dist && !off && dynamic_cast<NcclComm*>(M.dist->comm) != nullptr;
 }
 
 gse_status dist_allreduce_sum(const Matrix& M, double* d_vals, int count, cudaStream_t s) {
@@ -663,21 +781,62 @@ gse_status gse_encode_dist(gse_dist Dh, const gse_csr_f64* A, int64_t row_begin,
     set_error("row blocks do not cover [0, global_rows)");
     return GSE_ERR_DIM_MISMATCH;
   }
-  // columns to the host, local renumbering + halo plan
-  std::vector<int32_t> col_h((size_t)A->nnz), local_col((size_t)A->nnz);
-  if (A->nnz) {
-    GSE_CUDA_TRY(cudaMemcpyAsync(col_h.data(), A->col_idx, 4 * (size_t)A->nnz, cudaMemcpyDefault, s));
-    GSE_CUDA_TRY(cudaStreamSynchronize(s));
-  }
-  for (int64_t i = 0; i < A->nnz; ++i)
-    if (col_h[i] < 0 || col_h[i] >= global_rows) {
-      set_error("column index out of range");
-      return GSE_ERR_INVALID_ARG;
-    }
-  std::vector<int64_t> halo, recv_cnt;
-  st = build_plan_host(A->nnz, col_h.data(), row_begin, n_local, comm->nranks, rank_rows.data(),
-                       local_col.data(), halo, recv_cnt);
+  // local renumbering + halo plan on the device (k_plan_*); only the halo list comes back
+  const int32_t* dcol = nullptr;
+  void* col_owned = nullptr;
+  st = device_view(A->col_idx, (size_t)A->nnz, comm->device, s, &dcol, &col_owned);
   if (st != GSE_OK) return st;
+  const int64_t nw = (global_rows + 31) / 32 + 1;
+  const int64_t nbw = (nw + PLAN_TILE - 1) / PLAN_TILE;
+  uint32_t* bm = dev_alloc_n<uint32_t>((size_t)nw, s);
+  uint32_t* wpre = dev_alloc_n<uint32_t>((size_t)nw, s);
+  uint32_t* bcnt = dev_alloc_n<uint32_t>((size_t)nbw + 1, s);
+  unsigned long long* dbad = dev_alloc_n<unsigned long long>(1, s);
+  int* dnh = dev_alloc_n<int>(1, s);
+  int32_t* d_local_col = dev_alloc_n<int32_t>((size_t)A->nnz + 1, s);
+  if (!bm || !wpre || !bcnt || !dbad || !dnh || !d_local_col) return GSE_ERR_OOM;
+  GSE_CUDA_TRY(cudaMemsetAsync(bm, 0, 4 * (size_t)nw, s));
+  GSE_CUDA_TRY(cudaMemsetAsync(dbad, 0xFF, 8, s));
+  const int gsz = plan_grid(A->nnz, comm->device);
+  if (A->nnz)
+    k_plan_mark<<<gsz, 256, 0, s>>>(dcol, A->nnz, row_begin, row_begin + n_local, global_rows, bm,
+                                    dbad);
+  k_plan_bcount<<<(unsigned)nbw, PLAN_THREADS, 0, s>>>(bm, nw, bcnt);
+  k_cmp_scan<<<1, 1024, 0, s>>>(bcnt, nbw, dnh);
+  int nh_bad[3] = {0, 0, 0};
+  unsigned long long badi = 0;
+  GSE_CUDA_TRY(cudaMemcpyAsync(&nh_bad[0], dnh, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GSE_CUDA_TRY(cudaMemcpyAsync(&badi, dbad, 8, cudaMemcpyDeviceToHost, s));
+  GSE_CUDA_TRY(cudaStreamSynchronize(s));
+  if (badi != ~0ull) {
+    set_error("column index out of range at non-zero " + std::to_string(badi));
+    return GSE_ERR_INVALID_ARG;
+  }
+  const int64_t n_halo = nh_bad[0];
+  if (n_halo + n_local >= (1LL << 31)) {
+    set_error("local column space exceeds 2^31");
+    return GSE_ERR_INVALID_ARG;
+  }
+  int32_t* d_halo = dev_alloc_n<int32_t>((size_t)n_halo + 1, s);
+  if (!d_halo) return GSE_ERR_OOM;
+  k_plan_words<<<(unsigned)nbw, PLAN_THREADS, 0, s>>>(bm, nw, bcnt, wpre, d_halo);
+  if (A->nnz)
+    k_plan_renumber<<<gsz, 256, 0, s>>>(dcol, A->nnz, row_begin, row_begin + n_local, n_local, bm,
+                                        wpre, d_local_col);
+  GSE_CUDA_TRY(cudaGetLastError());
+  std::vector<int32_t> halo32((size_t)n_halo);
+  if (n_halo)
+    GSE_CUDA_TRY(cudaMemcpyAsync(halo32.data(), d_halo, 4 * (size_t)n_halo, cudaMemcpyDeviceToHost, s));
+  GSE_CUDA_TRY(cudaStreamSynchronize(s));
+  for (void* q : {(void*)bm, (void*)wpre, (void*)bcnt, (void*)dbad, (void*)d_halo}) dev_free(q, s);
+  std::vector<int64_t> halo(halo32.begin(), halo32.end()), recv_cnt(comm->nranks, 0);
+  {
+    int owner = 0;
+    for (int64_t c : halo) {
+      while (owner < comm->nranks - 1 && c >= rank_rows[owner + 1]) ++owner;
+      recv_cnt[owner]++;
+    }
+  }
   // tell every owner which of its entries this rank needs
   std::vector<std::vector<int64_t>> want(comm->nranks), give;
   {
@@ -696,7 +855,7 @@ gse_status gse_encode_dist(gse_dist Dh, const gse_csr_f64* A, int64_t row_begin,
   if (opts) o = *opts;
   o.device = comm->device;
   Matrix* M = nullptr;
-  st = create_from_csr(&L, GSE_KIND_GSE, o.k_max, o.device, out, s, &M, comm, local_col.data(),
+  st = create_from_csr(&L, GSE_KIND_GSE, o.k_max, o.device, out, s, &M, comm, d_local_col,
                        0, 0, o.per_shard_table ? 1 : 0);
   if (st != GSE_OK) return st;
   DistCtx* D = new DistCtx();
@@ -738,17 +897,38 @@ gse_status gse_encode_dist(gse_dist Dh, const gse_csr_f64* A, int64_t row_begin,
   // halo / interior overlap for row-walk matrices (local decision: every rank issues the
   // same collectives either way)
   if (M->spmv_mode == SPMV_RW && n_local > 0 && !getenv("GSE_NO_OVERLAP")) {
-    std::vector<int64_t> rp_h((size_t)n_local + 1);
-    if (A->row_ptr_64) {
-      GSE_CUDA_TRY(cudaMemcpyAsync(rp_h.data(), A->row_ptr, 8 * rp_h.size(), cudaMemcpyDefault, s));
-    } else {
-      std::vector<int32_t> t(rp_h.size());
-      GSE_CUDA_TRY(cudaMemcpyAsync(t.data(), A->row_ptr, 4 * t.size(), cudaMemcpyDefault, s));
-      GSE_CUDA_TRY(cudaStreamSynchronize(s));
-      for (size_t i = 0; i < t.size(); ++i) rp_h[i] = t[i];
-    }
+    // rows reading halo columns, compacted on the device; the longest run between them is
+    // the interior (host, on the short list)
+    const void* drp = nullptr;
+    void* rp_owned = nullptr;
+    if (A->row_ptr_64)
+      st = device_view((const long long*)A->row_ptr, (size_t)n_local + 1, comm->device, s,
+                       (const long long**)&drp, &rp_owned);
+    else
+      st = device_view((const int*)A->row_ptr, (size_t)n_local + 1, comm->device, s,
+                       (const int**)&drp, &rp_owned);
+    if (st != GSE_OK) return st;
+    uint8_t* rf = dev_alloc_n<uint8_t>((size_t)n_local, s);
+    uint32_t* hr = dev_alloc_n<uint32_t>((size_t)n_local + 1, s);
+    int* dcnt = dev_alloc_n<int>(1, s);
+    if (!rf || !hr || !dcnt) return GSE_ERR_OOM;
+    const int gr = plan_grid(n_local, comm->device);
+    if (A->row_ptr_64)
+      k_plan_rowflag<<<gr, 256, 0, s>>>((const long long*)drp, n_local, d_local_col, rf);
+    else
+      k_plan_rowflag<<<gr, 256, 0, s>>>((const int*)drp, n_local, d_local_col, rf);
+    GSE_CUDA_TRY(cudaGetLastError());
+    st = compact_flags(rf, n_local, hr, dcnt, s);
+    if (st != GSE_OK) return st;
+    int nhr = 0;
+    GSE_CUDA_TRY(cudaMemcpyAsync(&nhr, dcnt, sizeof(int), cudaMemcpyDeviceToHost, s));
     GSE_CUDA_TRY(cudaStreamSynchronize(s));
-    interior_range(n_local, rp_h, local_col, &D->ov_i0, &D->ov_i1);
+    std::vector<uint32_t> hrows((size_t)nhr);
+    if (nhr)
+      GSE_CUDA_TRY(cudaMemcpyAsync(hrows.data(), hr, 4 * (size_t)nhr, cudaMemcpyDeviceToHost, s));
+    GSE_CUDA_TRY(cudaStreamSynchronize(s));
+    for (void* q : {(void*)rf, (void*)hr, (void*)dcnt, rp_owned}) dev_free(q, s);
+    interior_from_halo_rows(n_local, hrows, &D->ov_i0, &D->ov_i1);
     if (D->ov_i1 > D->ov_i0) {
       const int np = 2048;  // partials per part (>= any persistent SpMV grid)
       D->part_buf = dev_alloc_n<double>((size_t)3 * (np + 1), s);
@@ -767,6 +947,9 @@ gse_status gse_encode_dist(gse_dist Dh, const gse_csr_f64* A, int64_t row_begin,
       D->overlap = true;
     }
   }
+  GSE_CUDA_TRY(cudaStreamSynchronize(s));
+  dev_free(d_local_col, s);
+  dev_free(col_owned, s);
   GSE_CUDA_TRY(cudaStreamSynchronize(s));
   return GSE_OK;
 }

@@ -233,6 +233,10 @@ gse_status dist_halo_exchange(const Matrix& M, double* x_local_ext, cudaStream_t
 gse_status dist_spmv(const Matrix& M, int level, double* x_ext, double* y, const DotOut* dot,
                      cudaStream_t s, const int* stop);
 gse_status dist_allreduce_sum(const Matrix& M, double* d_vals, int count, cudaStream_t s);
+// the distributed CG iteration batch can be captured in a CUDA graph: NCCL backend (its
+// collectives are stream-capturable), not the thread backend (host barriers);
+// GSE_DIST_NO_GRAPH=1 keeps the host-driven batches
+bool dist_capturable(const Matrix& M);
 gse_status comm_allreduce_u64(Comm* c, unsigned long long* d, int count, cudaStream_t s);
 gse_status comm_any(Comm* c, int local_flag, int* any);  // host: OR over ranks
 double* dist_xext(const Matrix& M);
@@ -241,7 +245,7 @@ int64_t dist_n_local(const Matrix& M);
 void free_dist(Matrix& M);
 gse_status create_from_csr(const gse_csr_f64* A, int kind, int k_max, int device,
                            gse_matrix* out, cudaStream_t s, Matrix** mout, Comm* comm,
-                           const int32_t* local_col_host, int64_t sample_block_rows = 0,
+                           const int32_t* local_col, int64_t sample_block_rows = 0,
                            uint64_t sample_seed = 0, int shard_table = 0);
 
 }  // namespace gse

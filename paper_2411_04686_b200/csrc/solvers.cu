@@ -88,6 +88,9 @@ struct SolverWs {
   cudaGraphExec_t cg_exec[3] = {nullptr, nullptr, nullptr};
   cudaGraph_t cg_graph[3] = {nullptr, nullptr, nullptr};
   cudaGraphExec_t gm_exec[3] = {nullptr, nullptr, nullptr};
+  // distributed CG (NCCL backend): one captured batch of DIST_BATCH iterations per level
+  cudaGraphExec_t dcg_exec[3] = {nullptr, nullptr, nullptr};
+  cudaGraph_t dcg_graph[3] = {nullptr, nullptr, nullptr};
   cudaGraph_t gm_graph[3] = {nullptr, nullptr, nullptr};
   int gm_restart = 0;
   int cg_xx = 0;  // the CG graphs compute ||x||^2 in k_cg_xpay (R29 trigger on)
@@ -1325,6 +1328,8 @@ void free_solver_ws(Matrix& M) {
     if (ws->cg_graph[L]) cudaGraphDestroy(ws->cg_graph[L]);
     if (ws->gm_exec[L]) cudaGraphExecDestroy(ws->gm_exec[L]);
     if (ws->gm_graph[L]) cudaGraphDestroy(ws->gm_graph[L]);
+    if (ws->dcg_exec[L]) cudaGraphExecDestroy(ws->dcg_exec[L]);
+    if (ws->dcg_graph[L]) cudaGraphDestroy(ws->dcg_graph[L]);
   }
   for (double* p : {ws->x, ws->r, ws->p, ws->q, ws->b, ws->tmp, ws->V, ws->partials,
                     ws->ring, ws->vcur})
@@ -1400,6 +1405,52 @@ static void drop_cg_graphs(SolverWs* ws) {
     ws->cg_exec[L] = nullptr;
     ws->cg_graph[L] = nullptr;
   }
+}
+
+// ---------------------------------------------------------------- distributed CG batch
+// One distributed CG iteration (every rank issues the same collectives): halo of p + SpMV
+// (interior rows overlapped with the exchange) + local p.q, allreduce, update + local r.r,
+// allreduce, the event logic on the global sums, x / p update.  After an event every kernel
+// returns at once and the collectives sum values nobody reads (all ranks stop together).
+constexpr int DIST_BATCH = 16;
+static gse_status dist_cg_iteration(Matrix& M, int level, cudaStream_t s) {
+  SolverWs* ws = M.ws;
+  const int64_t n = M.rows;
+  DotOut d = dot_to(ws, &ws->ctrl->pq);
+  gse_status rc = dist_spmv(M, level, ws->p, ws->q, &d, s, &ws->ctrl->event);
+  if (rc != GSE_OK) return rc;
+  rc = dist_allreduce_sum(M, &ws->ctrl->pq, 1, s);
+  if (rc != GSE_OK) return rc;
+  launch_k(k_cg_update, ws->vgrid, 256, 0, s, ws->ctrl, ws->ring, ws->r, ws->q, n, ws->partials,
+           ws->ticket, 0, 0, 1);
+  rc = dist_allreduce_sum(M, &ws->ctrl->rr_part, 1, s);
+  if (rc != GSE_OK) return rc;
+  launch_k(k_cg_events, 1, 32, 0, s, ws->ctrl, ws->ring);
+  launch_xpay(ws, s, n);
+  GSE_CUDA_TRY(cudaGetLastError());
+  return GSE_OK;
+}
+
+// NCCL backend: the batch captured once per level as a CUDA graph (NCCL grouped send/recv,
+// the two 8-byte allreduces, the side-stream interior SpMV and the kernels), replayed with
+// one launch per DIST_BATCH iterations instead of ~8 launches + 2 collectives per iteration
+static gse_status build_dist_cg_graph(Matrix& M, int level) {
+  SolverWs* ws = M.ws;
+  if (ws->dcg_exec[level - 1]) return GSE_OK;
+  cudaStream_t cs = ws->cap_stream;
+  GSE_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+  gse_status rc = GSE_OK;
+  for (int it = 0; it < DIST_BATCH && rc == GSE_OK; ++it) rc = dist_cg_iteration(M, level, cs);
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(cs, &g);
+  if (rc != GSE_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  GSE_CUDA_TRY(e);
+  GSE_CUDA_TRY(cudaGraphInstantiate(&ws->dcg_exec[level - 1], g, 0));
+  ws->dcg_graph[level - 1] = g;
+  return GSE_OK;
 }
 
 // ---------------------------------------------------------------- CG graph per level
@@ -1568,8 +1619,11 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
       if (rt <= tol) {
         status = GSE_OK;
         done = true;
+      } else if (level >= sched.max_level) {  // R16 capped by max_level: not converged
+        status = GSE_NOT_CONVERGED;
+        done = true;
       } else {
-        level = 3;
+        level = sched.max_level;  // x0 converged at A_L only: the highest allowed level
         log_switch(rep, 0, level);
         rc = residual(M, level, ws->x, ws->r, ws->p, &ws->ctrl->rr, rep, s);
         if (rc != GSE_OK) return rc;
@@ -1601,23 +1655,21 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
       break;
     }
     if (dist) {
-      // distributed: host-driven batches (every rank issues the same collectives); halo of
-      // p, SpMV + local p.q, allreduce, update + local r.r, allreduce, events, p update
+      // distributed: batches of DIST_BATCH iterations, captured (NCCL) or host-driven
+      const bool graph = dist_capturable(M) && !no_graph();
+      if (graph) {
+        rc = build_dist_cg_graph(M, level);
+        if (rc != GSE_OK) return rc;
+      }
       do {
-        DotOut d = dot_to(ws, &ws->ctrl->pq);
-        for (int bt = 0; bt < 16; ++bt) {
-          rc = dist_spmv(M, level, ws->p, ws->q, &d, s, &ws->ctrl->event);
-          if (rc != GSE_OK) return rc;
-          rc = dist_allreduce_sum(M, &ws->ctrl->pq, 1, s);
-          if (rc != GSE_OK) return rc;
-          launch_k(k_cg_update, ws->vgrid, 256, 0, s, ws->ctrl, ws->ring, ws->r, ws->q, n,
-                   ws->partials, ws->ticket, 0, 0, 1);
-          rc = dist_allreduce_sum(M, &ws->ctrl->rr_part, 1, s);
-          if (rc != GSE_OK) return rc;
-          launch_k(k_cg_events, 1, 32, 0, s, ws->ctrl, ws->ring);
-          launch_xpay(ws, s, n);
+        if (graph) {
+          GSE_CUDA_TRY(cudaGraphLaunch(ws->dcg_exec[level - 1], s));
+        } else {
+          for (int bt = 0; bt < DIST_BATCH; ++bt) {
+            rc = dist_cg_iteration(M, level, s);
+            if (rc != GSE_OK) return rc;
+          }
         }
-        GSE_CUDA_TRY(cudaGetLastError());
         rc = read_ctrl(ws, s);
         if (rc != GSE_OK) return rc;
       } while (hc->event == EV_NONE);
@@ -1663,6 +1715,10 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
       if (rc != GSE_OK) return rc;
       if (rt <= tol) {
         status = GSE_OK;
+        break;
+      }
+      if (level >= sched.max_level) {  // R16 capped by max_level: not converged
+        status = GSE_NOT_CONVERGED;
         break;
       }
       escalate = true;
@@ -2016,6 +2072,10 @@ gse_status solve_gmres(Matrix& M, const double* b, double* x, double tol, int re
       if (rc != GSE_OK) return rc;
       if (rt <= tol) {
         status = GSE_OK;
+        break;
+      }
+      if (level >= sched.max_level) {  // R16 capped by max_level: not converged
+        status = GSE_NOT_CONVERGED;
         break;
       }
       level++;

@@ -508,6 +508,8 @@ static void go(const Matrix& M, const SpmvParams<T>& p, cudaStream_t s) {
     std::lock_guard<std::mutex> lk(mu);
     if (!grid[dev]) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      // the largest shared-memory carveout, so the window buffers never cap residency
+      cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       int blocks = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, WIN_THREADS, smem);
       grid[dev] = (blocks < 1 ? 1 : blocks) * num_sms(M.device);

@@ -7,6 +7,7 @@ oracle:
   * P-rank SpMV within the SpMV tolerance of the oracle;
   * P-rank stepped CG: iterations within 2 of the single-GPU solve, true residual <= tol.
 """
+import os
 import threading
 import time
 
@@ -332,3 +333,52 @@ def test_nccl_backend_single_rank(g):
     assert rd["converged"] and abs(rd["iterations"] - r1["iterations"]) <= 2
     M.close()
     D.close()
+
+
+def _run_workers(world, prefix, env_extra=None, N=24):
+    import subprocess
+    import sys
+    env = dict(os.environ, **(env_extra or {}))
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "dist_worker.py")
+    procs = [subprocess.Popen([sys.executable, worker, str(r), str(world), prefix, str(N)], env=env)
+             for r in range(world)]
+    rcs = [p.wait(timeout=600) for p in procs]
+    assert rcs == [0] * world
+    import json
+    out = [np.load(f"{prefix}_{r}.npz") for r in range(world)]
+    return np.concatenate([o["x"] for o in out]), [json.loads(str(o["rep"])) for o in out]
+
+
+def test_nccl_cg_graph_capture_matches_host_driven(g, tmp_path):
+    """the distributed CG batch captured as a CUDA graph (NCCL backend: halo send/recv, the
+    two allreduces, the side-stream interior SpMV and the kernels) gives bitwise the solution,
+    iterations and switch points of the host-driven batches (GSE_DIST_NO_GRAPH=1), with the
+    scaled stepped schedule (two escalations)"""
+    xg, rg = _run_workers(1, str(tmp_path / "graph"))
+    xh, rh = _run_workers(1, str(tmp_path / "host"), {"GSE_DIST_NO_GRAPH": "1"})
+    assert rg[0]["converged"] and rg[0]["n_switches"] >= 1
+    assert (rg[0]["iterations"], rg[0]["switch_iter"]) == (rh[0]["iterations"], rh[0]["switch_iter"])
+    assert np.array_equal(xg.view(np.uint64), xh.view(np.uint64))
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="multi-rank NCCL needs >= 2 GPUs")
+@pytest.mark.parametrize("world", [2])
+def test_nccl_multi_rank_cg(g, tmp_path, world):
+    """P processes, one GPU each, NCCL over NVLink: the row-partitioned stepped CG matches the
+    single-GPU solve (iterations +-2, switch points +-2) and every rank reports the same
+    iterations and switch points (identical allreduced scalars)"""
+    if torch.cuda.device_count() < world:
+        pytest.skip("not enough GPUs")
+    N = 24
+    x, reps = _run_workers(world, str(tmp_path / "mr"), N=N)
+    assert all(r["iterations"] == reps[0]["iterations"] for r in reps)
+    assert all(r["switch_iter"] == reps[0]["switch_iter"] for r in reps)
+    A = gi.poisson3d(N, "varcoef")
+    M1 = g.gse_encode(A.row_ptr, A.col, A.val, A.rows, A.cols)
+    b = gi.ones_rhs(A)
+    x1, r1 = g.gse_solve_cg(M1, b, tol=1e-10, sched=g.gse_default_schedule("cg", l=30, t=10, m=10))
+    assert reps[0]["converged"] and abs(reps[0]["iterations"] - r1["iterations"]) <= 2
+    for a_, b_ in zip(reps[0]["switch_iter"], r1["switch_iter"]):
+        assert abs(a_ - b_) <= 2
+    assert np.abs(x - x1).max() <= 1e-7

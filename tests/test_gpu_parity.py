@@ -518,6 +518,23 @@ def test_cg_parity_c1(g, variant, mode):
     assert rg["converged"] and rg["rel_residual_true"] <= 1e-10
 
 
+@pytest.mark.parametrize("solver", ["cg", "gmres"])
+@pytest.mark.parametrize("max_level", [1, 2])
+def test_verify_respects_max_level(g, solver, max_level):
+    """R16 capped by max_level: the GPU reports what the oracle reports (status, levels used,
+    iterations +-2)"""
+    A = gi.poisson2d(16, "varcoef") if solver == "cg" else gi.convdiff3d(8)
+    b = gi.ones_rhs(A)
+    M, R = enc_both(g, A)
+    run_g = g.gse_solve_cg if solver == "cg" else g.gse_solve_gmres
+    run_o = O.cg if solver == "cg" else O.gmres
+    tol = 1e-10 if max_level == 1 else 1e-13
+    _, rg = run_g(M, b, tol=tol, sched=g.gse_default_schedule(solver, max_level=max_level))
+    _, ro = run_o(R, b, tol=tol, sched=O.schedule(solver, max_level=max_level))
+    assert rg["status"] == ro.status and abs(rg["iterations"] - ro.iterations) <= 2
+    assert all(v == 0 for v in rg["iters_per_level"][max_level:])
+
+
 @pytest.mark.parametrize("name", ["poisson2d_varcoef", "powerlaw_30k", "random_mixed", "random_wide"])
 def test_perturbation_bounds_bit_exact(g, name):
     """R29 eta_L = ||A_3 - A_L||_inf: bit-identical to the oracle (row sums in storage order)"""
@@ -598,6 +615,46 @@ def test_cg_parity_c2_full_size(g):
     F = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
     res = np.linalg.norm(b - O.spmv_fp64(F, xg.cpu().numpy())) / np.linalg.norm(b)
     assert res <= 1e-10 * 1.001
+
+
+@pytest.mark.parametrize("sched", ["default", "floors", "r29"])
+def test_cg_parity_c2_varcoef_full_size_switching(g, sched):
+    """configs[1] shape with varcoef values (head-lossy): full-size stepped CG that SWITCHES
+    levels -- paper defaults (verify-at-full escalations, R16), level floors (R17) and the R29
+    trigger -- against the oracle: iterations +-2, both switch points +-2, residual ratio in
+    [0.1, 10]"""
+    A = gi.poisson3d(128, "varcoef")
+    b = gi.ones_rhs(A)
+    M, R = enc_both(g, A, device_inputs=True)
+    kw = {"default": {}, "floors": {"level_floor": (1e-3, 1e-8)}, "r29": {"perturb_c": 0.1}}[sched]
+    _, rg = g.gse_solve_cg(M, torch.from_numpy(b).cuda(), tol=1e-10,
+                           sched=g.gse_default_schedule("cg", **kw))
+    O.set_threads(0)
+    _, ro = O.cg(R, b, tol=1e-10, sched=O.schedule("cg", **kw))
+    _cmp_reports(rg, ro)
+    assert rg["n_switches"] == ro.n_switches == 2
+    for a_, b_ in zip(rg["switch_iter"], ro.switch_iter):
+        assert abs(a_ - b_) <= 2, (rg, ro)
+    assert rg["converged"] and rg["rel_residual_true"] <= 1e-10
+
+
+@pytest.mark.parametrize("sched", ["floors", "r29"])
+def test_gmres_parity_convdiff64_switching(g, sched):
+    """C4-shaped conv-diff at 64^3: stepped GMRES(30) that switches levels against the
+    oracle (iterations +-2, switch points +-2, residual ratio)"""
+    A = gi.convdiff3d(64)
+    b = gi.ones_rhs(A)
+    M, R = enc_both(g, A, device_inputs=True)
+    kw = {"floors": {"level_floor": (1e-3, 1e-8)}, "r29": {"perturb_c": 0.1}}[sched]
+    _, rg = g.gse_solve_gmres(M, torch.from_numpy(b).cuda(), tol=1e-10,
+                              sched=g.gse_default_schedule("gmres", **kw))
+    O.set_threads(0)
+    _, ro = O.gmres(R, b, tol=1e-10, sched=O.schedule("gmres", **kw))
+    _cmp_reports(rg, ro)
+    assert rg["n_switches"] == ro.n_switches and rg["n_switches"] >= 1
+    for a_, b_ in zip(rg["switch_iter"], ro.switch_iter):
+        assert abs(a_ - b_) <= 2, (rg, ro)
+    assert rg["converged"] and rg["rel_residual_true"] <= 1e-10
 
 
 def test_cg_breakdown_abort(g):
@@ -687,6 +744,7 @@ def test_encode_sampled_unsampled_max_and_errors(g):
     M = g.gse_encode(A.row_ptr, A.col, A.val, n, n, k_max=2, sample_block_rows=n, seed=11)
     R = O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val, 2, sample_block_rows=n, seed=11)
     assert list(M.info["table"]) == list(R.table) and max(R.table) == 1023 + 40 + 1
+    assert len(R.table) == 2  # R27b: the sampled class keeps its entry, e_max takes the free slot
     assert np.array_equal(g.gse_decode(M, 3), O.decode_all(R, 3))
     with pytest.raises(g.GseError):
         g.gse_encode(A.row_ptr, A.col, A.val, n, n, sample_block_rows=-1)
@@ -854,3 +912,60 @@ def test_concurrent_spmv_threads(g):
     for t in th:
         t.join(timeout=120)
     assert not any(t.is_alive() for t in th) and not errs, errs
+
+
+# ------------------------------------------------------------------ allocator hook
+def test_set_allocator_torch_and_alignment(g):
+    """gse_set_allocator: every device allocation of an encode + SpMV + CG goes through the
+    caller's allocator (torch's caching allocator here: torch sees the planes), results are
+    bitwise those of the default pool; a misaligned allocator is refused with a detail message
+    and its block handed back; NULL restores the default"""
+    A = gi.poisson3d(20, "varcoef")
+    b = gi.ones_rhs(A)
+    x = gi.uniform_vec(A.cols, seed=3)
+    sched = g.gse_default_schedule("cg", l=30, t=10, m=10)
+    M0 = g.gse_encode(A.row_ptr, A.col, A.val, A.rows, A.cols)
+    y0 = g.gse_spmv(M0, x, segments=1)
+    x0, r0 = g.gse_solve_cg(M0, b, tol=1e-10, sched=sched)
+    M0.close()
+    calls = {"alloc": 0, "free": 0}
+    ta, tf = g.torch_allocator()
+
+    def alloc(n, s):
+        calls["alloc"] += 1
+        return ta(n, s)
+
+    def free(p, s):
+        calls["free"] += 1
+        tf(p, s)
+
+    try:
+        g.gse_set_allocator(alloc, free)
+        torch.cuda.synchronize()
+        before = torch.cuda.memory_allocated()
+        M1 = g.gse_encode(A.row_ptr, A.col, A.val, A.rows, A.cols)
+        assert torch.cuda.memory_allocated() - before >= 12 * A.nnz  # the planes live in torch
+        y1 = g.gse_spmv(M1, x, segments=1)
+        x1, r1 = g.gse_solve_cg(M1, b, tol=1e-10, sched=sched)
+        M1.close()
+        assert calls["alloc"] > 0 and calls["free"] == calls["alloc"]
+        assert np.array_equal(y0, y1) and np.array_equal(x0, x1)
+        assert (r0["iterations"], r0["switch_iter"]) == (r1["iterations"], r1["switch_iter"])
+        held = {}
+
+        def bad_alloc(n, s):  # 16 bytes off a 256-byte boundary
+            p = ta(n + 256, s)
+            held[p + 16] = p
+            return p + 16
+
+        def bad_free(p, s):
+            tf(held.pop(p), s)
+
+        g.gse_set_allocator(bad_alloc, bad_free)
+        with pytest.raises(g.GseError) as ei:
+            g.gse_encode(A.row_ptr, A.col, A.val, A.rows, A.cols)
+        assert "aligned" in str(ei.value) and not held
+    finally:
+        g.gse_set_allocator(None, None)
+    M2 = g.gse_encode(A.row_ptr, A.col, A.val, A.rows, A.cols)
+    assert np.array_equal(g.gse_spmv(M2, x, segments=1), y0)
