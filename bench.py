@@ -68,6 +68,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--dist1", action="store_true",
+                    help="diagnostic: the distributed (NCCL) path even at N = 1 (1-rank communicator)")
     a = ap.parse_args()
     a.N, a.cfg = WORKLOADS[a.workload]
     return a
@@ -405,6 +407,8 @@ def run_gse(args, world, rank, local, pg):
             uid.copy_(torch.frombuffer(bytearray(g.gse_nccl_unique_id()), dtype=torch.uint8))
         tdist.broadcast(uid, 0)
         D = g.gse_dist_create(bytes(uid.cpu().numpy()), rank, world, local)
+    elif args.dist1:
+        D = g.gse_dist_create(g.gse_nccl_unique_id(), 0, 1, local)
 
     def encode(rp_, col_, val_, **kw):
         if D is None:
@@ -450,11 +454,13 @@ def run_gse(args, world, rank, local, pg):
         "data": "synthetic (gse_inputs recipe, DESIGN.md 4)",
         "config": _config(args, n_glob, nnz_glob, world)}
     sub = {}
-    if world == 1 and rank == 0 and not args.quick and not args.no_sweep:
+    if args.dist1:
+        line["config"]["parallelism"] = "distributed path, 1-rank NCCL communicator (diagnostic)"
+    if world == 1 and rank == 0 and not args.quick and not args.no_sweep and not args.dist1:
         # the configs[1..3] sub-objects first (their GPU memory is freed before the C5 work)
         sub = sub_workloads(dev, stream, flush, hbm_peak)
     extra = None
-    if world == 1 and not args.no_sweep:
+    if world == 1 and not args.no_sweep and not args.dist1:
         extra = main_sweep(args, rp, col, val, b, n_loc, dev, stream, flush, hbm_peak)
     e2e = None if args.no_e2e else e2e_measure(args, rp, col, val, b, dev, stream, encode)
     cpu = None

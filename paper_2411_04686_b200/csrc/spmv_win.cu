@@ -144,6 +144,9 @@ struct WinStash {  // per warp, double-buffered across tiles
 
 // resident CTAs per SM the register budget is sized for: 4 (64 registers) where the lane's
 // planes fit, 3 for the 8-byte planes of level 3 / FP64 CSR (GSE_WIN_MINB: A/B knob)
+#ifndef GSE_WIN_HIADD
+#define GSE_WIN_HIADD 0
+#endif
 #ifndef GSE_WIN_MINB_LO
 #define GSE_WIN_MINB_LO 3
 #endif
@@ -163,6 +166,11 @@ __global__ void __launch_bounds__(WIN_THREADS, WIN_MINB(L)) k_spmv_win(const Spm
   // sign-folded scales (FAST): [EI | sign << ei_bits] = (sign ? -1 : 1) * scale[EI]
   // FP64: {ssc, -2^52 ssc} pairs (levels 1-2 decode as one FMA, one 16-byte table load)
   __shared__ __align__(16) T ssc2[256];
+#if GSE_WIN_HIADD
+  // FP64 levels 1-2: [EI | sign << ei_bits] = (k_EI << 20) + (sign << 31), added to the hi
+  // word of the exactly converted D_L (|v| = D_L 2^k; FAST excludes under/overflow)
+  __shared__ uint32_t shadd[128];
+#endif
   __shared__ WinStash<T> stash;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -180,6 +188,10 @@ __global__ void __launch_bounds__(WIN_THREADS, WIN_MINB(L)) k_spmv_win(const Spm
       if constexpr (sizeof(T) == 8) {
         ssc2[2 * t] = v;
         ssc2[2 * t + 1] = -4503599627370496.0 * (double)v;
+#if GSE_WIN_HIADD
+        shadd[t] = sign <= 1u ? (uint32_t)(__double2hiint(p.sc64[ei]) - (1023 << 20)) + (sign << 31)
+                              : 0u;
+#endif
       } else {
         ssc2[t] = v;
       }
@@ -308,6 +320,12 @@ __global__ void __launch_bounds__(WIN_THREADS, WIN_MINB(L)) k_spmv_win(const Spm
                                       : __funnelshift_rc(cw[j], h >> 15, p.ei_shift);
             if constexpr (L == 1) {
               const uint32_t D = h & 0x7FFFu;
+#if GSE_WIN_HIADD
+              if constexpr (sizeof(T) == 8) {  // exact D, exponent + sign by one integer add
+                const double dv = __uint2double_rn(D);
+                return __hiloint2double(__double2hiint(dv) + (D ? (int)shadd[idx] : 0), 0);
+              }
+#endif
               // (2^52 + D) sc - 2^52 sc = D sc exactly (D < 2^31, sc = +-2^k): one FMA
               if constexpr (sizeof(T) == 8)
               {
@@ -318,6 +336,13 @@ __global__ void __launch_bounds__(WIN_THREADS, WIN_MINB(L)) k_spmv_win(const Spm
               }
             } else if constexpr (L == 2) {
               const uint32_t D = ((h & 0x7FFFu) << 16) | t1;
+#if GSE_WIN_HIADD
+              if constexpr (sizeof(T) == 8) {
+                const double dv = __uint2double_rn(D);
+                return __hiloint2double(__double2hiint(dv) + (D ? (int)shadd[idx] : 0),
+                                        __double2loint(dv));
+              }
+#endif
               if constexpr (sizeof(T) == 8)
               {
                 const double2 sn = reinterpret_cast<const double2*>(ssc2)[idx];
