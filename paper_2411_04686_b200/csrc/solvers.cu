@@ -91,6 +91,10 @@ struct SolverWs {
   // distributed CG (NCCL backend): one captured batch of DIST_BATCH iterations per level
   cudaGraphExec_t dcg_exec[3] = {nullptr, nullptr, nullptr};
   cudaGraph_t dcg_graph[3] = {nullptr, nullptr, nullptr};
+  // distributed GMRES (NCCL backend): one captured restart cycle per level
+  cudaGraphExec_t dgm_exec[3] = {nullptr, nullptr, nullptr};
+  cudaGraph_t dgm_graph[3] = {nullptr, nullptr, nullptr};
+  int dgm_restart = 0;
   cudaGraph_t gm_graph[3] = {nullptr, nullptr, nullptr};
   int gm_restart = 0;
   int cg_xx = 0;  // the CG graphs compute ||x||^2 in k_cg_xpay (R29 trigger on)
@@ -1330,6 +1334,8 @@ void free_solver_ws(Matrix& M) {
     if (ws->gm_graph[L]) cudaGraphDestroy(ws->gm_graph[L]);
     if (ws->dcg_exec[L]) cudaGraphExecDestroy(ws->dcg_exec[L]);
     if (ws->dcg_graph[L]) cudaGraphDestroy(ws->dcg_graph[L]);
+    if (ws->dgm_exec[L]) cudaGraphExecDestroy(ws->dgm_exec[L]);
+    if (ws->dgm_graph[L]) cudaGraphDestroy(ws->dgm_graph[L]);
   }
   for (double* p : {ws->x, ws->r, ws->p, ws->q, ws->b, ws->tmp, ws->V, ws->partials,
                     ws->ring, ws->vcur})
@@ -1993,6 +1999,36 @@ static gse_status gm_cycle_dist(Matrix& M, int level, int restart, cudaStream_t 
   return GSE_OK;
 }
 
+// NCCL backend: the whole restart cycle (halo + SpMV per inner step, the j + 2 scalar
+// allreduces of MGS, Givens / monitor, the x update) captured once per level and restart
+// length, replayed with one launch per cycle
+static gse_status build_dist_gm_graph(Matrix& M, int level, int restart) {
+  SolverWs* ws = M.ws;
+  if (ws->dgm_restart != restart) {
+    for (int L = 0; L < 3; ++L) {
+      if (ws->dgm_exec[L]) cudaGraphExecDestroy(ws->dgm_exec[L]);
+      if (ws->dgm_graph[L]) cudaGraphDestroy(ws->dgm_graph[L]);
+      ws->dgm_exec[L] = nullptr;
+      ws->dgm_graph[L] = nullptr;
+    }
+    ws->dgm_restart = restart;
+  }
+  if (ws->dgm_exec[level - 1]) return GSE_OK;
+  cudaStream_t cs = ws->cap_stream;
+  GSE_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+  gse_status rc = gm_cycle_dist(M, level, restart, cs);
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(cs, &g);
+  if (rc != GSE_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  GSE_CUDA_TRY(e);
+  GSE_CUDA_TRY(cudaGraphInstantiate(&ws->dgm_exec[level - 1], g, 0));
+  ws->dgm_graph[level - 1] = g;
+  return GSE_OK;
+}
+
 gse_status solve_gmres(Matrix& M, const double* b, double* x, double tol, int restart,
                        int64_t max_iters, const gse_step_schedule& sched, gse_solve_report& rep,
                        cudaStream_t s) {
@@ -2043,8 +2079,14 @@ gse_status solve_gmres(Matrix& M, const double* b, double* x, double tol, int re
   int64_t last_iter = 0, iter = 0;
   for (;;) {
     if (M.dist) {
-      rc = gm_cycle_dist(M, level, restart, s);
-      if (rc != GSE_OK) return rc;
+      if (dist_capturable(M) && !no_graph()) {
+        rc = build_dist_gm_graph(M, level, restart);
+        if (rc != GSE_OK) return rc;
+        GSE_CUDA_TRY(cudaGraphLaunch(ws->dgm_exec[level - 1], s));
+      } else {
+        rc = gm_cycle_dist(M, level, restart, s);
+        if (rc != GSE_OK) return rc;
+      }
     } else {
       rc = build_gm_graph(M, level, restart, k16);
       if (rc != GSE_OK) return rc;

@@ -145,7 +145,7 @@ struct WinStash {  // per warp, double-buffered across tiles
 // resident CTAs per SM the register budget is sized for: 4 (64 registers) where the lane's
 // planes fit, 3 for the 8-byte planes of level 3 / FP64 CSR (GSE_WIN_MINB: A/B knob)
 #ifndef GSE_WIN_HIADD
-#define GSE_WIN_HIADD 0
+#define GSE_WIN_HIADD 1
 #endif
 #ifndef GSE_WIN_MINB_LO
 #define GSE_WIN_MINB_LO 3
@@ -533,8 +533,6 @@ static void go(const Matrix& M, const SpmvParams<T>& p, cudaStream_t s) {
     std::lock_guard<std::mutex> lk(mu);
     if (!grid[dev]) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      // the largest shared-memory carveout, so the window buffers never cap residency
-      cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       int blocks = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, WIN_THREADS, smem);
       grid[dev] = (blocks < 1 ? 1 : blocks) * num_sms(M.device);

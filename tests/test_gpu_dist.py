@@ -335,18 +335,31 @@ def test_nccl_backend_single_rank(g):
     D.close()
 
 
-def _run_workers(world, prefix, env_extra=None, N=24):
+def _run_workers(world, prefix, env_extra=None, N=24, solver="cg"):
     import subprocess
     import sys
     env = dict(os.environ, **(env_extra or {}))
     worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "dist_worker.py")
-    procs = [subprocess.Popen([sys.executable, worker, str(r), str(world), prefix, str(N)], env=env)
+    procs = [subprocess.Popen([sys.executable, worker, str(r), str(world), prefix, str(N), solver],
+                              env=env)
              for r in range(world)]
     rcs = [p.wait(timeout=600) for p in procs]
     assert rcs == [0] * world
     import json
     out = [np.load(f"{prefix}_{r}.npz") for r in range(world)]
     return np.concatenate([o["x"] for o in out]), [json.loads(str(o["rep"])) for o in out]
+
+
+def test_nccl_gmres_graph_capture_matches_host_driven(g, tmp_path):
+    """the distributed GMRES(30) restart cycle captured as a CUDA graph per level (NCCL
+    backend) gives bitwise the solution, inner iterations and switch points of the
+    host-enqueued cycles (GSE_DIST_NO_GRAPH=1); stepped with level floors (two switches)"""
+    xg, rg = _run_workers(1, str(tmp_path / "graph"), N=12, solver="gmres")
+    xh, rh = _run_workers(1, str(tmp_path / "host"), {"GSE_DIST_NO_GRAPH": "1"}, N=12,
+                          solver="gmres")
+    assert rg[0]["converged"] and rg[0]["n_switches"] >= 1
+    assert (rg[0]["iterations"], rg[0]["switch_iter"]) == (rh[0]["iterations"], rh[0]["switch_iter"])
+    assert np.array_equal(xg.view(np.uint64), xh.view(np.uint64))
 
 
 def test_nccl_cg_graph_capture_matches_host_driven(g, tmp_path):
