@@ -15,7 +15,12 @@
  * Pins (tests/test_oracle_*.py, -m "not gpu"): worked examples of S:60-105, S:162-173,
  * S:268-278; closed forms (|v| = D_L * 2^(E-1086), bit-exact round trip for
  * d <= 11, Poisson head-exactness); brute-force dense matvec; dense direct solves;
- * literal transcriptions of Alg. 1 / Alg. 2 in the tests.
+ * literal transcriptions of Alg. 1 / Alg. 2 in the tests; scipy CG / GMRES(30) iteration
+ * gauges; the R29 bound eta_L against a closed form.
+ *
+ * Parity unpinned by the paper (pinned only by agreement with this file under the DESIGN.md
+ * readings): FP32 accumulation (R20), the level floors (R17), verify-at-full (R16, R16b),
+ * the CG restart at a switch (R15), the R29 trigger's constant c.
  */
 #include "gse_oracle.h"
 
