@@ -456,12 +456,12 @@ def run_gse(args, world, rank, local, pg):
     sub = {}
     if args.dist1:
         line["config"]["parallelism"] = "distributed path, 1-rank NCCL communicator (diagnostic)"
-    if world == 1 and rank == 0 and not args.quick and not args.no_sweep and not args.dist1:
-        # the configs[1..3] sub-objects first (their GPU memory is freed before the C5 work)
-        sub = sub_workloads(dev, stream, flush, hbm_peak)
     extra = None
     if world == 1 and not args.no_sweep and not args.dist1:
+        # right after the timed steps, in the same thermal / power state
         extra = main_sweep(args, rp, col, val, b, n_loc, dev, stream, flush, hbm_peak)
+    if world == 1 and rank == 0 and not args.quick and not args.no_sweep and not args.dist1:
+        sub = sub_workloads(dev, stream, flush, hbm_peak)
     e2e = None if args.no_e2e else e2e_measure(args, rp, col, val, b, dev, stream, encode)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
