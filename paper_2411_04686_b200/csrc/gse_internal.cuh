@@ -36,10 +36,10 @@ constexpr int RW_TILE = 1024;  // max staged span (8-aligned non-zeros) of a row
 constexpr int WIN_EPT = 8;                  // consecutive non-zeros per lane and chunk
 constexpr int WIN_CH = 32 * WIN_EPT;        // non-zeros per warp chunk
 #ifndef GSE_WIN_HALF
-#define GSE_WIN_HALF 512
+#define GSE_WIN_HALF 384
 #endif
 #ifndef GSE_WIN_RMAX
-#define GSE_WIN_RMAX 2048
+#define GSE_WIN_RMAX 1280
 #endif
 constexpr uint32_t WIN_HALF = GSE_WIN_HALF;  // x window reaches this many columns past the rows
 constexpr uint32_t WIN_RMAX = GSE_WIN_RMAX;  // rows per tile (bounds the window)
