@@ -571,6 +571,12 @@ def main_sweep(args, rp, col, val, b, n, dev, stream, flush, hbm_peak):
     out["L1_dot_cg_loop"] = spmv_entry(b1, nnz, us_dot, hbm_peak)
     dot = {"bytes": b1, "us": us_dot, "GBps": b1 / (us_dot * 1e-6) / 1e9}
     del x32, y32
+    # the paper's FP16 / BF16 storage baselines: 6 B/nnz, FP64 products and sums
+    for kind in ("fp16", "bf16"):
+        H = g.gse_half_matrix(rp, col, val, n, n, kind=kind)
+        out[kind] = spmv_entry(nnz * 6 + rows_b + 16 * n, nnz,
+                               1e3 * cold(lambda: g.gse_spmv(H, x, y, segments=3)), hbm_peak)
+        H.close()
     F = g.gse_fp64_matrix(rp, col, val, n, n)
     out["fp64_csr"] = spmv_entry(nnz * 12 + rows_b + 16 * n, nnz,
                                  1e3 * cold(lambda: g.gse_spmv(F, x, y, segments=3)), hbm_peak)
@@ -681,11 +687,22 @@ def sub_c2(dev, stream, flush, peak):
     fn()
     sw["fp64_csr"] = spmv_entry(nnz * 12 + 4 * (n + 1) + 16 * n, nnz,
                                 1e3 * statistics.mean(time_cuda(fn, 20, stream, flush)), peak)
+    # the paper's 16-bit storage baselines and its GSE-SEM* projection (Eq. 7,
+    # the FP16 solver's time per iteration x the GSE iteration count)
+    half = {}
+    for kind in ("fp16", "bf16"):
+        H = g.gse_half_matrix(rp, col, val, n, n, kind=kind)
+        th, rh = _solve_ms(g, stream, flush, "cg", H, b, x, None)
+        half[kind] = {"ms": r3(th), "it": rh["iterations"],
+                      "res_vs_rounded_matrix": r3(rh["rel_residual_true"])}
+        H.close()
+    eq7 = half["fp16"]["ms"] / max(half["fp16"]["it"], 1) * rg["iterations"]
     M.close()
     F.close()
     return {"solves_per_s": r3(1e3 / t), "step_ms": r3(t), "cg_ms": r3(tg), "iters": rg["iterations"],
             "fp64_csr_cg_ms": r3(t64), "fp64_iters": r64["iterations"],
-            "speedup_vs_fp64_csr": r3(t64 / tg), "spmv": sw}
+            "speedup_vs_fp64_csr": r3(t64 / tg), "half_storage_cg": half,
+            "gse_sem_star_eq7_ms": r3(eq7), "gse_sem_star_x_fp64": r3(t64 / eq7), "spmv": sw}
 
 
 def sub_c2_varcoef(dev, stream, flush):

@@ -147,6 +147,9 @@ struct WinStash {  // per warp, double-buffered across tiles
 #ifndef GSE_WIN_HIADD
 #define GSE_WIN_HIADD 1
 #endif
+#ifndef GSE_WIN_HIADD3  // the same at level 3 (A/B)
+#define GSE_WIN_HIADD3 1
+#endif
 #ifndef GSE_WIN_MINB_LO
 #define GSE_WIN_MINB_LO 3
 #endif
@@ -352,6 +355,13 @@ __global__ void __launch_bounds__(WIN_THREADS, WIN_MINB(L)) k_spmv_win(const Spm
               }
             } else {
               const uint64_t D = ((uint64_t)(h & 0x7FFFu) << 48) | ((uint64_t)t1 << 32) | t2;
+#if GSE_WIN_HIADD3
+              if constexpr (sizeof(T) == 8) {  // encoder output: D has <= 53 significant bits
+                const double dv = __ull2double_rz(D);
+                const int hi = __double2hiint(dv);
+                return __hiloint2double(hi ? hi + (int)shadd[idx] : 0, __double2loint(dv));
+              }
+#endif
               if constexpr (sizeof(T) == 8)
                 return __ull2double_rz(D) * ssc2[2 * idx];
               else
