@@ -395,3 +395,45 @@ def test_nccl_multi_rank_cg(g, tmp_path, world):
     for a_, b_ in zip(reps[0]["switch_iter"], r1["switch_iter"]):
         assert abs(a_ - b_) <= 2
     assert np.abs(x - x1).max() <= 1e-7
+
+
+def test_dist_single_gpu_only_options_are_refused(g):
+    """options defined for one GPU fail loudly on a distributed matrix (no silent fallback):
+    gse_spmv_dot (its dot would need the solve's allreduce), the R29 trigger, the 16-bit
+    Krylov basis; the plain solves on the same handle still work"""
+    A = gi.poisson3d(12, "varcoef")
+    b = gi.ones_rhs(A)
+
+    def fn(r, D, st):
+        rr = partition(A.rows, 2)
+        a, bb = rr[r], rr[r + 1]
+        rp, col, val = slab(A, a, bb)
+        dev = lambda v: torch.from_numpy(v).cuda()
+        M = g.gse_encode_dist(D, dev(rp), dev(col), dev(val), a, A.rows, stream=st.cuda_stream)
+        x = dev(gi.uniform_vec(bb - a, seed=r))
+        errs = []
+        for call in (lambda: g.gse_spmv_dot(M, x, stream=st.cuda_stream),
+                     lambda: g.gse_solve_cg(M, dev(b[a:bb].copy()), tol=1e-10, stream=st.cuda_stream,
+                                            sched=g.gse_default_schedule("cg", perturb_c=0.1))):
+            try:
+                call()
+                errs.append(None)
+            except g.GseError as e:
+                errs.append(e.status)
+        k16 = g.gse_default_schedule("gmres")
+        k16.krylov_gse16 = 1
+        try:
+            g.gse_solve_gmres(M, dev(b[a:bb].copy()), tol=1e-10, sched=k16, stream=st.cuda_stream)
+            errs.append(None)
+        except g.GseError as e:
+            errs.append(e.status)
+        _, rep = g.gse_solve_cg(M, dev(b[a:bb].copy()), tol=1e-10, stream=st.cuda_stream,
+                                sched=g.gse_default_schedule("cg", l=30, t=10, m=10))
+        st.synchronize()
+        M.close()
+        return errs, rep
+
+    outs = run_ranks(2, fn)
+    for errs, rep in outs:
+        assert errs == [g.GSE_ERR_WRONG_FORMAT] * 3
+        assert rep["converged"]
