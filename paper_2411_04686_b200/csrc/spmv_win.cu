@@ -326,7 +326,8 @@ __global__ void __launch_bounds__(WIN_THREADS, WIN_MINB(L)) k_spmv_win(const Spm
 #if GSE_WIN_HIADD
               if constexpr (sizeof(T) == 8) {  // exact D, exponent + sign by one integer add
                 const double dv = __uint2double_rn(D);
-                return __hiloint2double(__double2hiint(dv) + (D ? (int)shadd[idx] : 0), 0);
+                const int e = (int)shadd[idx];
+                return __hiloint2double(__double2hiint(dv) + (D ? e : 0), 0);
               }
 #endif
               // (2^52 + D) sc - 2^52 sc = D sc exactly (D < 2^31, sc = +-2^k): one FMA
@@ -342,8 +343,8 @@ __global__ void __launch_bounds__(WIN_THREADS, WIN_MINB(L)) k_spmv_win(const Spm
 #if GSE_WIN_HIADD
               if constexpr (sizeof(T) == 8) {
                 const double dv = __uint2double_rn(D);
-                return __hiloint2double(__double2hiint(dv) + (D ? (int)shadd[idx] : 0),
-                                        __double2loint(dv));
+                const int e = (int)shadd[idx];
+                return __hiloint2double(__double2hiint(dv) + (D ? e : 0), __double2loint(dv));
               }
 #endif
               if constexpr (sizeof(T) == 8)
@@ -359,7 +360,8 @@ __global__ void __launch_bounds__(WIN_THREADS, WIN_MINB(L)) k_spmv_win(const Spm
               if constexpr (sizeof(T) == 8) {  // encoder output: D has <= 53 significant bits
                 const double dv = __ull2double_rz(D);
                 const int hi = __double2hiint(dv);
-                return __hiloint2double(hi ? hi + (int)shadd[idx] : 0, __double2loint(dv));
+                const int e = (int)shadd[idx];
+                return __hiloint2double(hi ? hi + e : 0, __double2loint(dv));
               }
 #endif
               if constexpr (sizeof(T) == 8)
