@@ -488,3 +488,93 @@ def test_verify_respects_max_level(solver):
     _, r2 = run(G, b, tol=1e-13, sched=O.schedule(solver, max_level=2))
     assert r2.iters_per_level[2] == 0 and max(r2.switch_to_level, default=1) <= 2
     assert r2.status == (O.OK if r2.rel_residual_true <= 1e-13 else O.NOT_CONVERGED)
+
+
+def _numpy_stepped_gmres(mats, b, tol, m, floors=None, c=None, eta=None, max_iters=3000):
+    """An independent stepped GMRES(m) (numpy, decoded level matrices): MGS Arnoldi, Givens
+    rotations in the R18 form, the estimate |g_{j+1}|/||b|| monitored after every inner
+    step; a switch (floor R17 or R29 bound with ||x|| at the cycle start) ends the cycle
+    (x += V y) and restarts at the next level (R15); an explicit-residual convergence at
+    L < 3 is verified with A_3 (R16)."""
+    n = b.size
+    nb = np.linalg.norm(b)
+    x = np.zeros(n)
+    L, jg, sw = 1, 0, []
+    while jg < max_iters:
+        r = b - mats[L] @ x
+        beta = np.linalg.norm(r)
+        if beta / nb <= tol:
+            if L < 3 and np.linalg.norm(b - mats[3] @ x) / nb > tol:
+                L += 1
+                sw.append(jg)
+                continue
+            break
+        xx = x @ x
+        V = np.zeros((m + 1, n))
+        H = np.zeros((m + 1, m))
+        cs, sn, g = np.zeros(m), np.zeros(m), np.zeros(m + 1)
+        V[0] = r / beta
+        g[0] = beta
+        k, esc = 0, False
+        for j in range(m):
+            jg += 1
+            w = mats[L] @ V[j]
+            for i in range(j + 1):
+                H[i, j] = w @ V[i]
+                w = w - H[i, j] * V[i]
+            hn = np.linalg.norm(w)
+            H[j + 1, j] = hn
+            for i in range(j):
+                h1, h2 = H[i, j], H[i + 1, j]
+                H[i, j], H[i + 1, j] = cs[i] * h1 + sn[i] * h2, cs[i] * h2 - sn[i] * h1
+            h1, h2 = H[j, j], H[j + 1, j]
+            if h2 == 0:
+                cc, ss = 1.0, 0.0
+            elif abs(h2) > abs(h1):
+                tau = h1 / h2
+                ss = 1 / np.sqrt(1 + tau * tau)
+                cc = ss * tau
+            else:
+                tau = h2 / h1
+                cc = 1 / np.sqrt(1 + tau * tau)
+                ss = cc * tau
+            cs[j], sn[j] = cc, ss
+            H[j, j], H[j + 1, j] = cc * h1 + ss * h2, 0.0
+            g[j + 1], g[j] = -ss * g[j], cc * g[j]
+            res = abs(g[j + 1]) / nb
+            k = j + 1
+            if res <= tol or hn == 0.0:
+                break
+            if L < 3 and ((floors and res < floors[L - 1]) or
+                          (c and xx > 0 and res <= c * eta[L - 1] * np.sqrt(xx) / nb)):
+                esc = True
+                break
+            V[j + 1] = w / hn
+        y = np.linalg.solve(np.triu(H[:k, :k]), g[:k])
+        x = x + V[:k].T @ y
+        if esc:
+            L += 1
+            sw.append(jg)
+    return jg, sw, np.linalg.norm(b - mats[3] @ x) / nb
+
+
+@pytest.mark.parametrize("mode", ["floors", "r29"])
+def test_stepped_gmres_matches_independent_numpy(mode):
+    """The oracle's stepped GMRES(30) switch points and inner-iteration count against the
+    independent numpy implementation above (floors R17 and the R29 trigger), conv-diff 10^3"""
+    import scipy.sparse as sp
+    A = gi.convdiff3d(10)
+    G = enc(A)
+    b = gi.ones_rhs(A)
+    mats = {L: sp.csr_matrix((O.decode_all(G, L), A.col, A.row_ptr), shape=(A.rows, A.cols))
+            for L in (1, 2, 3)}
+    if mode == "floors":
+        kw, args = {"level_floor": (1e-3, 1e-8)}, {"floors": (1e-3, 1e-8)}
+    else:
+        kw, args = {"perturb_c": 0.1}, {"c": 0.1, "eta": O.perturbation_bounds(G)}
+    its, sw, res = _numpy_stepped_gmres(mats, b, 1e-10, 30, **args)
+    _, rep = O.gmres(G, b, tol=1e-10, restart=30, sched=O.schedule("gmres", **kw))
+    assert rep.converged and res <= 1e-10
+    assert len(sw) == rep.n_switches >= 1
+    assert all(abs(a_ - b_) <= 2 for a_, b_ in zip(sw, rep.switch_iter)), (sw, rep.switch_iter)
+    assert abs(its - rep.iterations) <= 2, (its, rep.iterations)
