@@ -347,7 +347,12 @@ static void interior_from_halo_rows(int64_t n_local, const std::vector<uint32_t>
     }
     prev = r;
   }
-  int64_t a = (best0 + 63) / 64 * 64, b = best1 / 64 * 64;
+  // the end moves in by 128 rows besides the 64-row alignment: the row walk's stage
+  // over-copies (and gathers, then masks) up to 8 stored entries past a group's last row,
+  // which must still belong to interior rows so the interior SpMV never reads halo entries
+  // of x_ext while the exchange writes them (advisor finding)
+  const int64_t e = best1 > 128 ? best1 - 128 : 0;
+  int64_t a = (best0 + 63) / 64 * 64, b = e / 64 * 64;
   const int64_t min_len = n_local / 8 > 4096 ? n_local / 8 : 4096;
   if (b - a < min_len) a = b = 0;
   *i0 = a;
