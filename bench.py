@@ -490,11 +490,11 @@ def run_gse(args, world, rank, local, pg):
         line["roofline"] = {
             "bound": "hbm", "achieved": r3(dot["GBps"]), "peak": hbm_peak, "unit": "GB/s",
             "frac": r3(dot["GBps"] / hbm_peak), "traffic": _profiled_traffic(),
-            "kernel": "k_spmv_rw<L=1,DOT> (the CG's fused level-1 SpMV + p.q on C5)",
+            "kernel": "k_spmv_rw<L=1,DOT>: the CG's fused level-1 SpMV + p.q",
             "algorithmic_bytes_per_launch": dot["bytes"], "avg_launch_us": r3(dot["us"]),
             "peak_source": peak_src,
-            "timing": "gse_spmv_dot back to back (as in the CG loop), CUDA events on the "
-                      "launching stream, mean per launch"}
+            "timing": "gse_spmv_dot back to back right after the timed steps, CUDA events on "
+                      "its stream, mean per launch"}
     line["e2e"] = e2e
     line["cpu_baseline"] = cpu
     line["gpu_launches"] = launches
