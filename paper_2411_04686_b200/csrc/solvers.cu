@@ -288,6 +288,16 @@ __device__ void cg_events(SolveCtrl* c, double* ring, double tot, bool ok,
   }
 }
 
+// pairs in flight per thread in k_cg_update (A/B knob)
+#ifndef GSE_UPD_K
+#define GSE_UPD_K 1
+#endif
+constexpr int UPD_K = GSE_UPD_K;
+#ifndef GSE_XPAY_K
+#define GSE_XPAY_K 1
+#endif
+constexpr int XPAY_K = GSE_XPAY_K;
+
 // r -= alpha q ; rr_new = r.r ; monitor ; events.  x += alpha p is deferred to k_cg_xpay,
 // which reads p anyway (same arithmetic, one vector pass less per iteration); alpha is
 // handed over in c->alpha (0 when this iteration did not update).
@@ -316,10 +326,10 @@ __global__ void __launch_bounds__(256, 4) k_cg_update(SolveCtrl* __restrict__ c,
     const double2* __restrict__ q2 = reinterpret_cast<const double2*>(q);
     double2* __restrict__ r2 = reinterpret_cast<double2*>(r);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += 4 * stride) {
-      double2 rv[4], qv[4];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += UPD_K * stride) {
+      double2 rv[UPD_K], qv[UPD_K];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < UPD_K; ++k) {
         const int64_t j = i + k * stride;
         if (j < n2) {
           rv[k] = r2[j];
@@ -327,7 +337,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_update(SolveCtrl* __restrict__ c,
         }
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < UPD_K; ++k) {
         const int64_t j = i + k * stride;
         if (j < n2) {
           double2 ro;
@@ -387,10 +397,10 @@ __global__ void __launch_bounds__(256, 4) k_cg_xpay(SolveCtrl* __restrict__ c,
   double2* __restrict__ p2 = reinterpret_cast<double2*>(p);
   const double2* __restrict__ r2 = reinterpret_cast<const double2*>(r);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += 2 * stride) {
-    double2 pv[2], rv[2], xv[2];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += XPAY_K * stride) {
+    double2 pv[XPAY_K], rv[XPAY_K], xv[XPAY_K];
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < XPAY_K; ++k) {
       const int64_t j = i + k * stride;
       if (j < n2) {
         pv[k] = p2[j];
@@ -399,7 +409,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_xpay(SolveCtrl* __restrict__ c,
       }
     }
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < XPAY_K; ++k) {
       const int64_t j = i + k * stride;
       if (j < n2) {
         if (do_x) {
