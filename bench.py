@@ -49,6 +49,7 @@ METRIC = ("GSE SpMV GB/s & GFLOP/s (frac of HBM peak) per segment count; "
 WORKLOADS = {"c5": (512, "configs[4]"), "c2": (128, "configs[1]")}
 TOL = 1e-10
 R29_C = 0.1  # the R29 trigger constant of the stepped_r29 sub-results (R29)
+R30_C = 3.0  # R29 constant of the kept-direction (R30) sub-result
 
 
 def unit_for(N):
@@ -724,7 +725,10 @@ def sub_c2_varcoef(dev, stream, flush):
     out["fp64_csr"] = {"ms": r3(t64), "it": r64["iterations"]}
     for name, s in (("stepped_default", g.gse_default_schedule("cg")),
                     ("stepped_floors", g.gse_default_schedule("cg", level_floor=(1e-3, 1e-8))),
-                    ("stepped_r29", g.gse_default_schedule("cg", perturb_c=R29_C))):
+                    ("stepped_r29", g.gse_default_schedule("cg", perturb_c=R29_C)),
+                    # R29 trigger from level 2 with the R30 kept direction (R30)
+                    ("stepped_r29_keep_l2", g.gse_default_schedule(
+                        "cg", perturb_c=R30_C, start_level=2, cg_keep_direction=1))):
         t, r = _solve_ms(g, stream, flush, "cg", M, b, x, s)
         out[name] = {"ms": r3(t), "it": r["iterations"], "per_level": r["iters_per_level"],
                      "res": r3(r["rel_residual_true"]), "x_fp64": r3(t64 / t)}

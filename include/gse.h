@@ -214,6 +214,11 @@ typedef struct {
                                 * the true residual.  x = the iterate before the current CG
                                 * iteration's update / at the start of the GMRES cycle.
                                 * 0 = off (default, the paper's monitor only); must be >= 0 */
+  int cg_keep_direction;       /* R30 (build reading, CG, single GPU): at a level switch replace
+                                * the residual, r = b - A_new x, but keep the search direction:
+                                * beta = r.r / rr_{j-1}, p = r + beta p (a residual-replacement
+                                * step instead of the R15 restart p = r); 0 = R15 restart
+                                * (default), 1 = keep; GMRES ignores it                       */
 } gse_step_schedule;
 
 typedef struct {

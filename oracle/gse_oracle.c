@@ -16,7 +16,9 @@
  * S:268-278; closed forms (|v| = D_L * 2^(E-1086), bit-exact round trip for
  * d <= 11, Poisson head-exactness); brute-force dense matvec; dense direct solves;
  * literal transcriptions of Alg. 1 / Alg. 2 in the tests; scipy CG / GMRES(30) iteration
- * gauges; the R29 bound eta_L against a closed form.
+ * gauges; the R29 bound eta_L against a closed form; the R30 kept-direction switch against
+ * an independent numpy CG and, on a head-exact matrix with forced switches, against the
+ * fixed-level CG's iteration count (a pure residual replacement leaves CG unchanged).
  *
  * Parity unpinned by the paper (pinned only by agreement with this file under the DESIGN.md
  * readings): FP32 accumulation (R20), the level floors (R17), verify-at-full (R16, R16b),
@@ -728,6 +730,7 @@ static int monitor_check(const orc_schedule* s, const ring_t* ring, double* wbuf
 static int validate_sched(const orc_schedule* s) {
   if (s->start_level < 1 || s->start_level > 3) return 0;
   if (!(s->perturb_c >= 0.0)) return 0;
+  if (s->cg_keep_direction != 0 && s->cg_keep_direction != 1) return 0;
   if (s->enabled) {
     if (s->max_level < s->start_level || s->max_level > 3) return 0;
     if (s->t < 1 || s->m < 1) return 0;
@@ -839,13 +842,23 @@ int orc_cg(const orc_matrix* A, const double* b, double* x, double tol, int64_t 
     if (escalate) {
       level++;
       log_switch(rep, j, level);
-      /* R15: the operator changed, so CG restarts from the current x at the new level:
-       * r <- b - A_new x (residual replacement), p <- r, rr <- r.r */
       orc_apply(A, level, x, q);
       rep->spmv_count[level - 1]++;
       for (int64_t i = 0; i < n; ++i) r[i] = b[i] - q[i];
-      for (int64_t i = 0; i < n; ++i) p[i] = r[i];
-      rr = vdot(n, r, r);
+      if (sched->cg_keep_direction) {
+        /* R30: residual replacement r <- b - A_new x with the search direction kept:
+         * beta = r.r / rr_{j-1}, p <- r + beta p, rr <- r.r (the CG step with the
+         * replaced residual in place of the recurrence one) */
+        double rr_rep = vdot(n, r, r);
+        double beta = rr_rep / rr;
+        for (int64_t i = 0; i < n; ++i) { double t2 = beta * p[i]; p[i] = r[i] + t2; }
+        rr = rr_rep;
+      } else {
+        /* R15: the operator changed, so CG restarts from the current x at the new level:
+         * r <- b - A_new x (residual replacement), p <- r, rr <- r.r */
+        for (int64_t i = 0; i < n; ++i) p[i] = r[i];
+        rr = vdot(n, r, r);
+      }
       resid = sqrt(rr) / bnorm;
       rep->rel_residual_recurrence = resid;
       continue;

@@ -109,6 +109,7 @@ typedef struct {
   double level_floor[2];
   int krylov_gse16; /* GMRES: Krylov basis stored as 16-bit GSE-SEM vectors (NEXT-4, R28) */
   double perturb_c; /* R29: escalate at L < 3 when resid <= c * eta_L * ||x|| / ||b||; 0 = off */
+  int cg_keep_direction; /* R30: CG switch keeps p (r = b - A_new x, p = r + beta p); 0 = R15 */
 } orc_schedule;
 
 typedef struct {

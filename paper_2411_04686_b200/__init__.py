@@ -88,7 +88,7 @@ class StepSchedule(C.Structure):
                 ("rsd_limit", C.c_double), ("ndec_limit", C.c_int64),
                 ("reldec_limit", C.c_double), ("verify_at_full", C.c_int),
                 ("level_floor", C.c_double * 2), ("krylov_gse16", C.c_int),
-                ("perturb_c", C.c_double)]
+                ("perturb_c", C.c_double), ("cg_keep_direction", C.c_int)]
 
 
 class SolveReport(C.Structure):

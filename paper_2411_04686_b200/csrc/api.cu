@@ -283,6 +283,10 @@ static gse_status check_sched(const gse_step_schedule* sc) {
     set_error("perturb_c must be finite and >= 0 (0 = off)");
     return GSE_ERR_INVALID_ARG;
   }
+  if (sc->cg_keep_direction != 0 && sc->cg_keep_direction != 1) {
+    set_error("cg_keep_direction must be 0 or 1");
+    return GSE_ERR_INVALID_ARG;
+  }
   return GSE_OK;
 }
 
@@ -614,6 +618,10 @@ static gse_status solve_common(gse_matrix A, const double* b, double* x, double 
   if (rc != GSE_OK) return rc;
   if (M.dist && sc.enabled && sc.perturb_c > 0.0) {
     set_error("the R29 perturbation trigger (perturb_c) is single-GPU only");
+    return GSE_ERR_WRONG_FORMAT;
+  }
+  if (M.dist && sc.enabled && sc.cg_keep_direction) {
+    set_error("the R30 kept direction (cg_keep_direction) is single-GPU only");
     return GSE_ERR_WRONG_FORMAT;
   }
   gse_solve_report r;

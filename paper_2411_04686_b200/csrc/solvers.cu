@@ -1748,18 +1748,43 @@ gse_status solve_cg(Matrix& M, const double* b, double* x, double tol, int64_t m
       return GSE_ERR_CUDA;
     }
     if (escalate) {
-      // R15: restart from the current x at the new level: r = b - A_new x, p = r
       level++;
       log_switch(rep, iter, level);
-      rc = residual(M, level, ws->x, ws->r, ws->p, &ws->ctrl->rr, rep, s);
-      if (rc != GSE_OK) return rc;
+      if (sched.cg_keep_direction) {
+        // R30: residual replacement at the new level, the search direction kept:
+        // r = b - A_new x ; beta = r.r / rr_old ; p = r + beta p ; rr = r.r
+        rc = residual(M, level, ws->x, ws->r, nullptr, &ws->ctrl->rr_new, rep, s);
+        if (rc != GSE_OK) return rc;
+        rc = read_ctrl(ws, s);
+        if (rc != GSE_OK) return rc;
+        const double rr_new = hc->rr_new, beta = rr_new / hc->rr;
+        rc = set_field(ws, &SolveCtrl::alpha, 0.0, s);
+        if (rc != GSE_OK) return rc;
+        rc = set_field(ws, &SolveCtrl::beta, beta, s);
+        if (rc != GSE_OK) return rc;
+        rc = set_field(ws, &SolveCtrl::event, (int)EV_NONE, s);
+        if (rc != GSE_OK) return rc;
+        launch_k(k_cg_xpay<false>, ws->vgrid, 256, 0, s, ws->ctrl, ws->x, ws->p,
+                 (const double*)ws->r, n, ws->partials, ws->ticket);  // alpha = 0: p only
+        GSE_CUDA_TRY(cudaGetLastError());
+        rc = set_field(ws, &SolveCtrl::rr, rr_new, s);
+        if (rc != GSE_OK) return rc;
+      } else {
+        // R15: restart from the current x at the new level: r = b - A_new x, p = r
+        rc = residual(M, level, ws->x, ws->r, ws->p, &ws->ctrl->rr, rep, s);
+        if (rc != GSE_OK) return rc;
+      }
       rc = set_field(ws, &SolveCtrl::level, level, s);
       if (rc != GSE_OK) return rc;
       rc = set_field(ws, &SolveCtrl::event, (int)EV_NONE, s);
       if (rc != GSE_OK) return rc;
-      for (double SolveCtrl::*f : {&SolveCtrl::alpha, &SolveCtrl::beta}) {
-        rc = set_field(ws, f, 0.0, s);
-        if (rc != GSE_OK) return rc;
+      // (R30 already set them; a second set_field of beta would race its pinned staging
+      // with the p-update kernel's read)
+      if (!sched.cg_keep_direction) {
+        for (double SolveCtrl::*f : {&SolveCtrl::alpha, &SolveCtrl::beta}) {
+          rc = set_field(ws, f, 0.0, s);
+          if (rc != GSE_OK) return rc;
+        }
       }
       if (iter >= max_iters) {
         status = GSE_NOT_CONVERGED;

@@ -25,7 +25,8 @@ out["fp64_csr"] = {"ms": round(t64, 2), "it": r64["iterations"]}
 for start in (1, 2):
     for c in [float(v) for v in os.environ.get("R29_CS", "0.1,1,3,10").split(",")]:
         t, r = bench._solve_ms(g, stream, flush, "cg", M, b, x,
-                               g.gse_default_schedule("cg", perturb_c=c, start_level=start))
+                               g.gse_default_schedule("cg", perturb_c=c, start_level=start,
+                                                     cg_keep_direction=int(os.environ.get("GSE_CG_KEEP", "0"))))
         out[f"s{start}_c{c}"] = {"ms": round(t, 2), "it": r["iterations"], "per_level": r["iters_per_level"],
                                  "switch": r["switch_iter"], "res": r["rel_residual_true"],
                                  "x_fp64": round(t64 / t, 3)}

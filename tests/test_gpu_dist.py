@@ -427,6 +427,12 @@ def test_dist_single_gpu_only_options_are_refused(g):
             errs.append(None)
         except g.GseError as e:
             errs.append(e.status)
+        try:  # R30 kept direction: single-GPU only too
+            g.gse_solve_cg(M, dev(b[a:bb].copy()), tol=1e-10, stream=st.cuda_stream,
+                           sched=g.gse_default_schedule("cg", cg_keep_direction=1))
+            errs.append(None)
+        except g.GseError as e:
+            errs.append(e.status)
         _, rep = g.gse_solve_cg(M, dev(b[a:bb].copy()), tol=1e-10, stream=st.cuda_stream,
                                 sched=g.gse_default_schedule("cg", l=30, t=10, m=10))
         st.synchronize()
@@ -435,5 +441,5 @@ def test_dist_single_gpu_only_options_are_refused(g):
 
     outs = run_ranks(2, fn)
     for errs, rep in outs:
-        assert errs == [g.GSE_ERR_WRONG_FORMAT] * 3
+        assert errs == [g.GSE_ERR_WRONG_FORMAT] * 4
         assert rep["converged"]

@@ -570,6 +570,47 @@ def test_perturbation_trigger_parity(g, solver, c):
                                                                r_plain["switch_iter"])
 
 
+@pytest.mark.parametrize("start,c", [(1, 0.1), (1, 1.0), (2, 3.0), (1, 1e300)])
+def test_kept_direction_parity(g, start, c):
+    """R30 (CG switch keeps p: r = b - A_new x, p = r + (r.r / rr_{j-1}) p) on the GPU
+    against the oracle: iterations +-2, switch points +-2, residual ratio"""
+    A = gi.poisson3d(16, "varcoef")
+    b = gi.ones_rhs(A)
+    M, R = enc_both(g, A)
+    kw = dict(perturb_c=c, start_level=start, cg_keep_direction=1)
+    _, rg = g.gse_solve_cg(M, b, tol=1e-10, sched=g.gse_default_schedule("cg", **kw))
+    _, ro = O.cg(R, b, tol=1e-10, sched=O.schedule("cg", **kw))
+    _cmp_reports(rg, ro)
+    assert rg["n_switches"] == ro.n_switches == 3 - start
+    for a_, b_ in zip(rg["switch_iter"], ro.switch_iter):
+        assert abs(a_ - b_) <= 2
+    assert rg["converged"] and rg["rel_residual_true"] <= 1e-10
+
+
+def test_kept_direction_exact_levels_gpu(g):
+    """R30 on a head-exact matrix with floor-forced switches: the GPU's kept-direction solve
+    takes the fixed-level iteration count (within 1), the R15 restart more -- as the
+    oracle's pin (tests/test_oracle_spmv_solvers.py)"""
+    A = gi.poisson3d(14)
+    b = gi.ones_rhs(A)
+    M, _ = enc_both(g, A)
+    kw = dict(level_floor=(1e-2, 1e-5))
+    _, r3 = g.gse_solve_cg(M, b, tol=1e-10, sched=g.fixed_schedule(3))
+    _, rk = g.gse_solve_cg(M, b, tol=1e-10, sched=g.gse_default_schedule("cg", cg_keep_direction=1, **kw))
+    _, rr_ = g.gse_solve_cg(M, b, tol=1e-10, sched=g.gse_default_schedule("cg", **kw))
+    assert rk["n_switches"] == rr_["n_switches"] == 2
+    assert abs(rk["iterations"] - r3["iterations"]) <= 1
+    assert rr_["iterations"] >= r3["iterations"] + 5
+
+
+def test_kept_direction_rejects_bad_value(g):
+    A = gi.poisson3d(4)
+    M, _ = enc_both(g, A)
+    with pytest.raises(g.GseError) as e:
+        g.gse_solve_cg(M, gi.ones_rhs(A), sched=g.gse_default_schedule("cg", cg_keep_direction=2))
+    assert e.value.status == g.GSE_ERR_INVALID_ARG
+
+
 @pytest.mark.parametrize("mode", ["stepped_scaled", "stepped", "fp64"])
 def test_cg_graph_unroll_invariant(g, mode, monkeypatch):
     """the CG graph's while body holds GSE_CG_UNROLL iterations; the kernels after an event
@@ -617,7 +658,7 @@ def test_cg_parity_c2_full_size(g):
     assert res <= 1e-10 * 1.001
 
 
-@pytest.mark.parametrize("sched", ["default", "floors", "r29"])
+@pytest.mark.parametrize("sched", ["default", "floors", "r29", "r29_keep_l2"])
 def test_cg_parity_c2_varcoef_full_size_switching(g, sched):
     """configs[1] shape with varcoef values (head-lossy): full-size stepped CG that SWITCHES
     levels -- paper defaults (verify-at-full escalations, R16), level floors (R17) and the R29
@@ -626,13 +667,14 @@ def test_cg_parity_c2_varcoef_full_size_switching(g, sched):
     A = gi.poisson3d(128, "varcoef")
     b = gi.ones_rhs(A)
     M, R = enc_both(g, A, device_inputs=True)
-    kw = {"default": {}, "floors": {"level_floor": (1e-3, 1e-8)}, "r29": {"perturb_c": 0.1}}[sched]
+    kw = {"default": {}, "floors": {"level_floor": (1e-3, 1e-8)}, "r29": {"perturb_c": 0.1},
+          "r29_keep_l2": {"perturb_c": 3.0, "start_level": 2, "cg_keep_direction": 1}}[sched]
     _, rg = g.gse_solve_cg(M, torch.from_numpy(b).cuda(), tol=1e-10,
                            sched=g.gse_default_schedule("cg", **kw))
     O.set_threads(0)
     _, ro = O.cg(R, b, tol=1e-10, sched=O.schedule("cg", **kw))
     _cmp_reports(rg, ro)
-    assert rg["n_switches"] == ro.n_switches == 2
+    assert rg["n_switches"] == ro.n_switches == (1 if sched == "r29_keep_l2" else 2)
     for a_, b_ in zip(rg["switch_iter"], ro.switch_iter):
         assert abs(a_ - b_) <= 2, (rg, ro)
     assert rg["converged"] and rg["rel_residual_true"] <= 1e-10

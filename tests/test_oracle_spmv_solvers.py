@@ -392,15 +392,17 @@ def test_perturbation_trigger_behaviour(solver):
     assert rc.iterations < r0.iterations
 
 
-def test_perturbation_trigger_matches_independent_numpy_cg():
+@pytest.mark.parametrize("keep,c", [(0, 0.1), (1, 0.1), (1, 3.0)])
+def test_perturbation_trigger_matches_independent_numpy_cg(keep, c):
     """The oracle's R29 switch points against a plain numpy CG on the decoded level
     matrices (scipy CSR products, BLAS dots) with the same rule: escalate when
-    ||r||/||b|| <= c eta_L ||x_{j-1}|| / ||b||, restart r = b - A_new x, p = r."""
+    ||r||/||b|| <= c eta_L ||x_{j-1}|| / ||b||; at a switch r = b - A_new x and either the
+    R15 restart p = r or the R30 kept direction p = r + (r.r / rr_{j-1}) p."""
     import scipy.sparse as sp
     A = gi.poisson3d(10, "varcoef")
     G = enc(A)
     b = gi.ones_rhs(A)
-    c, tol = 0.1, 1e-10
+    tol = 1e-10
     eta = O.perturbation_bounds(G)
     mats = {L: sp.csr_matrix((O.decode_all(G, L), A.col, A.row_ptr), shape=(A.rows, A.cols))
             for L in (1, 2, 3)}
@@ -427,14 +429,48 @@ def test_perturbation_trigger_matches_independent_numpy_cg():
             L += 1
             sw.append(j)
             r = b - mats[L] @ x
-            p, rr = r.copy(), r @ r
+            if keep:
+                rn = r @ r
+                p = r + (rn / rr) * p
+                rr = rn
+            else:
+                p, rr = r.copy(), r @ r
             continue
         p = r + (rn / rr) * p
         rr = rn
-    _, rep = O.cg(G, b, tol=tol, sched=O.schedule("cg", perturb_c=c))
+    _, rep = O.cg(G, b, tol=tol, sched=O.schedule("cg", perturb_c=c, cg_keep_direction=keep))
+    assert rep.converged and rep.rel_residual_true <= tol
     assert len(sw) == rep.n_switches == 2
     assert all(abs(a_ - b_) <= 1 for a_, b_ in zip(sw, rep.switch_iter))
     assert abs(j - rep.iterations) <= 2
+
+
+def test_kept_direction_is_a_pure_residual_replacement_on_exact_levels():
+    """R30 on a head-exact matrix (Poisson const: A_1 = A_2 = A_3), switches forced by the
+    level floors (R17): r = b - A_new x equals the recurrence residual up to rounding, so
+    keeping p continues the same Krylov process -- the iteration count is the fixed-level
+    CG's (within 1) -- while the R15 restart p = r discards the search directions and needs
+    more iterations (both take the first switch at the same iteration, the restarted solve
+    reaches the second floor later)."""
+    A = gi.poisson3d(14)
+    G = enc(A)
+    b = gi.ones_rhs(A)
+    _, r3 = O.cg(G, b, tol=1e-10, sched=O.fixed_schedule(3))
+    kw = dict(level_floor=(1e-2, 1e-5))
+    _, rk = O.cg(G, b, tol=1e-10, sched=O.schedule("cg", cg_keep_direction=1, **kw))
+    _, rr_ = O.cg(G, b, tol=1e-10, sched=O.schedule("cg", **kw))
+    assert rk.n_switches == rr_.n_switches == 2
+    assert rk.switch_iter[0] == rr_.switch_iter[0] and rk.switch_iter[1] < rr_.switch_iter[1]
+    assert abs(rk.iterations - r3.iterations) <= 1
+    assert rr_.iterations >= r3.iterations + 5
+    assert rk.converged and rk.rel_residual_true <= 1e-10
+
+
+def test_kept_direction_schedule_validation():
+    """cg_keep_direction is 0 or 1 (anything else: invalid argument)"""
+    A = gi.poisson3d(4)
+    with pytest.raises(O.OracleError):
+        O.cg(enc(A), gi.ones_rhs(A), sched=O.schedule("cg", cg_keep_direction=2))
 
 
 # ------------------------------------------------------------------ independent iteration gauges
