@@ -196,7 +196,9 @@ gse_status gse_spmv_dot(gse_matrix A, const double* x, double* y, int segments, 
 typedef struct {
   int enabled;                 /* 1: stepped (Alg. stepped-GMRES); 0: fixed start_level     */
   int start_level, max_level;  /* 1..3 (A_1 head, A_2 head+tail1, A_3 full)          */
-  int64_t l, t, m;             /* first check at l, window t, period m (t < l)        */
+  int64_t l, t, m;             /* first check at l, window t, period m (t < l in the
+                                * paper's settings; t >= l is accepted -- a check also needs a
+                                * full window of t + 1 residuals, so the first one waits)     */
   double rsd_limit;            /* Condition 1, Eq. 3                                  */
   int64_t ndec_limit;          /* replaces t/2 in Conditions 1-2 (R13)                */
   double reldec_limit;         /* Condition 2, Eq. 6                                  */
