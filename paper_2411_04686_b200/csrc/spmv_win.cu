@@ -157,9 +157,20 @@ struct WinStash {  // per warp, double-buffered across tiles
 #define GSE_WIN_MINB_HI 3
 #endif
 #define WIN_MINB(L) ((L) == 3 || (L) == 0 ? GSE_WIN_MINB_HI : GSE_WIN_MINB_LO)
+// 4 resident CTAs (64 registers) where that measured faster on C3: level 1 (FP64: 550 ->
+// 526 us, FP32 428 -> 401 us) and level 2 with FP32 accumulation (447 -> 419 us); level 2
+// FP64 and the fused-dot variants spill more at 64 registers and keep 3
+// (profiles/r02k/win_c3_minb4.json vs win_c3_base_same_run_as_minb4.json)
+#ifndef GSE_WIN_MINB4
+#define GSE_WIN_MINB4 1
+#endif
+template <int L, bool DOT, class T>
+constexpr int win_minb() {
+  return (GSE_WIN_MINB4 && !DOT && (L == 1 || (L == 2 && sizeof(T) == 4))) ? 4 : WIN_MINB(L);
+}
 
 template <int L, bool SIDE, bool DOT, bool FAST, bool EMPTY, class T>
-__global__ void __launch_bounds__(WIN_THREADS, WIN_MINB(L)) k_spmv_win(const SpmvParams<T> p) {
+__global__ void __launch_bounds__(WIN_THREADS, (win_minb<L, DOT, T>())) k_spmv_win(const SpmvParams<T> p) {
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t bars[2];
   __shared__ long long sd64[64];
