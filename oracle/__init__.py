@@ -137,6 +137,10 @@ def _declare(L):
     L.orc_default_schedule.restype = None
     L.orc_cg.argtypes = [_p(OrcMatrix), _p(dbl), _p(dbl), dbl, i64, _p(OrcSchedule),
                          _p(OrcReport)]
+    L.orc_cg_part.argtypes = [_p(OrcMatrix), _p(dbl), _p(dbl), dbl, i64, _p(OrcSchedule), i32,
+                              _p(i64), _p(OrcReport)]
+    L.orc_gmres_part.argtypes = [_p(OrcMatrix), _p(dbl), _p(dbl), dbl, i32, i64, _p(OrcSchedule),
+                                 i32, _p(i64), _p(OrcReport)]
     L.orc_gmres.argtypes = [_p(OrcMatrix), _p(dbl), _p(dbl), dbl, i32, i64, _p(OrcSchedule),
                             _p(OrcReport)]
     L.orc_set_threads.argtypes = [i32]
@@ -562,28 +566,45 @@ def _report(st, r: OrcReport) -> Report:
                   r.rel_residual_recurrence, r.rel_residual_true, tuple(r.spmv_count))
 
 
-def cg(A, b, x0=None, tol=1e-10, max_iters=5000, sched: OrcSchedule | None = None):
+def _bounds(parts):
+    bd = np.ascontiguousarray(parts, dtype=np.int64)
+    return len(bd) - 1, bd
+
+
+def cg(A, b, x0=None, tol=1e-10, max_iters=5000, sched: OrcSchedule | None = None, parts=None):
+    """parts: row-block bounds [0, ..., rows] -> c.1 step 10 partitioned mode"""
     m = A.orc()
     bb = _arr(b)
     x = np.zeros(A.rows, np.float64) if x0 is None else _arr(x0).copy()
     s = sched if sched is not None else fixed_schedule(3)
     rep = OrcReport()
-    st = lib().orc_cg(C.byref(m), _ptr(bb, C.c_double), _ptr(x, C.c_double), tol, max_iters,
-                      C.byref(s), C.byref(rep))
+    if parts is None:
+        st = lib().orc_cg(C.byref(m), _ptr(bb, C.c_double), _ptr(x, C.c_double), tol, max_iters,
+                          C.byref(s), C.byref(rep))
+    else:
+        P, bd = _bounds(parts)
+        st = lib().orc_cg_part(C.byref(m), _ptr(bb, C.c_double), _ptr(x, C.c_double), tol,
+                               max_iters, C.byref(s), P, _ptr(bd, C.c_int64), C.byref(rep))
     if st >= 10:
         raise OracleError(st, "cg")
     return x, _report(st, rep)
 
 
 def gmres(A, b, x0=None, tol=1e-10, restart=30, max_iters=15000,
-          sched: OrcSchedule | None = None):
+          sched: OrcSchedule | None = None, parts=None):
     m = A.orc()
     bb = _arr(b)
     x = np.zeros(A.rows, np.float64) if x0 is None else _arr(x0).copy()
     s = sched if sched is not None else fixed_schedule(3)
     rep = OrcReport()
-    st = lib().orc_gmres(C.byref(m), _ptr(bb, C.c_double), _ptr(x, C.c_double), tol, restart,
-                         max_iters, C.byref(s), C.byref(rep))
+    if parts is None:
+        st = lib().orc_gmres(C.byref(m), _ptr(bb, C.c_double), _ptr(x, C.c_double), tol, restart,
+                             max_iters, C.byref(s), C.byref(rep))
+    else:
+        P, bd = _bounds(parts)
+        st = lib().orc_gmres_part(C.byref(m), _ptr(bb, C.c_double), _ptr(x, C.c_double), tol,
+                                  restart, max_iters, C.byref(s), P, _ptr(bd, C.c_int64),
+                                  C.byref(rep))
     if st >= 10:
         raise OracleError(st, "gmres")
     return x, _report(st, rep)

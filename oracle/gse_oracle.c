@@ -18,7 +18,9 @@
  * literal transcriptions of Alg. 1 / Alg. 2 in the tests; scipy CG / GMRES(30) iteration
  * gauges; the R29 bound eta_L against a closed form; the R30 kept-direction switch against
  * an independent numpy CG and, on a head-exact matrix with forced switches, against the
- * fixed-level CG's iteration count (a pure residual replacement leaves CG unchanged).
+ * fixed-level CG's iteration count (a pure residual replacement leaves CG unchanged); the
+ * partitioned mode (c.1 step 10, orc_cg_part / orc_gmres_part) against an independent numpy
+ * CG with per-rank sequential dots summed in rank order (identical iterations and switches).
  *
  * Parity unpinned by the paper (pinned only by agreement with this file under the DESIGN.md
  * readings): FP32 accumulation (R20), the level floors (R17), verify-at-full (R16, R16b),
@@ -677,13 +679,41 @@ void orc_default_schedule(int solver, orc_schedule* s) {
 }
 
 /* ---- plain FP64 vector helpers (sequential, index order) ---- */
-static double vdot(int64_t n, const double* a, const double* b) {
+static double vdot_seq(int64_t n, const double* a, const double* b) {
   double s = 0.0;
   for (int64_t i = 0; i < n; ++i) {
     double p = a[i] * b[i];
     s = s + p;
   }
   return s;
+}
+
+/* c.1 step 10 (partitioned mode): the solvers' vectors are split into P
+ * row blocks [bounds[r], bounds[r+1]) as the row-partitioned GPU path splits them; every
+ * dot product is summed per simulated rank (sequentially, as vdot_seq) and the P partial
+ * sums are added in rank order (the allreduce).  SpMV rows are independent, so a rank's
+ * rows -- computed with the halo entries of x gathered -- are the same numbers as in the
+ * single-rank product.  Set only for the duration of orc_cg_part / orc_gmres_part. */
+static __thread int t_parts = 0;
+static __thread const int64_t* t_bounds = NULL;
+
+static double vdot(int64_t n, const double* a, const double* b) {
+  if (t_parts > 1 && t_bounds[t_parts] == n) {
+    double s = 0.0;
+    for (int r = 0; r < t_parts; ++r) {
+      const int64_t lo = t_bounds[r], hi = t_bounds[r + 1];
+      s = s + vdot_seq(hi - lo, a + lo, b + lo);
+    }
+    return s;
+  }
+  return vdot_seq(n, a, b);
+}
+
+static int valid_parts(const orc_matrix* A, int P, const int64_t* bounds) {
+  if (P < 1 || !bounds || bounds[0] != 0 || bounds[P] != A->rows) return 0;
+  for (int r = 0; r < P; ++r)
+    if (bounds[r + 1] < bounds[r]) return 0;
+  return 1;
 }
 
 /* ring of the last t+1 residuals */
@@ -1033,4 +1063,30 @@ done:
   if (n > 0 && bnorm > 0.0) rep->rel_residual_true = true_resid(A, 3, b, x, w, bnorm, rep);
   free(V); free(w); free(H); free(cs); free(sn); free(g); free(yv); free(ring.buf); free(wbuf);
   return status;
+}
+
+/* c.1 step 10: CG / GMRES(m) in partitioned mode (P simulated ranks, row blocks
+ * [bounds[r], bounds[r+1]), dots summed per rank then in rank order).  P = 1 is orc_cg /
+ * orc_gmres exactly. */
+int orc_cg_part(const orc_matrix* A, const double* b, double* x, double tol, int64_t max_iters,
+                const orc_schedule* sched, int P, const int64_t* bounds, orc_report* rep) {
+  if (!valid_parts(A, P, bounds)) return ORC_ERR_INVALID_ARG;
+  t_parts = P;
+  t_bounds = bounds;
+  int st = orc_cg(A, b, x, tol, max_iters, sched, rep);
+  t_parts = 0;
+  t_bounds = NULL;
+  return st;
+}
+
+int orc_gmres_part(const orc_matrix* A, const double* b, double* x, double tol, int restart,
+                   int64_t max_iters, const orc_schedule* sched, int P, const int64_t* bounds,
+                   orc_report* rep) {
+  if (!valid_parts(A, P, bounds)) return ORC_ERR_INVALID_ARG;
+  t_parts = P;
+  t_bounds = bounds;
+  int st = orc_gmres(A, b, x, tol, restart, max_iters, sched, rep);
+  t_parts = 0;
+  t_bounds = NULL;
+  return st;
 }

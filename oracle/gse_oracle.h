@@ -132,6 +132,14 @@ int orc_cg(const orc_matrix* A, const double* b, double* x, double tol, int64_t 
            const orc_schedule* sched, orc_report* rep);
 int orc_gmres(const orc_matrix* A, const double* b, double* x, double tol, int restart,
               int64_t max_iters, const orc_schedule* sched, orc_report* rep);
+/* c.1 step 10 partitioned mode: P simulated ranks own rows [bounds[r], bounds[r+1])
+ * (bounds[0] = 0, bounds[P] = rows, non-decreasing); dots summed per rank, then in rank
+ * order.  ORC_ERR_INVALID_ARG for bad bounds. */
+int orc_cg_part(const orc_matrix* A, const double* b, double* x, double tol, int64_t max_iters,
+                const orc_schedule* sched, int P, const int64_t* bounds, orc_report* rep);
+int orc_gmres_part(const orc_matrix* A, const double* b, double* x, double tol, int restart,
+                   int64_t max_iters, const orc_schedule* sched, int P, const int64_t* bounds,
+                   orc_report* rep);
 
 /* cost of the oracle's plain threads knob (GSE_THREADS); returns threads used */
 int orc_set_threads(int n);

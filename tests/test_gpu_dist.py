@@ -143,6 +143,40 @@ def test_dist_cg(g, P, variant):
 
 
 @pytest.mark.parametrize("P", [2, 3])
+def test_dist_cg_vs_partitioned_oracle(g, P):
+    """the row-partitioned GPU CG (R29-free scaled schedule; thread backend) against the
+    oracle's partitioned mode with the same row blocks: iterations
+    and switch points within 2, true residual <= tol"""
+    A = gi.poisson3d(16, "varcoef")
+    b = gi.ones_rhs(A)
+    rr = partition(A.rows, P)
+    kw = dict(l=30, t=10, m=10)
+
+    def fn(r, D, st):
+        a, bb = rr[r], rr[r + 1]
+        rp, col, val = slab(A, a, bb)
+        dev = lambda v: torch.from_numpy(v).cuda()
+        M = g.gse_encode_dist(D, dev(rp), dev(col), dev(val), a, A.rows, stream=st.cuda_stream)
+        x, rep = g.gse_solve_cg(M, dev(b[a:bb].copy()), tol=1e-10,
+                                sched=g.gse_default_schedule("cg", **kw), stream=st.cuda_stream)
+        st.synchronize()
+        M.close()
+        return x.cpu().numpy(), rep
+
+    outs = run_ranks(P, fn)
+    rep = outs[0][1]
+    R = O.encode_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+    _, ro = O.cg(R, b, tol=1e-10, sched=O.schedule("cg", **kw), parts=rr)
+    assert rep["converged"] and abs(rep["iterations"] - ro.iterations) <= 2, (rep, ro)
+    assert rep["n_switches"] == ro.n_switches
+    for a_, b_ in zip(rep["switch_iter"], ro.switch_iter):
+        assert abs(a_ - b_) <= 2
+    x = np.concatenate([xx for xx, _ in outs])
+    F = O.fp64_csr(A.rows, A.cols, A.row_ptr, A.col, A.val)
+    assert np.linalg.norm(b - O.spmv_fp64(F, x)) / np.linalg.norm(b) <= 1e-10 * 1.01
+
+
+@pytest.mark.parametrize("P", [2, 3])
 @pytest.mark.parametrize("mode", ["fp64", "stepped_scaled"])
 def test_dist_gmres(g, P, mode):
     """row-partitioned GMRES(30) (halo per SpMV, one allreduce per MGS dot and norm): every

@@ -473,6 +473,95 @@ def test_kept_direction_schedule_validation():
         O.cg(enc(A), gi.ones_rhs(A), sched=O.schedule("cg", cg_keep_direction=2))
 
 
+# ------------------------------------------------------------------ c.1 step 10: partitioned mode
+def _parts(n, P):
+    return [round(i * n / P) for i in range(P + 1)]
+
+
+def _seq_dot(a, b):
+    """sequential left-to-right sum of the rounded products (np.cumsum accumulates in order)"""
+    return float(np.cumsum(a * b)[-1]) if len(a) else 0.0
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_partitioned_cg_matches_independent_rank_loop(P):
+    """the oracle's partitioned CG (R29-stepped, so the switching
+    logic runs on the rank-summed dots) against an independent numpy CG in which every dot
+    is a per-rank sequential sum added in rank order and each rank's SpMV rows come from the
+    decoded level matrices (scipy CSR): same iteration count and switch points, same x to
+    1e-13 relative"""
+    import scipy.sparse as sp
+    A = gi.poisson3d(10, "varcoef")
+    G = enc(A)
+    b = gi.ones_rhs(A)
+    parts = _parts(A.rows, P)
+    c, tol = 0.1, 1e-10
+    eta = O.perturbation_bounds(G)
+    mats = {L: sp.csr_matrix((O.decode_all(G, L), A.col, A.row_ptr), shape=(A.rows, A.cols))
+            for L in (1, 2, 3)}
+
+    def dot(u, v):
+        s = 0.0
+        for r in range(P):
+            s = s + _seq_dot(u[parts[r]:parts[r + 1]], v[parts[r]:parts[r + 1]])
+        return s
+
+    nb = np.sqrt(dot(b, b))
+    x = np.zeros(A.rows)
+    L, r = 1, b - mats[1] @ x
+    p, rr, sw, j = r.copy(), dot(r, r), [], 0
+    while j < 2000:
+        j += 1
+        q = mats[L] @ p
+        pq = dot(p, q)
+        xx = dot(x, x)
+        al = rr / pq
+        x = x + al * p
+        r = r - al * q
+        rn = dot(r, r)
+        res = np.sqrt(rn) / nb
+        if res <= tol:
+            if L == 3 or np.sqrt(dot(b - mats[3] @ x, b - mats[3] @ x)) / nb <= tol:
+                break
+            esc = True
+        else:
+            esc = L < 3 and xx > 0 and res <= c * eta[L - 1] * np.sqrt(xx) / nb
+        if esc:
+            L += 1
+            sw.append(j)
+            r = b - mats[L] @ x
+            p, rr = r.copy(), dot(r, r)
+            continue
+        p = r + (rn / rr) * p
+        rr = rn
+    xo, rep = O.cg(G, b, tol=tol, sched=O.schedule("cg", perturb_c=c), parts=parts)
+    assert tuple(sw) == rep.switch_iter and j == rep.iterations
+    assert np.abs(xo - x).max() <= 1e-13 * np.abs(x).max()
+
+
+@pytest.mark.parametrize("solver", ["cg", "gmres"])
+def test_partitioned_mode_properties(solver):
+    """P = 1 is the unpartitioned solver bit for bit; P = 2, 3, 7 (uneven blocks, an empty
+    block) change only the dot order: iterations within 2, the same switches, true residual
+    <= tol; malformed bounds are rejected"""
+    A = gi.poisson3d(12, "varcoef") if solver == "cg" else gi.convdiff3d(10)
+    G = enc(A)
+    b = gi.ones_rhs(A)
+    run = O.cg if solver == "cg" else O.gmres
+    sch = lambda: O.schedule(solver, perturb_c=0.1)
+    x0, r0 = run(G, b, tol=1e-10, sched=sch())
+    x1, r1 = run(G, b, tol=1e-10, sched=sch(), parts=[0, A.rows])
+    assert np.array_equal(x0, x1) and r1.iterations == r0.iterations
+    n = A.rows
+    for parts in (_parts(n, 2), _parts(n, 3), [0, 5, 5, n // 3, n // 2, n - 1, n - 1, n]):
+        x, r = run(G, b, tol=1e-10, sched=sch(), parts=parts)
+        assert r.converged and r.rel_residual_true <= 1e-10
+        assert abs(r.iterations - r0.iterations) <= 2 and r.n_switches == r0.n_switches
+    for bad in ([0, n + 1], [1, n], [0, n // 2, n // 3, n]):
+        with pytest.raises(O.OracleError):
+            run(G, b, tol=1e-10, sched=sch(), parts=bad)
+
+
 # ------------------------------------------------------------------ independent iteration gauges
 @pytest.mark.parametrize("N,gauge", [(16, 46), (32, 93)])
 def test_cg_iteration_gauges(N, gauge):
