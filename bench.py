@@ -772,7 +772,8 @@ def sub_c3(dev, stream, flush, peak):
 
 def sub_c4(dev, stream, flush):
     """configs[3]: conv-diff 256^3 restarted GMRES(30) to a true relative residual of 1e-10
-    (and the paper's 1e-6): FP64-CSR vs stepped GSE (paper defaults, level floors, R29)"""
+    (and the paper's 1e-6): FP64-CSR vs stepped GSE (paper defaults, level floors, R29, R29
+    from level 2)"""
     import torch
     import gse_inputs as gi
     import paper_2411_04686_b200 as g
@@ -792,6 +793,9 @@ def sub_c4(dev, stream, flush):
         if tol == 1e-10:
             runs.append(("stepped_floors", g.gse_default_schedule("gmres", level_floor=(1e-3, 1e-8))))
             runs.append(("stepped_r29", g.gse_default_schedule("gmres", perturb_c=R29_C)))
+            # the R29 trigger from level 2 (head + tail1): one switch, near the end
+            runs.append(("stepped_r29_l2", g.gse_default_schedule("gmres", perturb_c=R29_C,
+                                                                  start_level=2)))
         for name, s in runs:
             t, r = _solve_ms(g, stream, flush, "gmres", M, b, x, s, tol)
             out[name + tag] = {"ms": r3(t), "it": r["iterations"], "per_level": r["iters_per_level"],
