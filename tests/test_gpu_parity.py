@@ -680,14 +680,15 @@ def test_cg_parity_c2_varcoef_full_size_switching(g, sched):
     assert rg["converged"] and rg["rel_residual_true"] <= 1e-10
 
 
-@pytest.mark.parametrize("sched", ["floors", "r29"])
+@pytest.mark.parametrize("sched", ["floors", "r29", "r29_l2"])
 def test_gmres_parity_convdiff64_switching(g, sched):
     """C4-shaped conv-diff at 64^3: stepped GMRES(30) that switches levels against the
     oracle (iterations +-2, switch points +-2, residual ratio)"""
     A = gi.convdiff3d(64)
     b = gi.ones_rhs(A)
     M, R = enc_both(g, A, device_inputs=True)
-    kw = {"floors": {"level_floor": (1e-3, 1e-8)}, "r29": {"perturb_c": 0.1}}[sched]
+    kw = {"floors": {"level_floor": (1e-3, 1e-8)}, "r29": {"perturb_c": 0.1},
+          "r29_l2": {"perturb_c": 0.1, "start_level": 2}}[sched]
     _, rg = g.gse_solve_gmres(M, torch.from_numpy(b).cuda(), tol=1e-10,
                               sched=g.gse_default_schedule("gmres", **kw))
     O.set_threads(0)
