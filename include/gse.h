@@ -248,7 +248,8 @@ void gse_default_schedule(int solver /* 0 = CG, 1 = GMRES */, gse_step_schedule*
 /* Unpreconditioned CG with the stepped driver: w = A_tag p each iteration; the
  * monitor (Eqs. 3-6, Conditions 1-3) sees ||r_j||/||b|| after iteration j, checks at
  * j >= l, (j - l) % m == 0, window of t+1 full; one level per trigger (R12); at a switch
- * CG restarts from the current x with r = b - A_new x, p = r (R15).  b[n], x[n] (in: x0,
+ * CG restarts from the current x with r = b - A_new x, p = r (R15), or keeps its direction,
+ * p = r + (r.r / rr) p (R30, sched->cg_keep_direction = 1).  b[n], x[n] (in: x0,
  * out: solution); n = rows = cols.  Returns OK (converged), NOT_CONVERGED, NUMERICAL_ABORT
  * or an error; rep may be NULL.  sched NULL = fixed level 3. */
 gse_status gse_solve_cg(gse_matrix A, const double* b, double* x, double tol, int64_t max_iters,
