@@ -329,7 +329,8 @@ def run_reference(args, world, rank, pg):
     iters_full = int(round(n128 * args.N / 128))
     t1 = oracle_iters(O, R, b, 1 if args.N > 256 else 8)
     times = []
-    if t_enc + t1 * iters_full < 30.0:
+    # (GSE_REF_FULL_S: the budget for running full solves instead of sampled iterations)
+    if t_enc + t1 * iters_full < float(os.environ.get("GSE_REF_FULL_S", "30")):
         # a full oracle solve costs seconds: each step IS the workload (oracle encode +
         # stepped CG to a true relative residual of 1e-10), nothing extrapolated
         its = []
