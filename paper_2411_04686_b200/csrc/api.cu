@@ -348,6 +348,7 @@ void gse_default_schedule(int solver, gse_step_schedule* o) {
 
 gse_status gse_encode(const gse_csr_f64* A, const gse_encode_opts* opts, gse_matrix* out,
                       void* stream) {
+  gse::NvtxRange nvtx_("gse_encode");
   gse_encode_opts o = {8, -1, 0, 0, 0};
   if (opts) o = *opts;
   if (o.k_max < 1 || o.k_max > 64 || (o.k_max & (o.k_max - 1))) {
@@ -363,12 +364,14 @@ gse_status gse_encode(const gse_csr_f64* A, const gse_encode_opts* opts, gse_mat
 }
 
 gse_status gse_fp64_matrix(const gse_csr_f64* A, int device, gse_matrix* out, void* stream) {
+  gse::NvtxRange nvtx_("gse_fp64_matrix");
   return create_from_csr(A, GSE_KIND_FP64, 1, device, out, (cudaStream_t)stream, nullptr, nullptr,
                          nullptr);
 }
 
 gse_status gse_half_matrix(const gse_csr_f64* A, int kind, int device, gse_matrix* out,
                            void* stream) {
+  gse::NvtxRange nvtx_("gse_half_matrix");
   if (kind != GSE_KIND_FP16 && kind != GSE_KIND_BF16) {
     set_error("kind must be GSE_KIND_FP16 or GSE_KIND_BF16");
     return GSE_ERR_INVALID_ARG;
@@ -440,6 +443,7 @@ gse_status gse_matrix_copy_planes(gse_matrix A, uint32_t* col_ei, uint8_t* side_
 }
 
 gse_status gse_decode(gse_matrix A, int segments, double* values, void* stream) {
+  gse::NvtxRange nvtx_("gse_decode");
   if (!A || segments < 1 || segments > 3) {
     set_error("invalid matrix or segments (must be 1, 2 or 3)");
     return GSE_ERR_INVALID_ARG;
@@ -463,6 +467,7 @@ gse_status gse_decode(gse_matrix A, int segments, double* values, void* stream) 
 }
 
 gse_status gse_spmv(gse_matrix A, const double* x, double* y, int segments, void* stream) {
+  gse::NvtxRange nvtx_("gse_spmv");
   if (!A || segments < 1 || segments > 3) {
     set_error("invalid matrix or segments (must be 1, 2 or 3)");
     return GSE_ERR_INVALID_ARG;
@@ -500,6 +505,7 @@ gse_status gse_spmv(gse_matrix A, const double* x, double* y, int segments, void
 
 gse_status gse_spmv_dot(gse_matrix A, const double* x, double* y, int segments, double* dot,
                         void* stream) {
+  gse::NvtxRange nvtx_("gse_spmv_dot");
   if (!A || segments < 1 || segments > 3 || !dot) {
     set_error("invalid matrix, segments (must be 1, 2 or 3) or NULL dot");
     return GSE_ERR_INVALID_ARG;
@@ -540,6 +546,7 @@ gse_status gse_spmv_dot(gse_matrix A, const double* x, double* y, int segments, 
 }
 
 gse_status gse_perturbation_bounds(gse_matrix A, double* eta, void* stream) {
+  gse::NvtxRange nvtx_("gse_perturbation_bounds");
   if (!A || !eta) {
     set_error("NULL matrix or eta");
     return GSE_ERR_INVALID_ARG;
@@ -554,6 +561,7 @@ gse_status gse_perturbation_bounds(gse_matrix A, double* eta, void* stream) {
 }
 
 gse_status gse_spmv_f32acc(gse_matrix A, const float* x, float* y, int segments, void* stream) {
+  gse::NvtxRange nvtx_("gse_spmv_f32acc");
   if (!A || segments < 1 || segments > 3) {
     set_error("invalid matrix or segments (must be 1, 2 or 3)");
     return GSE_ERR_INVALID_ARG;
@@ -653,17 +661,20 @@ static gse_status solve_common(gse_matrix A, const double* b, double* x, double 
 
 gse_status gse_solve_cg(gse_matrix A, const double* b, double* x, double tol, int64_t max_iters,
                         const gse_step_schedule* sched, gse_solve_report* rep, void* stream) {
+  gse::NvtxRange nvtx_("gse_solve_cg");
   return solve_common(A, b, x, tol, max_iters, sched, 0, rep, stream, false);
 }
 
 gse_status gse_solve_gmres(gse_matrix A, const double* b, double* x, double tol, int restart,
                            int64_t max_iters, const gse_step_schedule* sched,
                            gse_solve_report* rep, void* stream) {
+  gse::NvtxRange nvtx_("gse_solve_gmres");
   return solve_common(A, b, x, tol, max_iters, sched, restart, rep, stream, true);
 }
 
 gse_status gse_encode_vector16(const double* v, int64_t n, int k_max, uint16_t* words,
                                uint16_t* table, int* table_len, void* stream) {
+  gse::NvtxRange nvtx_("gse_encode_vector16");
   if (n < 0 || (n > 0 && (!v || !words)) || !table || !table_len || k_max < 1 ||
       k_max > V16_KMAX || (k_max & (k_max - 1))) {
     set_error("invalid arguments (k_max a power of two in [1, 16], non-NULL arrays)");
@@ -708,6 +719,7 @@ gse_status gse_encode_vector16(const double* v, int64_t n, int k_max, uint16_t* 
 
 gse_status gse_decode_vector16(const uint16_t* words, int64_t n, const uint16_t* table,
                                int table_len, int ei_bits, double* out, void* stream) {
+  gse::NvtxRange nvtx_("gse_decode_vector16");
   if (n < 0 || (n > 0 && (!words || !out)) || (table_len > 0 && !table) || ei_bits < 0 ||
       ei_bits > 4 || table_len < 0 || table_len > (1 << ei_bits) || table_len > V16_KMAX) {
     set_error("invalid arguments (ei_bits in [0, 4], table_len <= 2^ei_bits)");

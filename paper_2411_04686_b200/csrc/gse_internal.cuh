@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only; no-ops unless a profiler injects a handler
 
 #include <cstdint>
 #include <cstdio>
@@ -12,6 +13,15 @@
 #include "../../include/gse.h"
 
 namespace gse {
+
+// NVTX range around each C-ABI call (encode, SpMV, solves) and marks at level switches, so
+// ncu --nvtx / nsys timelines attribute the kernels to the paper's operations
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ---------------------------------------------------------------- SpMV partition constants
 // A "warp block" (the unit one warp of the SpMV kernel processes) covers a run of

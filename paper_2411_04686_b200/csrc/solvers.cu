@@ -1534,6 +1534,9 @@ static void fill_sched(SolveCtrl* h, const gse_step_schedule& sc, int stepped, c
 }
 
 static void log_switch(gse_solve_report& rep, int64_t j, int lvl) {
+  char mark[64];  // NVTX mark on the profiler timeline
+  snprintf(mark, sizeof(mark), "gse level switch -> %d at iteration %lld", lvl, (long long)j);
+  nvtxMarkA(mark);
   if (rep.n_switches < 2) {
     rep.switch_iter[rep.n_switches] = j;
     rep.switch_to_level[rep.n_switches] = lvl;
